@@ -1,0 +1,145 @@
+/*
+ * eagercoll_b200 -- C ABI of the B200-native partial-collective engine
+ * (solo / majority / sync allreduce + the eager-SGD fold and update kernels).
+ *
+ * This is the drop-in boundary.  The reference (arXiv 1908.04207 artifact,
+ * /root/reference/pkg/src/eagercoll) is pure Python; its path is reached through
+ * `AllreduceHandle` (collectives.py:207-345) sitting on an `Engine`
+ * (schedule.py:178-465) that a transport pumps (transport.py:169-320).  Each
+ * entry point below replaces one reference operation, cited per function.
+ * The Python host package (paper_1908_04207_b200/) binds these with ctypes;
+ * INTEGRATION.md shows the binding.
+ *
+ * Conventions: plain pointers and sizes only; device pointers are CUDA device
+ * addresses; `stream` is a cudaStream_t passed as void* (NULL = legacy default
+ * stream).  Every function returns 0 on success or a negative EC_E* code, with a
+ * thread-local message in ec_last_error().  Element types: EC_F32 (the product
+ * path), EC_F64 and EC_I64 (the reference's "f8"/"i8", collectives.py:40).
+ * One ec_comm_t serves the local ranks of one collective instance (`cid`); a
+ * process normally holds one local rank per GPU, or all P ranks of an
+ * emulated world on one GPU.
+ */
+#ifndef EAGERCOLL_B200_H
+#define EAGERCOLL_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* element types (collectives.py:40 _ELEMENTS, plus fp32) */
+enum { EC_F32 = 0, EC_F64 = 1, EC_I64 = 2 };
+/* flavors (collectives.py:37) */
+enum { EC_SYNC = 0, EC_SOLO = 1, EC_MAJORITY = 2 };
+/* fold modes (eagersgd.py:55-57): COPY = stash was null (0 + grad), ADD = stash + grad */
+enum { EC_FOLD_COPY = 0, EC_FOLD_ADD = 1 };
+/* contribution flags */
+enum {
+  EC_CF_FRESH = 1,      /* set this rank's flag bit (collectives.py:304-306) */
+  EC_CF_ACTIVATE = 2,   /* activate after an accepted offer (eagersgd.py:162-163) */
+  EC_CF_ALL_ARRIVE = 4, /* bench: activate only once every rank has boarded */
+};
+/* request replies */
+enum {
+  EC_R_PENDING = 0, EC_R_ACCEPTED = 1, EC_R_REFUSED = 2, EC_R_OK = 3,
+  EC_R_POISONED = 4, EC_R_ERROR = 5
+};
+/* error codes */
+enum {
+  EC_OK = 0, EC_E_ARG = -1, EC_E_CUDA = -2, EC_E_TIMEOUT = -3, EC_E_STATE = -4,
+  EC_E_ORDER = -5, EC_E_DEVICE = -6, EC_E_NOMEM = -7
+};
+
+typedef struct ec_comm ec_comm_t;
+
+/* Library identity. */
+int ec_version(void);
+const char* ec_last_error(void);
+
+/* ---- communicator lifecycle ------------------------------------------------
+ * Replaces AllreduceHandle.__init__ + Engine(...) + commit()
+ * (collectives.py:218-235, schedule.py:186-273) for ranks
+ * [rank_lo, rank_lo + n_local) of a world of `world_size`.  Allocates per local
+ * rank: the peer-visible control block, the send/stash buffer (n_elems), a ring
+ * of `ring_slots` result slots, host-mapped request/reply/log pages.
+ * workers_per_rank = worker CTAs of the persistent engine per rank (0 = auto). */
+int ec_comm_create(int world_size, int rank_lo, int n_local, int device,
+                   int64_t n_elems, int dtype, int flavor, int ring_slots,
+                   int workers_per_rank, ec_comm_t** out);
+/* CUDA IPC handles of local rank `local_idx`'s buffers, for exchange over the
+ * process group at init (replaces transport.register_engine, transport.py:205-214). */
+int ec_comm_export(ec_comm_t* c, int local_idx, void* blob, size_t cap, size_t* len);
+/* Map a remote rank's buffers from its exported blob. */
+int ec_comm_import(ec_comm_t* c, int peer_rank, const void* blob, size_t len);
+/* Replay mode: force generation g's inclusion mask to masks[g] (g < n). */
+int ec_comm_set_replay(ec_comm_t* c, int local_idx, const uint64_t* masks, int64_t n);
+/* Start (or resume) the persistent engine kernel on the comm's own stream. */
+int ec_comm_start(ec_comm_t* c);
+/* Drain and stop the engine at a round boundary so device-wide syncs return;
+ * ec_comm_start resumes it with all protocol state preserved. */
+int ec_comm_pause(ec_comm_t* c, int timeout_ms);
+int ec_comm_destroy(ec_comm_t* c);
+int ec_comm_error(ec_comm_t* c, int local_idx, uint64_t* code, uint64_t* info);
+
+/* device addresses of the local rank's send buffer and of result slot `gen % R` */
+void* ec_send_ptr(ec_comm_t* c, int local_idx);
+void* ec_slot_ptr(ec_comm_t* c, int local_idx, int64_t gen);
+int64_t ec_n_elems(ec_comm_t* c);
+
+/* ---- application protocol -------------------------------------------------
+ * GradientBuffer.fold (eagersgd.py:55-57) into the send buffer, stream-ordered.
+ * Non-finite gradients set a poison flag that the next post turns into
+ * EC_R_POISONED (train_step's DivergenceError, eagersgd.py:145-147). */
+int ec_fold(ec_comm_t* c, int local_idx, const void* grad, int mode, void* stream);
+/* np.copyto(send, vec) of try_contribute (collectives.py:301-303), stream-ordered. */
+int ec_copy_in(ec_comm_t* c, int local_idx, const void* src, void* stream);
+/* try_contribute(t, ..., fresh) [+ activate(t)] (collectives.py:291-317), posted
+ * in stream order after the fold/copy; *seq identifies the reply. */
+int ec_post_contribute(ec_comm_t* c, int local_idx, int64_t t, uint32_t flags,
+                       void* stream, uint64_t* seq);
+/* activate(t) (collectives.py:311-317), posted from the host. */
+int ec_post_activate(ec_comm_t* c, int local_idx, int64_t t, uint64_t* seq);
+/* staleness guard (eagersgd.py:89-110): generations >= hold_from are held
+ * until this rank contributes; INT64_MAX disables. */
+int ec_post_hold(ec_comm_t* c, int local_idx, int64_t hold_from, uint64_t* seq);
+/* Reply to request `seq` (EC_R_*), waiting up to timeout_ms (0 = poll once). */
+int ec_reply(ec_comm_t* c, int local_idx, uint64_t seq, int timeout_ms, int* status);
+/* done_generation (collectives.py:278-289); -1 before the first round. */
+int ec_done_gen(ec_comm_t* c, int local_idx, int64_t* gen);
+/* wait_done / wait_blocking (collectives.py:319-332): block until a generation
+ * >= t completed, return the latest one with its mask and nap.  pin != 0 pins
+ * its result slot against reuse until ec_set_pin releases it. */
+int ec_wait(ec_comm_t* c, int local_idx, int64_t t, int timeout_ms, int pin,
+            int64_t* gen, uint64_t* mask, int* nap);
+/* Mask / nap of an earlier generation from the device log (RoundRecord source). */
+int ec_gen_info(ec_comm_t* c, int local_idx, int64_t gen, uint64_t* mask,
+                uint64_t* has_data, int* nap);
+/* Lowest generation the host may still read: the engine never overwrites the
+ * slot of generation h unless h < pin_lo.  ordered != 0 performs the store in
+ * `stream` order (release after the update kernel read the slot); ordered == 0
+ * stores from the host immediately. */
+int ec_set_pin(ec_comm_t* c, int local_idx, uint64_t pin_lo, int ordered, void* stream);
+
+/* ---- standalone sm_100a kernels (no communicator) --------------------------- */
+/* stash (+)= grad: mode COPY writes 0+grad, ADD writes stash+grad (eagersgd.py:56). */
+int ec_fold_raw(void* stash, const void* grad, int64_t n, int dtype, int mode,
+                uint32_t* nonfinite_flag, void* stream);
+/* w = w - lr*u, two roundings, no FMA (eagersgd.py:165). */
+int ec_sgd_update(void* w, const void* u, double lr, int64_t n, int dtype, void* stream);
+/* buf = mu*buf + u ; w = w - lr*buf (opt-in momentum; mu == 0 is plain SGD). */
+int ec_momentum_update(void* w, void* buf, const void* u, double lr, double mu,
+                       int64_t n, int dtype, void* stream);
+/* tree_order_sum (collectives.py:385-403) of p device vectors in the engine's
+ * snapshot semantics (0+x leaves, has_mask bit clear = null), optionally / p
+ * (collectives.py:254-260).  srcs is a HOST array of p device pointers. */
+int ec_local_reduce(const void* const* srcs, int p, uint64_t has_mask, void* dst,
+                    int64_t n, int dtype, int divide, void* stream);
+/* Device-side imbalance injection (transport.py:137-149): spin for ns. */
+int ec_spin(uint64_t ns, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* EAGERCOLL_B200_H */

@@ -1,0 +1,22 @@
+"""eagercoll on B200: partial collectives (solo / majority allreduce) and eager-SGD.
+
+A from-scratch sm_100a implementation of the hot path of arXiv 1908.04207's
+reference package `eagercoll`, behind the same Python API.  See DESIGN.md.
+
+    from paper_1908_04207_b200 import (CollectiveConfig, AllreduceHandle,
+                                       EmulatedWorld, ProcessWorld, train_step)
+"""
+
+__version__ = "0.1.0"
+
+from .collectives import (  # noqa: E402,F401
+    FLAVORS, MAJORITY, SOLO, SYNC, AllreduceHandle, CollectiveConfig, CollectiveResult,
+    ceil_log2, drive, floor_pow2, initiator_for_round, run_allreduce, tree_order_sum,
+)
+from .eagersgd import (  # noqa: E402,F401
+    DivergenceError, GradientBuffer, TrainState, attach_delivery_tracking, resync_models,
+    resync_step, staleness_guard, train_step, training_process,
+)
+from .trace import TraceRecorder  # noqa: E402,F401
+from .transport import DelayModel, Sleep, delayed_ranks, inject_delay  # noqa: E402,F401
+from .world import EmulatedWorld, ProcessWorld  # noqa: E402,F401

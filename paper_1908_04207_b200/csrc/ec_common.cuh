@@ -1,0 +1,172 @@
+// Shared layouts and PTX helpers of the eagercoll_b200 engine (sm_100a).
+//
+// Memory map per rank:
+//   EcCtrl     device memory, IPC-mapped by every peer.  Peers WRITE their
+//              per-source words here (activation, snapshot, shard-ready,
+//              arrival), so every wait is a poll of local HBM/L2.
+//   EcLocal    device memory, private to the rank's engine CTAs (round command,
+//              worker counters, controller state saved across pause/resume).
+//   EcHostCtl  pinned, host-mapped: request ring (host/stream -> engine),
+//              replies, done generation and per-generation mask log
+//              (engine -> host), pin and stop words (host -> engine).
+//   send       the rank's contribution / eager-SGD stash (n elements).
+//   ring       R result slots of n elements; slot g % R holds u of generation g.
+#pragma once
+#include <stdint.h>
+
+#define EC_MAX_P 64
+#define EC_REQ_RING 1024
+#define EC_LOG_RING 4096
+#define EC_INF_GEN 0x7fffffffffffffffLL
+
+// request types
+#define EC_REQ_CONTRIB 1
+#define EC_REQ_ACTIVATE 2
+#define EC_REQ_HOLD 3
+// internal contribution flag (set by the post kernel from the fold's poison word)
+#define EC_CF_POISON 0x100
+
+// snapshot word: ((gen+1) << 2) | has_data << 1 | fresh
+#define EC_SNAP_FRESH 1ull
+#define EC_SNAP_DATA 2ull
+
+// device error codes (EcHostCtl::error)
+#define EC_DERR_ORDER 1      // contribution for a future generation
+#define EC_DERR_TIMEOUT 2    // watchdog expired inside a round
+#define EC_DERR_REPLAY 3     // replay table exhausted / inconsistent
+
+struct alignas(128) EcCtrl {
+  unsigned long long act_from[EC_MAX_P];     // gen+1 activated by source rank
+  unsigned long long snap_from[EC_MAX_P];    // snapshot word of source rank
+  unsigned long long rsdone_from[EC_MAX_P];  // gen+1: source's reduced shard ready
+  unsigned long long arrive_from[EC_MAX_P];  // gen+1: source boarded (all-arrive)
+};
+
+struct alignas(128) EcLocal {
+  // round command: controller -> workers
+  unsigned long long cmd_seq;      // incremented per round; ~0ull = exit
+  long long cmd_gen;
+  unsigned long long cmd_has;      // has-data mask of the round
+  unsigned long long exit_epoch;   // workers of launch `epoch` exit when this equals it
+  unsigned long long pad0[4];
+  unsigned long long rs_count;     // worker CTAs finished reduce-scatter (monotone)
+  unsigned long long pad1[7];
+  unsigned long long ag_count;     // worker CTAs finished all-gather (monotone)
+  unsigned long long pad2[7];
+  unsigned long long round_done;   // last cmd_seq fully done
+  unsigned long long pad3[7];
+  // controller state (persisted across pause/resume)
+  long long g;                     // current generation
+  long long hold_from;
+  long long contributed_round;
+  unsigned long long next_req;
+  int snapped;
+  int contrib;                     // EC_SNAP_* bits of the accepted offer
+  int internal_act;
+  int arrive_pending;              // all-arrive: activate once everyone boarded
+  int arrive_activate;
+  int initialized;
+  unsigned int poison;             // fold's non-finite flag (device word)
+  int pad4;
+};
+
+struct alignas(64) EcReq {
+  unsigned long long seq1;   // request sequence + 1; written last (release)
+  unsigned int type;
+  unsigned int flags;
+  long long t;
+  long long arg;
+  unsigned long long pad[4];
+};
+
+struct alignas(32) EcLog {
+  unsigned long long gen1;
+  unsigned long long mask;
+  unsigned long long has;
+  unsigned long long nap;
+};
+
+struct alignas(128) EcHostCtl {
+  unsigned long long stop;          // host -> engine: drain and exit
+  unsigned long long pin_lo;        // host -> engine
+  unsigned long long pad0[14];
+  unsigned long long done_gen1;     // engine -> host: last completed generation + 1
+  unsigned long long req_done;      // engine -> host: requests consumed
+  unsigned long long error;
+  unsigned long long error_info;
+  unsigned long long exited;        // engine -> host: controller parked (pause ack)
+  unsigned long long snap_gen1;     // engine -> host: last snapshotted generation + 1
+  unsigned long long pad1[10];
+  EcReq req[EC_REQ_RING];
+  unsigned long long reply[EC_REQ_RING];   // ((seq+1) << 8) | status
+  EcLog log[EC_LOG_RING];
+};
+
+struct EcDesc {
+  int rank, P, flavor, dtype;
+  int R, W, replay, vec;              // ring slots, worker CTAs, replay flag, elems / 16 B
+  long long n, nvec;                  // elements, whole 16-B vectors
+  long long slot_bytes;
+  long long n_forced;
+  unsigned long long timeout_ns;      // in-round watchdog
+  EcCtrl* ctrl[EC_MAX_P];
+  char* send[EC_MAX_P];
+  char* ring[EC_MAX_P];
+  EcHostCtl* hctl;
+  EcLocal* local;
+  const unsigned long long* forced;
+};
+
+// ----------------------------------------------------------------------------
+// PTX helpers.  Cross-GPU and host-visible words use .sys scope; engine-internal
+// counters use .gpu scope.  Data moved between rounds is read with ld.cg (L2
+// only) so no SM ever serves a stale L1 line of a reused slot.
+
+__device__ __forceinline__ unsigned long long ld_acquire_sys(const unsigned long long* p) {
+  unsigned long long v;
+  asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ unsigned long long ld_acquire_gpu(const unsigned long long* p) {
+  unsigned long long v;
+  asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ unsigned long long ld_relaxed_sys(const unsigned long long* p) {
+  unsigned long long v;
+  asm volatile("ld.relaxed.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_release_sys(unsigned long long* p, unsigned long long v) {
+  asm volatile("st.release.sys.global.u64 [%0], %1;" :: "l"(p), "l"(v) : "memory");
+}
+__device__ __forceinline__ void st_release_gpu(unsigned long long* p, unsigned long long v) {
+  asm volatile("st.release.gpu.global.u64 [%0], %1;" :: "l"(p), "l"(v) : "memory");
+}
+__device__ __forceinline__ void st_relaxed_sys(unsigned long long* p, unsigned long long v) {
+  asm volatile("st.relaxed.sys.global.u64 [%0], %1;" :: "l"(p), "l"(v) : "memory");
+}
+__device__ __forceinline__ void fence_sc_sys() { asm volatile("fence.sc.sys;" ::: "memory"); }
+__device__ __forceinline__ void fence_acq_rel_sys() { asm volatile("fence.acq_rel.sys;" ::: "memory"); }
+
+__device__ __forceinline__ uint4 ld_cg_v4(const void* p) {
+  uint4 v;
+  asm volatile("ld.global.cg.v4.u32 {%0,%1,%2,%3}, [%4];"
+               : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_v4(void* p, uint4 v) {
+  asm volatile("st.global.v4.u32 [%0], {%1,%2,%3,%4};"
+               :: "l"(p), "r"(v.x), "r"(v.y), "r"(v.z), "r"(v.w) : "memory");
+}
+__device__ __forceinline__ uint4 ld_stream_v4(const void* p) {
+  uint4 v;
+  asm volatile("ld.global.L1::no_allocate.v4.u32 {%0,%1,%2,%3}, [%4];"
+               : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "l"(p));
+  return v;
+}
+__device__ __forceinline__ unsigned long long globaltimer_ns() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}

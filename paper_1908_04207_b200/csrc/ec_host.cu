@@ -1,0 +1,618 @@
+// Host side of the eagercoll_b200 C ABI: communicator, IPC peer mapping,
+// request ring, waits and launches.  See include/eagercoll_b200.h.
+#include <cuda_runtime.h>
+#include <errno.h>
+#include <immintrin.h>
+#include <sched.h>
+#include <stdarg.h>
+#include <stdio.h>
+#include <stdlib.h>
+#include <string.h>
+#include <time.h>
+
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include "../../include/eagercoll_b200.h"
+#include "ec_common.cuh"
+
+// launchers (ec_kernels.cu)
+cudaError_t launch_engine(int dtype, const EcDesc* d_descs, int n_local, int blocks_per_rank,
+                          unsigned long long epoch, cudaStream_t s);
+cudaError_t launch_fold(int dtype, void* stash, const void* grad, long long n, int mode,
+                        unsigned int* nonfinite, cudaStream_t s);
+cudaError_t launch_update(int dtype, void* w, const void* u, double lr, long long n, cudaStream_t s);
+cudaError_t launch_momentum(int dtype, void* w, void* buf, const void* u, double lr, double mu,
+                            long long n, cudaStream_t s);
+cudaError_t launch_reduce(int dtype, const void* const* srcs, int p, unsigned long long has,
+                          void* dst, long long n, int div, cudaStream_t s);
+cudaError_t launch_post(EcReq* rec, unsigned long long seq1, unsigned int type, unsigned int flags,
+                        long long t, long long arg, unsigned int* poison, cudaStream_t s);
+cudaError_t launch_write_u64(unsigned long long* p, unsigned long long v, cudaStream_t s);
+cudaError_t launch_spin(unsigned long long ns, cudaStream_t s);
+
+#define EC_VERSION 10000
+#define BLOB_MAGIC 0x45434231u  // "ECB1"
+
+static thread_local std::string g_err;
+
+static int fail(int code, const char* fmt, ...) {
+  char buf[512];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof(buf), fmt, ap);
+  va_end(ap);
+  g_err = buf;
+  return code;
+}
+
+#define CK(call)                                                                        \
+  do {                                                                                  \
+    cudaError_t e_ = (call);                                                            \
+    if (e_ != cudaSuccess)                                                              \
+      return fail(EC_E_CUDA, "%s: %s (%s:%d)", #call, cudaGetErrorString(e_), __FILE__, \
+                  __LINE__);                                                            \
+  } while (0)
+
+static inline unsigned long long now_ns() {
+  struct timespec ts;
+  clock_gettime(CLOCK_MONOTONIC, &ts);
+  return (unsigned long long)ts.tv_sec * 1000000000ull + ts.tv_nsec;
+}
+
+template <typename T>
+static inline T aload(const T* p) { return __atomic_load_n(p, __ATOMIC_ACQUIRE); }
+template <typename T>
+static inline void astore(T* p, T v) { __atomic_store_n(p, v, __ATOMIC_RELEASE); }
+
+// Spin, then back off: tight for the first ~50 us (latency of a round), then yield.
+struct Backoff {
+  unsigned long long t0 = now_ns();
+  unsigned it = 0;
+  void pause() {
+    ++it;
+    if (it < 2000) {
+      _mm_pause();
+    } else if (it < 20000) {
+      sched_yield();
+    } else {
+      struct timespec ts = {0, 20000};
+      nanosleep(&ts, nullptr);
+    }
+  }
+  bool expired(int timeout_ms) const {
+    return timeout_ms >= 0 && now_ns() - t0 > (unsigned long long)timeout_ms * 1000000ull;
+  }
+};
+
+struct EcRankHost {
+  int rank = -1;
+  EcCtrl* ctrl = nullptr;
+  char* send = nullptr;
+  char* ring = nullptr;
+  EcHostCtl* h = nullptr;      // host view
+  EcHostCtl* hd = nullptr;     // device view of the same pinned page
+  EcLocal* local = nullptr;
+  unsigned long long* forced = nullptr;
+  long long n_forced = 0;
+  unsigned long long next_seq = 0;
+  std::mutex mu;
+};
+
+struct BlobV1 {
+  unsigned magic;
+  int rank;
+  long long n;
+  int dtype, R;
+  cudaIpcMemHandle_t ctrl, send, ring;
+};
+
+struct ec_comm {
+  int P = 0, rank_lo = 0, n_local = 0, device = 0, dtype = 0, flavor = 0, R = 2, W = 0;
+  long long n = 0, slot_bytes = 0;
+  int elem = 4;
+  unsigned long long timeout_ns = 60ull * 1000000000ull;
+  std::vector<EcRankHost*> L;
+  std::vector<EcCtrl*> ctrl;
+  std::vector<char*> send, ring;
+  std::vector<int> opened;  // 1 = IPC-opened peer
+  EcDesc* d_descs = nullptr;
+  cudaStream_t es = nullptr;
+  bool running = false;
+  unsigned long long epoch = 0;
+};
+
+static int check_li(ec_comm_t* c, int li) {
+  if (!c) return fail(EC_E_ARG, "null communicator");
+  if (li < 0 || li >= c->n_local) return fail(EC_E_ARG, "local index %d out of range", li);
+  return EC_OK;
+}
+
+static int device_error(EcRankHost* r) {
+  unsigned long long e = aload(&r->h->error);
+  if (e) {
+    return fail(EC_E_DEVICE, "engine error %llu (info 0x%llx) at rank %d", e,
+                aload(&r->h->error_info), r->rank);
+  }
+  return EC_OK;
+}
+
+extern "C" {
+
+int ec_version(void) { return EC_VERSION; }
+const char* ec_last_error(void) { return g_err.c_str(); }
+
+int ec_comm_create(int world_size, int rank_lo, int n_local, int device, int64_t n_elems,
+                   int dtype, int flavor, int ring_slots, int workers_per_rank, ec_comm_t** out) {
+  if (!out) return fail(EC_E_ARG, "out is null");
+  *out = nullptr;
+  if (world_size < 1 || world_size > EC_MAX_P)
+    return fail(EC_E_ARG, "world_size must be in [1, %d]", EC_MAX_P);
+  if (n_local < 1 || rank_lo < 0 || rank_lo + n_local > world_size)
+    return fail(EC_E_ARG, "bad local rank range [%d, %d)", rank_lo, rank_lo + n_local);
+  if (n_elems < 1) return fail(EC_E_ARG, "n_elems must be >= 1");
+  if (dtype < EC_F32 || dtype > EC_I64) return fail(EC_E_ARG, "bad dtype %d", dtype);
+  if (flavor < EC_SYNC || flavor > EC_MAJORITY) return fail(EC_E_ARG, "bad flavor %d", flavor);
+  if (ring_slots < 2) return fail(EC_E_ARG, "ring_slots must be >= 2");
+  CK(cudaSetDevice(device));
+  ec_comm* c = new ec_comm();
+  c->P = world_size;
+  c->rank_lo = rank_lo;
+  c->n_local = n_local;
+  c->device = device;
+  c->dtype = dtype;
+  c->flavor = flavor;
+  c->R = ring_slots;
+  c->n = n_elems;
+  c->elem = dtype == EC_F32 ? 4 : 8;
+  c->slot_bytes = ((n_elems * c->elem + 255) / 256) * 256;
+  if (workers_per_rank <= 0) {
+    const char* env = getenv("EC_WORKERS");
+    workers_per_rank = env ? atoi(env) : 0;
+  }
+  if (workers_per_rank <= 0) {
+    workers_per_rank = n_local == 1 ? 64 : (144 / n_local) - 1;
+    if (workers_per_rank > 16) workers_per_rank = 16;
+    if (workers_per_rank < 1) workers_per_rank = 1;
+  }
+  c->W = workers_per_rank;
+  if (const char* env = getenv("EC_TIMEOUT_S")) c->timeout_ns = (unsigned long long)(atof(env) * 1e9);
+  c->ctrl.assign(world_size, nullptr);
+  c->send.assign(world_size, nullptr);
+  c->ring.assign(world_size, nullptr);
+  c->opened.assign(world_size, 0);
+  for (int i = 0; i < n_local; ++i) {
+    EcRankHost* r = new EcRankHost();
+    r->rank = rank_lo + i;
+    c->L.push_back(r);
+    cudaError_t e;
+    if ((e = cudaMalloc(&r->ctrl, sizeof(EcCtrl))) != cudaSuccess ||
+        (e = cudaMalloc(&r->send, c->slot_bytes)) != cudaSuccess ||
+        (e = cudaMalloc(&r->ring, c->slot_bytes * c->R)) != cudaSuccess ||
+        (e = cudaMalloc(&r->local, sizeof(EcLocal))) != cudaSuccess ||
+        (e = cudaMemset(r->ctrl, 0, sizeof(EcCtrl))) != cudaSuccess ||
+        (e = cudaMemset(r->send, 0, c->slot_bytes)) != cudaSuccess ||
+        (e = cudaMemset(r->ring, 0, c->slot_bytes * c->R)) != cudaSuccess ||
+        (e = cudaHostAlloc(&r->h, sizeof(EcHostCtl), cudaHostAllocMapped | cudaHostAllocPortable)) != cudaSuccess) {
+      ec_comm_destroy(c);
+      return fail(EC_E_NOMEM, "allocation failed: %s", cudaGetErrorString(e));
+    }
+    memset((void*)r->h, 0, sizeof(EcHostCtl));
+    r->h->pin_lo = ~0ull;
+    if ((e = cudaHostGetDevicePointer((void**)&r->hd, r->h, 0)) != cudaSuccess) {
+      ec_comm_destroy(c);
+      return fail(EC_E_CUDA, "cudaHostGetDevicePointer: %s", cudaGetErrorString(e));
+    }
+    EcLocal init;
+    memset(&init, 0, sizeof(init));
+    init.hold_from = EC_INF_GEN;
+    init.contributed_round = -1;
+    if ((e = cudaMemcpy(r->local, &init, sizeof(init), cudaMemcpyHostToDevice)) != cudaSuccess) {
+      ec_comm_destroy(c);
+      return fail(EC_E_CUDA, "init local: %s", cudaGetErrorString(e));
+    }
+    c->ctrl[r->rank] = r->ctrl;
+    c->send[r->rank] = r->send;
+    c->ring[r->rank] = r->ring;
+  }
+  if (cudaMalloc(&c->d_descs, sizeof(EcDesc) * n_local) != cudaSuccess) {
+    ec_comm_destroy(c);
+    return fail(EC_E_NOMEM, "descriptor allocation failed");
+  }
+  int lo = 0, hi = 0;
+  cudaDeviceGetStreamPriorityRange(&lo, &hi);
+  if (cudaStreamCreateWithPriority(&c->es, cudaStreamNonBlocking, hi) != cudaSuccess) {
+    ec_comm_destroy(c);
+    return fail(EC_E_CUDA, "engine stream creation failed");
+  }
+  *out = c;
+  return EC_OK;
+}
+
+int ec_comm_export(ec_comm_t* c, int li, void* blob, size_t cap, size_t* len) {
+  int rc = check_li(c, li);
+  if (rc) return rc;
+  if (!blob || cap < sizeof(BlobV1)) return fail(EC_E_ARG, "blob buffer too small (%zu)", sizeof(BlobV1));
+  EcRankHost* r = c->L[li];
+  BlobV1 b;
+  memset(&b, 0, sizeof(b));
+  b.magic = BLOB_MAGIC;
+  b.rank = r->rank;
+  b.n = c->n;
+  b.dtype = c->dtype;
+  b.R = c->R;
+  CK(cudaSetDevice(c->device));
+  CK(cudaIpcGetMemHandle(&b.ctrl, r->ctrl));
+  CK(cudaIpcGetMemHandle(&b.send, r->send));
+  CK(cudaIpcGetMemHandle(&b.ring, r->ring));
+  memcpy(blob, &b, sizeof(b));
+  if (len) *len = sizeof(b);
+  return EC_OK;
+}
+
+int ec_comm_import(ec_comm_t* c, int peer, const void* blob, size_t len) {
+  if (!c) return fail(EC_E_ARG, "null communicator");
+  if (peer < 0 || peer >= c->P) return fail(EC_E_ARG, "peer %d out of range", peer);
+  if (peer >= c->rank_lo && peer < c->rank_lo + c->n_local) return EC_OK;  // local rank
+  if (!blob || len < sizeof(BlobV1)) return fail(EC_E_ARG, "blob too short");
+  BlobV1 b;
+  memcpy(&b, blob, sizeof(b));
+  if (b.magic != BLOB_MAGIC || b.rank != peer)
+    return fail(EC_E_ARG, "blob is not rank %d's (magic %x rank %d)", peer, b.magic, b.rank);
+  if (b.n != c->n || b.dtype != c->dtype || b.R != c->R)
+    return fail(EC_E_ARG, "peer %d geometry mismatch (n %lld/%lld dtype %d/%d R %d/%d)", peer,
+                b.n, c->n, b.dtype, c->dtype, b.R, c->R);
+  if (c->opened[peer]) return EC_OK;
+  CK(cudaSetDevice(c->device));
+  void *pc = nullptr, *ps = nullptr, *pr = nullptr;
+  CK(cudaIpcOpenMemHandle(&pc, b.ctrl, cudaIpcMemLazyEnablePeerAccess));
+  CK(cudaIpcOpenMemHandle(&ps, b.send, cudaIpcMemLazyEnablePeerAccess));
+  CK(cudaIpcOpenMemHandle(&pr, b.ring, cudaIpcMemLazyEnablePeerAccess));
+  c->ctrl[peer] = (EcCtrl*)pc;
+  c->send[peer] = (char*)ps;
+  c->ring[peer] = (char*)pr;
+  c->opened[peer] = 1;
+  return EC_OK;
+}
+
+int ec_comm_set_replay(ec_comm_t* c, int li, const uint64_t* masks, int64_t n) {
+  int rc = check_li(c, li);
+  if (rc) return rc;
+  if (c->running) return fail(EC_E_STATE, "set_replay while the engine runs");
+  EcRankHost* r = c->L[li];
+  CK(cudaSetDevice(c->device));
+  if (r->forced) {
+    cudaFree(r->forced);
+    r->forced = nullptr;
+  }
+  r->n_forced = 0;
+  if (n > 0) {
+    CK(cudaMalloc(&r->forced, sizeof(unsigned long long) * n));
+    CK(cudaMemcpy(r->forced, masks, sizeof(unsigned long long) * n, cudaMemcpyHostToDevice));
+    r->n_forced = n;
+  }
+  return EC_OK;
+}
+
+int ec_comm_start(ec_comm_t* c) {
+  if (!c) return fail(EC_E_ARG, "null communicator");
+  if (c->running) return EC_OK;
+  for (int q = 0; q < c->P; ++q)
+    if (!c->ctrl[q]) return fail(EC_E_STATE, "rank %d's buffers are not mapped (import first)", q);
+  CK(cudaSetDevice(c->device));
+  std::vector<EcDesc> d(c->n_local);
+  const int V = 16 / c->elem;
+  for (int i = 0; i < c->n_local; ++i) {
+    EcRankHost* r = c->L[i];
+    EcDesc& x = d[i];
+    memset(&x, 0, sizeof(x));
+    x.rank = r->rank;
+    x.P = c->P;
+    x.flavor = c->flavor;
+    x.dtype = c->dtype;
+    x.R = c->R;
+    x.W = c->W;
+    x.replay = r->forced != nullptr;
+    x.vec = V;
+    x.n = c->n;
+    x.nvec = c->n / V;
+    x.slot_bytes = c->slot_bytes;
+    x.n_forced = r->n_forced;
+    x.timeout_ns = c->timeout_ns;
+    for (int q = 0; q < c->P; ++q) {
+      x.ctrl[q] = c->ctrl[q];
+      x.send[q] = c->send[q];
+      x.ring[q] = c->ring[q];
+    }
+    x.hctl = r->hd;
+    x.local = r->local;
+    x.forced = r->forced;
+    astore(&r->h->stop, 0ull);
+  }
+  CK(cudaMemcpy(c->d_descs, d.data(), sizeof(EcDesc) * c->n_local, cudaMemcpyHostToDevice));
+  c->epoch += 1;
+  CK(launch_engine(c->dtype, c->d_descs, c->n_local, 1 + c->W, c->epoch, c->es));
+  c->running = true;
+  return EC_OK;
+}
+
+int ec_comm_pause(ec_comm_t* c, int timeout_ms) {
+  if (!c) return fail(EC_E_ARG, "null communicator");
+  if (!c->running) return EC_OK;
+  for (EcRankHost* r : c->L) astore(&r->h->stop, 1ull);
+  Backoff bo;
+  for (EcRankHost* r : c->L) {
+    while (aload(&r->h->exited) != c->epoch) {
+      if (bo.expired(timeout_ms))
+        return fail(EC_E_TIMEOUT, "engine of rank %d did not park within %d ms", r->rank, timeout_ms);
+      bo.pause();
+    }
+  }
+  CK(cudaSetDevice(c->device));
+  CK(cudaStreamSynchronize(c->es));
+  c->running = false;
+  for (EcRankHost* r : c->L) astore(&r->h->stop, 0ull);
+  return EC_OK;
+}
+
+int ec_comm_destroy(ec_comm_t* c) {
+  if (!c) return EC_OK;
+  int rc = EC_OK;
+  cudaSetDevice(c->device);
+  if (c->running) rc = ec_comm_pause(c, 10000);
+  if (c->running) {
+    // the engine did not park: do not free memory a live kernel still touches
+    return fail(EC_E_STATE, "engine still running; communicator leaked");
+  }
+  for (int q = 0; q < c->P; ++q) {
+    if (c->opened[q]) {
+      cudaIpcCloseMemHandle(c->ctrl[q]);
+      cudaIpcCloseMemHandle(c->send[q]);
+      cudaIpcCloseMemHandle(c->ring[q]);
+    }
+  }
+  for (EcRankHost* r : c->L) {
+    if (r->ctrl) cudaFree(r->ctrl);
+    if (r->send) cudaFree(r->send);
+    if (r->ring) cudaFree(r->ring);
+    if (r->local) cudaFree(r->local);
+    if (r->forced) cudaFree(r->forced);
+    if (r->h) cudaFreeHost(r->h);
+    delete r;
+  }
+  if (c->d_descs) cudaFree(c->d_descs);
+  if (c->es) cudaStreamDestroy(c->es);
+  delete c;
+  return rc;
+}
+
+int ec_comm_error(ec_comm_t* c, int li, uint64_t* code, uint64_t* info) {
+  int rc = check_li(c, li);
+  if (rc) return rc;
+  if (code) *code = aload(&c->L[li]->h->error);
+  if (info) *info = aload(&c->L[li]->h->error_info);
+  return EC_OK;
+}
+
+void* ec_send_ptr(ec_comm_t* c, int li) {
+  if (check_li(c, li)) return nullptr;
+  return c->L[li]->send;
+}
+
+void* ec_slot_ptr(ec_comm_t* c, int li, int64_t gen) {
+  if (check_li(c, li) || gen < 0) return nullptr;
+  return c->L[li]->ring + (gen % c->R) * c->slot_bytes;
+}
+
+int64_t ec_n_elems(ec_comm_t* c) { return c ? c->n : -1; }
+
+int ec_fold(ec_comm_t* c, int li, const void* grad, int mode, void* stream) {
+  int rc = check_li(c, li);
+  if (rc) return rc;
+  if (!grad) return fail(EC_E_ARG, "null gradient");
+  EcRankHost* r = c->L[li];
+  CK(launch_fold(c->dtype, r->send, grad, c->n, mode, &r->local->poison, (cudaStream_t)stream));
+  return EC_OK;
+}
+
+int ec_copy_in(ec_comm_t* c, int li, const void* src, void* stream) {
+  int rc = check_li(c, li);
+  if (rc) return rc;
+  EcRankHost* r = c->L[li];
+  if (src != r->send)
+    CK(cudaMemcpyAsync(r->send, src, c->n * c->elem, cudaMemcpyDeviceToDevice, (cudaStream_t)stream));
+  return EC_OK;
+}
+
+static int reserve_seq(ec_comm_t* c, EcRankHost* r, unsigned long long* seq) {
+  Backoff bo;
+  while (r->next_seq - aload(&r->h->req_done) >= EC_REQ_RING) {
+    if (bo.expired(60000)) return fail(EC_E_TIMEOUT, "request ring full at rank %d", r->rank);
+    int e = device_error(r);
+    if (e) return e;
+    bo.pause();
+  }
+  *seq = r->next_seq++;
+  (void)c;
+  return EC_OK;
+}
+
+static int host_post(ec_comm_t* c, int li, unsigned type, unsigned flags, long long t, long long arg,
+                     uint64_t* seq_out) {
+  int rc = check_li(c, li);
+  if (rc) return rc;
+  EcRankHost* r = c->L[li];
+  std::lock_guard<std::mutex> g(r->mu);
+  unsigned long long seq;
+  if ((rc = reserve_seq(c, r, &seq))) return rc;
+  EcReq* q = &r->h->req[seq % EC_REQ_RING];
+  q->type = type;
+  q->flags = flags;
+  q->t = t;
+  q->arg = arg;
+  __atomic_thread_fence(__ATOMIC_SEQ_CST);
+  astore(&q->seq1, seq + 1);
+  if (seq_out) *seq_out = seq;
+  return EC_OK;
+}
+
+int ec_post_contribute(ec_comm_t* c, int li, int64_t t, uint32_t flags, void* stream, uint64_t* seq_out) {
+  int rc = check_li(c, li);
+  if (rc) return rc;
+  EcRankHost* r = c->L[li];
+  std::lock_guard<std::mutex> g(r->mu);
+  unsigned long long seq;
+  if ((rc = reserve_seq(c, r, &seq))) return rc;
+  EcReq* dq = &r->hd->req[seq % EC_REQ_RING];
+  CK(launch_post(dq, seq + 1, EC_REQ_CONTRIB, flags & 7u, t, 0, &r->local->poison, (cudaStream_t)stream));
+  if (seq_out) *seq_out = seq;
+  return EC_OK;
+}
+
+int ec_post_activate(ec_comm_t* c, int li, int64_t t, uint64_t* seq) {
+  return host_post(c, li, EC_REQ_ACTIVATE, 0, t, 0, seq);
+}
+
+int ec_post_hold(ec_comm_t* c, int li, int64_t hold_from, uint64_t* seq) {
+  return host_post(c, li, EC_REQ_HOLD, 0, 0, hold_from, seq);
+}
+
+int ec_reply(ec_comm_t* c, int li, uint64_t seq, int timeout_ms, int* status) {
+  int rc = check_li(c, li);
+  if (rc) return rc;
+  EcRankHost* r = c->L[li];
+  Backoff bo;
+  while (true) {
+    unsigned long long v = aload(&r->h->reply[seq % EC_REQ_RING]);
+    if ((v >> 8) == seq + 1) {
+      if (status) *status = (int)(v & 0xff);
+      return EC_OK;
+    }
+    if (timeout_ms == 0) {
+      if (status) *status = EC_R_PENDING;
+      return EC_OK;
+    }
+    if ((rc = device_error(r))) return rc;
+    if (bo.expired(timeout_ms))
+      return fail(EC_E_TIMEOUT, "rank %d: no reply to request %llu within %d ms", r->rank,
+                  (unsigned long long)seq, timeout_ms);
+    bo.pause();
+  }
+}
+
+int ec_done_gen(ec_comm_t* c, int li, int64_t* gen) {
+  int rc = check_li(c, li);
+  if (rc) return rc;
+  if (gen) *gen = (int64_t)aload(&c->L[li]->h->done_gen1) - 1;
+  return EC_OK;
+}
+
+int ec_gen_info(ec_comm_t* c, int li, int64_t gen, uint64_t* mask, uint64_t* has, int* nap) {
+  int rc = check_li(c, li);
+  if (rc) return rc;
+  EcRankHost* r = c->L[li];
+  if (gen < 0 || (long long)aload(&r->h->done_gen1) <= gen)
+    return fail(EC_E_STATE, "generation %lld has not completed", (long long)gen);
+  EcLog* lg = &r->h->log[gen % EC_LOG_RING];
+  unsigned long long g1 = aload(&lg->gen1);
+  unsigned long long m = aload(&lg->mask), hm = aload(&lg->has), np = aload(&lg->nap);
+  __atomic_thread_fence(__ATOMIC_ACQUIRE);
+  if (aload(&lg->gen1) != g1 || g1 != (unsigned long long)gen + 1)
+    return fail(EC_E_STATE, "generation %lld fell out of the %d-entry log", (long long)gen, EC_LOG_RING);
+  if (mask) *mask = m;
+  if (has) *has = hm;
+  if (nap) *nap = (int)np;
+  return EC_OK;
+}
+
+int ec_wait(ec_comm_t* c, int li, int64_t t, int timeout_ms, int pin, int64_t* gen_out,
+            uint64_t* mask, int* nap) {
+  int rc = check_li(c, li);
+  if (rc) return rc;
+  EcRankHost* r = c->L[li];
+  Backoff bo;
+  unsigned long long d1;
+  while ((d1 = aload(&r->h->done_gen1)) < (unsigned long long)t + 1) {
+    if ((rc = device_error(r))) return rc;
+    if (bo.expired(timeout_ms))
+      return fail(EC_E_TIMEOUT, "rank %d round %lld did not complete", r->rank, (long long)t);
+    bo.pause();
+  }
+  long long G = (long long)d1 - 1;
+  if (pin) {
+    // Dekker handshake with the engine's pre-write check (ec_kernels.cu): publish
+    // the pin, then make sure the engine had not already passed the check for
+    // the round that would reuse G's slot.
+    while (true) {
+      __atomic_store_n(&r->h->pin_lo, (unsigned long long)G, __ATOMIC_SEQ_CST);
+      __atomic_thread_fence(__ATOMIC_SEQ_CST);
+      long long D = (long long)aload(&r->h->done_gen1) - 1;
+      if (D < G + c->R - 1) break;
+      G = D;
+    }
+  }
+  if (gen_out) *gen_out = G;
+  if (mask || nap) {
+    uint64_t m = 0;
+    int np = 0;
+    if ((rc = ec_gen_info(c, li, G, &m, nullptr, &np))) return rc;
+    if (mask) *mask = m;
+    if (nap) *nap = np;
+  }
+  return EC_OK;
+}
+
+int ec_set_pin(ec_comm_t* c, int li, uint64_t pin_lo, int ordered, void* stream) {
+  int rc = check_li(c, li);
+  if (rc) return rc;
+  EcRankHost* r = c->L[li];
+  if (ordered) {
+    CK(launch_write_u64(&r->hd->pin_lo, pin_lo, (cudaStream_t)stream));
+  } else {
+    __atomic_store_n(&r->h->pin_lo, (unsigned long long)pin_lo, __ATOMIC_SEQ_CST);
+  }
+  return EC_OK;
+}
+
+int ec_fold_raw(void* stash, const void* grad, int64_t n, int dtype, int mode, uint32_t* nonfinite,
+                void* stream) {
+  if (!stash || !grad || n < 0) return fail(EC_E_ARG, "bad fold arguments");
+  if (dtype < EC_F32 || dtype > EC_I64) return fail(EC_E_ARG, "bad dtype");
+  if (n == 0) return EC_OK;
+  CK(launch_fold(dtype, stash, grad, n, mode, nonfinite, (cudaStream_t)stream));
+  return EC_OK;
+}
+
+int ec_sgd_update(void* w, const void* u, double lr, int64_t n, int dtype, void* stream) {
+  if (!w || !u || n < 0) return fail(EC_E_ARG, "bad update arguments");
+  if (dtype != EC_F32 && dtype != EC_F64) return fail(EC_E_ARG, "update needs a float dtype");
+  if (n == 0) return EC_OK;
+  CK(launch_update(dtype, w, u, lr, n, (cudaStream_t)stream));
+  return EC_OK;
+}
+
+int ec_momentum_update(void* w, void* buf, const void* u, double lr, double mu, int64_t n, int dtype,
+                       void* stream) {
+  if (!w || !buf || !u || n < 0) return fail(EC_E_ARG, "bad momentum arguments");
+  if (dtype != EC_F32 && dtype != EC_F64) return fail(EC_E_ARG, "momentum needs a float dtype");
+  if (n == 0) return EC_OK;
+  CK(launch_momentum(dtype, w, buf, u, lr, mu, n, (cudaStream_t)stream));
+  return EC_OK;
+}
+
+int ec_local_reduce(const void* const* srcs, int p, uint64_t has, void* dst, int64_t n, int dtype,
+                    int divide, void* stream) {
+  if (!srcs || !dst || p < 1 || p > EC_MAX_P || n < 0) return fail(EC_E_ARG, "bad reduce arguments");
+  if (dtype < EC_F32 || dtype > EC_I64) return fail(EC_E_ARG, "bad dtype");
+  if (n == 0) return EC_OK;
+  CK(launch_reduce(dtype, srcs, p, has, dst, n, divide, (cudaStream_t)stream));
+  return EC_OK;
+}
+
+int ec_spin(uint64_t ns, void* stream) {
+  CK(launch_spin(ns, (cudaStream_t)stream));
+  return EC_OK;
+}
+
+}  // extern "C"

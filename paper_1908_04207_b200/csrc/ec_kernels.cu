@@ -1,0 +1,770 @@
+// sm_100a kernels of the eager-SGD partial-collective path.
+//
+//   ec_engine<T>        persistent per-rank collective engine (controller CTA +
+//                       worker CTAs): activation / snapshot protocol, two-shot
+//                       peer-memory reduction in tree order, result publish.
+//   ec_fold_kernel      GradientBuffer.fold          (eagersgd.py:55-57)
+//   ec_update_kernel    w = w - lr*u                 (eagersgd.py:165)
+//   ec_momentum_kernel  opt-in SGD momentum
+//   ec_reduce_kernel    tree_order_sum of local vectors (collectives.py:385-403)
+//   ec_post_kernel      stream-ordered request doorbell
+//   ec_spin_kernel      device imbalance injection   (transport.py:137-149)
+//
+// All bulk traffic moves in 16-byte vectors; the engine reads peer and reused
+// buffers with ld.global.cg so it never serves a stale L1 line.
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "ec_common.cuh"
+#include "ec_ops.cuh"
+
+// ---------------------------------------------------------------------------
+// engine: reduce-scatter (pull) of this rank's shard
+
+template <typename T, int P, int U>
+__device__ __forceinline__ void rs_fixed(const EcDesc& d, unsigned long long has, long long v0,
+                                         long long v1, char* dst, long long start,
+                                         long long stride, T inv, bool pow2) {
+  constexpr int V = Ops<T>::V;
+  const char* src[P];
+#pragma unroll
+  for (int q = 0; q < P; ++q) src[q] = d.send[q];
+  for (long long base = v0 + start; base < v1; base += stride * U) {
+    Vec16<T> x[U][P];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      long long v = base + (long long)u * stride;
+#pragma unroll
+      for (int q = 0; q < P; ++q) {
+        if (v < v1 && ((has >> q) & 1ull))
+          x[u][q].raw = ld_cg_v4(src[q] + v * 16);
+        else
+          x[u][q].raw = make_uint4(0, 0, 0, 0);
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      long long v = base + (long long)u * stride;
+      if (v < v1) {
+        Vec16<T> o;
+#pragma unroll
+        for (int l = 0; l < V; ++l) {
+          T c[P];
+#pragma unroll
+          for (int q = 0; q < P; ++q) c[q] = Ops<T>::canon(x[u][q].e[l]);
+          o.e[l] = Ops<T>::divp(tree_sum<T, P>(c), d.P, inv, pow2);
+        }
+        st_v4(dst + v * 16, o.raw);
+      }
+    }
+  }
+}
+
+template <typename T>
+__device__ void rs_dyn(const EcDesc& d, unsigned long long has, long long v0, long long v1,
+                       char* dst, long long start, long long stride, T inv, bool pow2) {
+  constexpr int V = Ops<T>::V;
+  for (long long v = v0 + start; v < v1; v += stride) {
+    Vec16<T> o;
+#pragma unroll
+    for (int l = 0; l < V; ++l) {
+      auto leaf = [&](int q) -> T {
+        if (!((has >> q) & 1ull)) return Ops<T>::zero();
+        Vec16<T> x;
+        x.raw = ld_cg_v4(d.send[q] + v * 16);
+        return Ops<T>::canon(x.e[l]);
+      };
+      o.e[l] = Ops<T>::divp(tree_sum_dyn<T>(d.P, leaf), d.P, inv, pow2);
+    }
+    st_v4(dst + v * 16, o.raw);
+  }
+}
+
+template <typename T>
+__device__ void rs_shard(const EcDesc& d, unsigned long long has, long long v0, long long v1,
+                         char* dst, long long start, long long stride) {
+  const bool pow2 = (d.P & (d.P - 1)) == 0;
+  const T inv = (T)1 / (T)d.P;  // exact for powers of two
+  switch (d.P) {
+    case 1: rs_fixed<T, 1, 4>(d, has, v0, v1, dst, start, stride, inv, pow2); break;
+    case 2: rs_fixed<T, 2, 4>(d, has, v0, v1, dst, start, stride, inv, pow2); break;
+    case 3: rs_fixed<T, 3, 2>(d, has, v0, v1, dst, start, stride, inv, pow2); break;
+    case 4: rs_fixed<T, 4, 2>(d, has, v0, v1, dst, start, stride, inv, pow2); break;
+    case 5: rs_fixed<T, 5, 2>(d, has, v0, v1, dst, start, stride, inv, pow2); break;
+    case 6: rs_fixed<T, 6, 2>(d, has, v0, v1, dst, start, stride, inv, pow2); break;
+    case 7: rs_fixed<T, 7, 2>(d, has, v0, v1, dst, start, stride, inv, pow2); break;
+    case 8: rs_fixed<T, 8, 2>(d, has, v0, v1, dst, start, stride, inv, pow2); break;
+    default: rs_dyn<T>(d, has, v0, v1, dst, start, stride, inv, pow2); break;
+  }
+}
+
+// scalar tail (n % V elements) -- reduced by the last owner
+template <typename T>
+__device__ void rs_tail(const EcDesc& d, unsigned long long has, char* dst, int lane) {
+  const long long e0 = d.nvec * Ops<T>::V;
+  const long long e = e0 + lane;
+  if (e >= d.n) return;
+  const bool pow2 = (d.P & (d.P - 1)) == 0;
+  const T inv = (T)1 / (T)d.P;
+  auto leaf = [&](int q) -> T {
+    if (!((has >> q) & 1ull)) return Ops<T>::zero();
+    const volatile T* s = reinterpret_cast<const volatile T*>(d.send[q]);
+    return Ops<T>::canon(s[e]);
+  };
+  reinterpret_cast<T*>(dst)[e] = Ops<T>::divp(tree_sum_dyn<T>(d.P, leaf), d.P, inv, pow2);
+}
+
+__device__ __forceinline__ long long shard_lo(long long nvec, int q, int P) {
+  return (long long)(((unsigned long long)nvec * (unsigned long long)q) / (unsigned long long)P);
+}
+
+template <typename T>
+__device__ void engine_worker(const EcDesc& d, int w, unsigned long long epoch) {
+  EcLocal* L = d.local;
+  EcCtrl* C = d.ctrl[d.rank];
+  __shared__ unsigned long long s_seq, s_has;
+  __shared__ long long s_gen;
+  __shared__ int s_exit;
+  const int tid = threadIdx.x;
+  const long long bt = blockDim.x;
+  if (tid == 0) s_seq = ld_acquire_gpu(&L->cmd_seq);
+  __syncthreads();
+  unsigned long long seen = s_seq;
+  __syncthreads();
+  while (true) {
+    if (tid == 0) {
+      unsigned ns = 64;
+      while (true) {
+        unsigned long long s = ld_acquire_gpu(&L->cmd_seq);
+        if (s != seen) {
+          s_seq = s;
+          s_gen = *(volatile long long*)&L->cmd_gen;
+          s_has = *(volatile unsigned long long*)&L->cmd_has;
+          s_exit = 0;
+          break;
+        }
+        if (ld_acquire_gpu(&L->exit_epoch) == epoch) {
+          s_exit = 1;
+          break;
+        }
+        __nanosleep(ns);
+        if (ns < 2048) ns <<= 1;
+      }
+    }
+    __syncthreads();
+    if (s_exit) return;
+    seen = s_seq;
+    const long long g = s_gen;
+    const unsigned long long has = s_has;
+    char* my_slot = d.ring[d.rank] + (g % d.R) * d.slot_bytes;
+    const long long off = (g % d.R) * d.slot_bytes;
+
+    // ---- reduce-scatter: my shard, read from every rank's send buffer
+    {
+      const long long v0 = shard_lo(d.nvec, d.rank, d.P), v1 = shard_lo(d.nvec, d.rank + 1, d.P);
+      rs_shard<T>(d, has, v0, v1, my_slot, (long long)w * bt + tid, (long long)d.W * bt);
+      if (d.rank == d.P - 1 && w == 0 && tid < Ops<T>::V) rs_tail<T>(d, has, my_slot, tid);
+    }
+    __syncthreads();
+    if (tid == 0) {
+      fence_acq_rel_sys();
+      unsigned long long old = atomicAdd(&L->rs_count, 1ull);
+      if (old + 1 == (unsigned long long)d.W * seen) {
+        fence_acq_rel_sys();
+        for (int q = 0; q < d.P; ++q) st_release_sys(&d.ctrl[q]->rsdone_from[d.rank], (unsigned long long)g + 1);
+      }
+      // ---- all-gather: wait for every owner's shard
+      const unsigned long long t0 = globaltimer_ns();
+      unsigned ns = 32;
+      for (int q = 0; q < d.P; ++q) {
+        while (ld_acquire_sys(&C->rsdone_from[q]) < (unsigned long long)g + 1) {
+          if (globaltimer_ns() - t0 > d.timeout_ns) {
+            st_release_sys(&d.hctl->error, EC_DERR_TIMEOUT);
+            st_release_sys(&d.hctl->error_info, 0x100 + q);
+            break;
+          }
+          __nanosleep(ns);
+          if (ns < 1024) ns <<= 1;
+        }
+      }
+    }
+    __syncthreads();
+    {
+      constexpr int U = 4;
+      const long long start = (long long)w * bt + tid, stride = (long long)d.W * bt;
+      for (int k = 1; k < d.P; ++k) {
+        const int q = (d.rank + k) % d.P;
+        const char* src = d.ring[q] + off;
+        const long long v0 = shard_lo(d.nvec, q, d.P), v1 = shard_lo(d.nvec, q + 1, d.P);
+        for (long long base = v0 + start; base < v1; base += stride * U) {
+          uint4 x[U];
+#pragma unroll
+          for (int u = 0; u < U; ++u) {
+            long long v = base + (long long)u * stride;
+            if (v < v1) x[u] = ld_cg_v4(src + v * 16);
+          }
+#pragma unroll
+          for (int u = 0; u < U; ++u) {
+            long long v = base + (long long)u * stride;
+            if (v < v1) st_v4(my_slot + v * 16, x[u]);
+          }
+        }
+      }
+      if (d.rank != d.P - 1 && w == 0 && tid < Ops<T>::V) {
+        const long long e = d.nvec * Ops<T>::V + tid;
+        if (e < d.n) {
+          const volatile T* s = reinterpret_cast<const volatile T*>(d.ring[d.P - 1] + off);
+          reinterpret_cast<T*>(my_slot)[e] = s[e];
+        }
+      }
+    }
+    __syncthreads();
+    if (tid == 0) {
+      __threadfence();
+      unsigned long long old = atomicAdd(&L->ag_count, 1ull);
+      if (old + 1 == (unsigned long long)d.W * seen) st_release_gpu(&L->round_done, seen);
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// engine: controller (one thread per rank)
+
+__device__ __forceinline__ unsigned int ld_relaxed_sys_u32(const unsigned int* p) {
+  unsigned int v;
+  asm volatile("ld.relaxed.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+
+__device__ void engine_controller(const EcDesc& d, unsigned long long epoch) {
+  EcLocal* L = d.local;
+  EcHostCtl* H = d.hctl;
+  EcCtrl* C = d.ctrl[d.rank];
+  const int r = d.rank, P = d.P;
+  long long g = L->g, hold_from = L->hold_from, contributed_round = L->contributed_round;
+  unsigned long long next_req = L->next_req;
+  int snapped = L->snapped, contrib = L->contrib, internal_act = L->internal_act;
+  int arrive_pending = L->arrive_pending, arrive_activate = L->arrive_activate;
+  unsigned long long seq = L->cmd_seq;
+  bool stopping = false;
+  unsigned long long stop_t0 = 0;
+  unsigned ns = 32;
+
+  // write this rank's word into every rank's control block (peer stores over NVLink)
+  auto push_all = [&](int which, unsigned long long v) {
+    for (int q = 0; q < P; ++q) {
+      unsigned long long* base;
+      if (which == 0) base = &d.ctrl[q]->act_from[r];
+      else if (which == 1) base = &d.ctrl[q]->snap_from[r];
+      else base = &d.ctrl[q]->arrive_from[r];
+      st_release_sys(base, v);
+    }
+  };
+  auto activate = [&]() {
+    internal_act = 1;
+    if (d.flavor != 0 && !d.replay) push_all(0, (unsigned long long)g + 1);
+  };
+  auto forced_bit = [&](long long gen) -> int {
+    if (gen >= d.n_forced) return -1;
+    return (int)((d.forced[gen] >> r) & 1ull);
+  };
+
+  while (true) {
+    bool progress = false;
+    if (!stopping && ld_relaxed_sys(&H->stop)) {
+      stopping = true;
+      stop_t0 = globaltimer_ns();
+    }
+    // ---- requests, strictly in sequence order
+    while (true) {
+      EcReq* q = &H->req[next_req % EC_REQ_RING];
+      if (ld_acquire_sys(&q->seq1) != next_req + 1) break;
+      const unsigned type = ld_relaxed_sys_u32(&q->type);
+      const unsigned fl = ld_relaxed_sys_u32(&q->flags);
+      const long long t = (long long)ld_relaxed_sys((const unsigned long long*)&q->t);
+      const long long arg = (long long)ld_relaxed_sys((const unsigned long long*)&q->arg);
+      unsigned long long status = 3;  // OK
+      if (type == EC_REQ_CONTRIB) {
+        if (fl & EC_CF_POISON) {
+          status = 4;
+        } else if (t < g || (t == g && snapped)) {
+          status = 2;  // the round already consumed this rank's slot
+        } else if (t > g) {
+          status = 5;
+          st_release_sys(&H->error, EC_DERR_ORDER);
+          st_release_sys(&H->error_info, (unsigned long long)t);
+        } else if (d.replay && forced_bit(g) != 1) {
+          status = 2;
+        } else {
+          contrib = (int)(EC_SNAP_DATA | ((fl & 1u) ? EC_SNAP_FRESH : 0ull));
+          contributed_round = t;
+          status = 1;
+          if (fl & 4u) {  // all-arrive
+            push_all(2, (unsigned long long)g + 1);
+            arrive_pending = 1;
+            arrive_activate = (fl & 2u) ? 1 : 0;
+          } else if (fl & 2u) {
+            activate();
+          }
+        }
+      } else if (type == EC_REQ_ACTIVATE) {
+        if (t == g) activate();
+      } else if (type == EC_REQ_HOLD) {
+        hold_from = arg;
+      }
+      st_release_sys(&H->reply[next_req % EC_REQ_RING], ((next_req + 1) << 8) | status);
+      ++next_req;
+      st_release_sys(&H->req_done, next_req);
+      progress = true;
+    }
+    // ---- all-arrive barrier (bench): everyone boarded -> activate
+    if (arrive_pending) {
+      bool all = true;
+      for (int q = 0; q < P && all; ++q)
+        all = ld_acquire_sys(&C->arrive_from[q]) >= (unsigned long long)g + 1;
+      if (all) {
+        arrive_pending = 0;
+        if (arrive_activate) activate();
+        progress = true;
+      }
+    }
+    // ---- snapshot decision (collectives.py:146-153, schedule.py:452-455)
+    if (!snapped) {
+      bool go = false;
+      if (d.replay) {
+        int b = forced_bit(g);
+        if (b == 0) go = true;
+        else if (b == 1) go = contrib != 0;
+      } else if (internal_act) {
+        go = true;
+      } else if (d.flavor != 0) {
+        bool ext = false;
+        for (int q = 0; q < P && !ext; ++q) ext = ld_acquire_sys(&C->act_from[q]) >= (unsigned long long)g + 1;
+        if (ext) {
+          const bool held = !stopping && g >= hold_from && contributed_round < g;
+          go = !held;
+        }
+      }
+      if (go) {
+        push_all(1, (((unsigned long long)g + 1) << 2) | (unsigned long long)contrib);
+        st_release_sys(&H->snap_gen1, (unsigned long long)g + 1);
+        if (contrib & (int)EC_SNAP_FRESH) hold_from = EC_INF_GEN;  // stash delivered (eagersgd.py:117-124)
+        snapped = 1;
+        progress = true;
+      }
+    }
+    // ---- round: all snapshots in -> two-shot reduction -> publish
+    if (snapped) {
+      bool all = true;
+      unsigned long long fresh = 0, has = 0;
+      for (int q = 0; q < P; ++q) {
+        unsigned long long w = ld_acquire_sys(&C->snap_from[q]);
+        if ((w >> 2) < (unsigned long long)g + 1) { all = false; break; }
+        fresh |= (w & EC_SNAP_FRESH) << q;
+        has |= ((w >> 1) & 1ull) << q;
+      }
+      if (all) {
+        // result-slot reuse guard: never overwrite generation h = g - R while h >= pin_lo
+        bool timed_out = false;
+        if (g >= d.R) {
+          fence_sc_sys();
+          const unsigned long long tp = globaltimer_ns();
+          unsigned ns2 = 32;
+          while (ld_acquire_sys(&H->pin_lo) <= (unsigned long long)(g - d.R)) {
+            if (globaltimer_ns() - tp > d.timeout_ns) { timed_out = true; break; }
+            __nanosleep(ns2);
+            if (ns2 < 1024) ns2 <<= 1;
+          }
+        }
+        if (timed_out) {
+          st_release_sys(&H->error_info, (unsigned long long)g | (1ull << 62));
+          st_release_sys(&H->error, EC_DERR_TIMEOUT);
+          break;
+        }
+        L->cmd_gen = g;
+        L->cmd_has = has;
+        ++seq;
+        st_release_gpu(&L->cmd_seq, seq);
+        const unsigned long long t0 = globaltimer_ns();
+        unsigned ns3 = 32;
+        while (ld_acquire_gpu(&L->round_done) != seq) {
+          if (globaltimer_ns() - t0 > d.timeout_ns) { timed_out = true; break; }
+          __nanosleep(ns3);
+          if (ns3 < 256) ns3 <<= 1;
+        }
+        if (timed_out) {
+          st_release_sys(&H->error_info, (unsigned long long)g);
+          st_release_sys(&H->error, EC_DERR_TIMEOUT);
+          break;
+        }
+        EcLog* lg = &H->log[g % EC_LOG_RING];
+        st_relaxed_sys(&lg->mask, fresh);
+        st_relaxed_sys(&lg->has, has);
+        st_relaxed_sys(&lg->nap, (unsigned long long)__popcll(fresh));
+        st_release_sys(&lg->gen1, (unsigned long long)g + 1);
+        st_release_sys(&H->done_gen1, (unsigned long long)g + 1);
+        ++g;
+        snapped = 0;
+        contrib = 0;
+        internal_act = 0;
+        arrive_pending = 0;
+        arrive_activate = 0;
+        progress = true;
+        continue;
+      }
+    }
+    if (stopping) {
+      const bool idle = !snapped && !arrive_pending;
+      if (idle || globaltimer_ns() - stop_t0 > 2000000000ull) break;
+    }
+    if (progress) {
+      ns = 32;
+    } else {
+      __nanosleep(ns);
+      if (ns < 512) ns <<= 1;
+    }
+  }
+  // park: persist the protocol state, release the workers, acknowledge
+  L->g = g;
+  L->hold_from = hold_from;
+  L->contributed_round = contributed_round;
+  L->next_req = next_req;
+  L->snapped = snapped;
+  L->contrib = contrib;
+  L->internal_act = internal_act;
+  L->arrive_pending = arrive_pending;
+  L->arrive_activate = arrive_activate;
+  __threadfence();
+  st_release_gpu(&L->exit_epoch, epoch);
+  st_release_sys(&H->exited, epoch);
+}
+
+template <typename T>
+__global__ void __launch_bounds__(256, 2)
+ec_engine(const EcDesc* __restrict__ descs, int blocks_per_rank, unsigned long long epoch) {
+  const int lr = blockIdx.x / blocks_per_rank;
+  const int role = blockIdx.x % blocks_per_rank;
+  const EcDesc& d = descs[lr];
+  if (role == 0) {
+    if (threadIdx.x == 0) engine_controller(d, epoch);
+    return;
+  }
+  engine_worker<T>(d, role - 1, epoch);
+}
+
+template __global__ void ec_engine<float>(const EcDesc*, int, unsigned long long);
+template __global__ void ec_engine<double>(const EcDesc*, int, unsigned long long);
+template __global__ void ec_engine<long long>(const EcDesc*, int, unsigned long long);
+
+// ---------------------------------------------------------------------------
+// standalone streaming kernels
+
+template <typename T, int MODE>
+__global__ void __launch_bounds__(256)
+ec_fold_kernel(T* __restrict__ stash, const T* __restrict__ grad, long long n,
+               unsigned int* nonfinite, int vec_ok) {
+  constexpr int V = Ops<T>::V;
+  constexpr int U = 4;
+  bool bad = false;
+  const long long tid = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  const long long nth = (long long)gridDim.x * blockDim.x;
+  long long done = 0;
+  if (vec_ok) {
+    const long long nv = n / V;
+    for (long long base = tid; base < nv; base += nth * U) {
+      Vec16<T> gv[U], sv[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        long long v = base + u * nth;
+        if (v < nv) {
+          gv[u].raw = ld_stream_v4(grad + v * V);
+          if (MODE == 1) sv[u].raw = ld_stream_v4(stash + v * V);
+        }
+      }
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        long long v = base + u * nth;
+        if (v < nv) {
+          Vec16<T> o;
+#pragma unroll
+          for (int l = 0; l < V; ++l) {
+            bad |= !Ops<T>::finite(gv[u].e[l]);
+            o.e[l] = MODE == 1 ? Ops<T>::add(sv[u].e[l], gv[u].e[l]) : Ops<T>::canon(gv[u].e[l]);
+          }
+          st_v4(stash + v * V, o.raw);
+        }
+      }
+    }
+    done = nv * V;
+  }
+  for (long long e = done + tid; e < n; e += nth) {
+    T gv = grad[e];
+    bad |= !Ops<T>::finite(gv);
+    stash[e] = MODE == 1 ? Ops<T>::add(stash[e], gv) : Ops<T>::canon(gv);
+  }
+  if (nonfinite && __any_sync(0xffffffffu, bad) && (threadIdx.x & 31) == 0) atomicOr(nonfinite, 1u);
+}
+
+template <typename T>
+__global__ void __launch_bounds__(256)
+ec_update_kernel(T* __restrict__ w, const T* __restrict__ u, T lr, long long n, int vec_ok) {
+  constexpr int V = Ops<T>::V;
+  constexpr int U = 4;
+  const long long tid = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  const long long nth = (long long)gridDim.x * blockDim.x;
+  long long done = 0;
+  if (vec_ok) {
+    const long long nv = n / V;
+    for (long long base = tid; base < nv; base += nth * U) {
+      Vec16<T> wv[U], uv[U];
+#pragma unroll
+      for (int k = 0; k < U; ++k) {
+        long long v = base + k * nth;
+        if (v < nv) {
+          wv[k].raw = ld_stream_v4(w + v * V);
+          uv[k].raw = ld_stream_v4(u + v * V);
+        }
+      }
+#pragma unroll
+      for (int k = 0; k < U; ++k) {
+        long long v = base + k * nth;
+        if (v < nv) {
+#pragma unroll
+          for (int l = 0; l < V; ++l) wv[k].e[l] = Ops<T>::sgd(wv[k].e[l], lr, uv[k].e[l]);
+          st_v4(w + v * V, wv[k].raw);
+        }
+      }
+    }
+    done = nv * V;
+  }
+  for (long long e = done + tid; e < n; e += nth) w[e] = Ops<T>::sgd(w[e], lr, u[e]);
+}
+
+template <typename T>
+__global__ void __launch_bounds__(256)
+ec_momentum_kernel(T* __restrict__ w, T* __restrict__ buf, const T* __restrict__ u, T lr, T mu,
+                   long long n, int vec_ok) {
+  constexpr int V = Ops<T>::V;
+  const long long tid = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  const long long nth = (long long)gridDim.x * blockDim.x;
+  long long done = 0;
+  if (vec_ok) {
+    const long long nv = n / V;
+    for (long long v = tid; v < nv; v += nth) {
+      Vec16<T> wv, bv, uv;
+      wv.raw = ld_stream_v4(w + v * V);
+      bv.raw = ld_stream_v4(buf + v * V);
+      uv.raw = ld_stream_v4(u + v * V);
+#pragma unroll
+      for (int l = 0; l < V; ++l) {
+        bv.e[l] = Ops<T>::mom(mu, bv.e[l], uv.e[l]);
+        wv.e[l] = Ops<T>::sgd(wv.e[l], lr, bv.e[l]);
+      }
+      st_v4(buf + v * V, bv.raw);
+      st_v4(w + v * V, wv.raw);
+    }
+    done = nv * V;
+  }
+  for (long long e = done + tid; e < n; e += nth) {
+    T b = Ops<T>::mom(mu, buf[e], u[e]);
+    buf[e] = b;
+    w[e] = Ops<T>::sgd(w[e], lr, b);
+  }
+}
+
+struct EcSrcs {
+  const void* p[EC_MAX_P];
+};
+
+template <typename T, int P>
+__device__ __forceinline__ void reduce_vec(const EcSrcs& s, unsigned long long has, T* dst, long long v,
+                                           int div, T inv, bool pow2, int p) {
+  constexpr int V = Ops<T>::V;
+  Vec16<T> x[P];
+#pragma unroll
+  for (int q = 0; q < P; ++q)
+    x[q].raw = ((has >> q) & 1ull) ? ld_stream_v4(reinterpret_cast<const T*>(s.p[q]) + v * V)
+                                   : make_uint4(0, 0, 0, 0);
+  Vec16<T> o;
+#pragma unroll
+  for (int l = 0; l < V; ++l) {
+    T c[P];
+#pragma unroll
+    for (int q = 0; q < P; ++q) c[q] = Ops<T>::canon(x[q].e[l]);
+    T sum = tree_sum<T, P>(c);
+    o.e[l] = div ? Ops<T>::divp(sum, p, inv, pow2) : sum;
+  }
+  st_v4(dst + v * V, o.raw);
+}
+
+template <typename T>
+__global__ void __launch_bounds__(256)
+ec_reduce_kernel(EcSrcs s, int p, unsigned long long has, T* __restrict__ dst, long long n,
+                 int div, int vec_ok) {
+  constexpr int V = Ops<T>::V;
+  const long long tid = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  const long long nth = (long long)gridDim.x * blockDim.x;
+  const bool pow2 = (p & (p - 1)) == 0;
+  const T inv = (T)1 / (T)p;
+  long long done = 0;
+  if (vec_ok) {
+    const long long nv = n / V;
+    for (long long v = tid; v < nv; v += nth) {
+      switch (p) {
+        case 1: reduce_vec<T, 1>(s, has, dst, v, div, inv, pow2, p); break;
+        case 2: reduce_vec<T, 2>(s, has, dst, v, div, inv, pow2, p); break;
+        case 3: reduce_vec<T, 3>(s, has, dst, v, div, inv, pow2, p); break;
+        case 4: reduce_vec<T, 4>(s, has, dst, v, div, inv, pow2, p); break;
+        case 5: reduce_vec<T, 5>(s, has, dst, v, div, inv, pow2, p); break;
+        case 6: reduce_vec<T, 6>(s, has, dst, v, div, inv, pow2, p); break;
+        case 7: reduce_vec<T, 7>(s, has, dst, v, div, inv, pow2, p); break;
+        case 8: reduce_vec<T, 8>(s, has, dst, v, div, inv, pow2, p); break;
+        default: {
+          Vec16<T> o;
+#pragma unroll
+          for (int l = 0; l < V; ++l) {
+            auto leaf = [&](int q) -> T {
+              if (!((has >> q) & 1ull)) return Ops<T>::zero();
+              return Ops<T>::canon(reinterpret_cast<const T*>(s.p[q])[v * V + l]);
+            };
+            T sum = tree_sum_dyn<T>(p, leaf);
+            o.e[l] = div ? Ops<T>::divp(sum, p, inv, pow2) : sum;
+          }
+          st_v4(dst + v * V, o.raw);
+        }
+      }
+    }
+    done = nv * V;
+  }
+  for (long long e = done + tid; e < n; e += nth) {
+    auto leaf = [&](int q) -> T {
+      if (!((has >> q) & 1ull)) return Ops<T>::zero();
+      return Ops<T>::canon(reinterpret_cast<const T*>(s.p[q])[e]);
+    };
+    T sum = tree_sum_dyn<T>(p, leaf);
+    dst[e] = div ? Ops<T>::divp(sum, p, inv, pow2) : sum;
+  }
+}
+
+__global__ void ec_post_kernel(EcReq* rec, unsigned long long seq1, unsigned int type,
+                               unsigned int flags, long long t, long long arg,
+                               unsigned int* poison) {
+  if (threadIdx.x != 0) return;
+  if (poison) {
+    if (*(volatile unsigned int*)poison) flags |= EC_CF_POISON;
+    *(volatile unsigned int*)poison = 0u;
+  }
+  volatile EcReq* v = rec;
+  v->type = type;
+  v->flags = flags;
+  v->t = t;
+  v->arg = arg;
+  fence_acq_rel_sys();
+  st_release_sys(&rec->seq1, seq1);
+}
+
+__global__ void ec_write_u64_kernel(unsigned long long* p, unsigned long long v) {
+  if (threadIdx.x == 0) {
+    fence_acq_rel_sys();
+    st_release_sys(p, v);
+  }
+}
+
+__global__ void ec_spin_kernel(unsigned long long ns) {
+  if (threadIdx.x != 0) return;
+  const unsigned long long t0 = globaltimer_ns();
+  while (globaltimer_ns() - t0 < ns) __nanosleep(1000);
+}
+
+// ---------------------------------------------------------------------------
+// host-side launch helpers (C++ linkage, used by ec_host.cu)
+
+static inline int grid_for(long long work, int threads) {
+  long long b = (work + threads - 1) / threads;
+  const long long cap = 148LL * 8;
+  if (b > cap) b = cap;
+  if (b < 1) b = 1;
+  return (int)b;
+}
+
+cudaError_t launch_engine(int dtype, const EcDesc* d_descs, int n_local, int blocks_per_rank,
+                          unsigned long long epoch, cudaStream_t s) {
+  void* args[] = {(void*)&d_descs, (void*)&blocks_per_rank, (void*)&epoch};
+  dim3 grid(n_local * blocks_per_rank), block(256);
+  const void* fn = dtype == 0 ? (const void*)ec_engine<float>
+                  : dtype == 1 ? (const void*)ec_engine<double>
+                               : (const void*)ec_engine<long long>;
+  return cudaLaunchCooperativeKernel(fn, grid, block, args, 0, s);
+}
+
+cudaError_t launch_fold(int dtype, void* stash, const void* grad, long long n, int mode,
+                        unsigned int* nonfinite, cudaStream_t s) {
+  const int vec_ok = ((((uintptr_t)stash) | ((uintptr_t)grad)) & 15) == 0;
+  const int V = dtype == 0 ? 4 : 2;
+  const int grid = grid_for((n / V + 3) / 4 + 1, 256);
+  if (dtype == 0) {
+    if (mode) ec_fold_kernel<float, 1><<<grid, 256, 0, s>>>((float*)stash, (const float*)grad, n, nonfinite, vec_ok);
+    else ec_fold_kernel<float, 0><<<grid, 256, 0, s>>>((float*)stash, (const float*)grad, n, nonfinite, vec_ok);
+  } else if (dtype == 1) {
+    if (mode) ec_fold_kernel<double, 1><<<grid, 256, 0, s>>>((double*)stash, (const double*)grad, n, nonfinite, vec_ok);
+    else ec_fold_kernel<double, 0><<<grid, 256, 0, s>>>((double*)stash, (const double*)grad, n, nonfinite, vec_ok);
+  } else {
+    if (mode) ec_fold_kernel<long long, 1><<<grid, 256, 0, s>>>((long long*)stash, (const long long*)grad, n, nonfinite, vec_ok);
+    else ec_fold_kernel<long long, 0><<<grid, 256, 0, s>>>((long long*)stash, (const long long*)grad, n, nonfinite, vec_ok);
+  }
+  return cudaGetLastError();
+}
+
+cudaError_t launch_update(int dtype, void* w, const void* u, double lr, long long n, cudaStream_t s) {
+  const int vec_ok = ((((uintptr_t)w) | ((uintptr_t)u)) & 15) == 0;
+  const int V = dtype == 0 ? 4 : 2;
+  const int grid = grid_for((n / V + 3) / 4 + 1, 256);
+  if (dtype == 0) ec_update_kernel<float><<<grid, 256, 0, s>>>((float*)w, (const float*)u, (float)lr, n, vec_ok);
+  else if (dtype == 1) ec_update_kernel<double><<<grid, 256, 0, s>>>((double*)w, (const double*)u, lr, n, vec_ok);
+  else return cudaErrorInvalidValue;
+  return cudaGetLastError();
+}
+
+cudaError_t launch_momentum(int dtype, void* w, void* buf, const void* u, double lr, double mu,
+                            long long n, cudaStream_t s) {
+  const int vec_ok = ((((uintptr_t)w) | ((uintptr_t)u) | ((uintptr_t)buf)) & 15) == 0;
+  const int V = dtype == 0 ? 4 : 2;
+  const int grid = grid_for(n / V + 1, 256);
+  if (dtype == 0) ec_momentum_kernel<float><<<grid, 256, 0, s>>>((float*)w, (float*)buf, (const float*)u, (float)lr, (float)mu, n, vec_ok);
+  else if (dtype == 1) ec_momentum_kernel<double><<<grid, 256, 0, s>>>((double*)w, (double*)buf, (const double*)u, lr, mu, n, vec_ok);
+  else return cudaErrorInvalidValue;
+  return cudaGetLastError();
+}
+
+cudaError_t launch_reduce(int dtype, const void* const* srcs, int p, unsigned long long has, void* dst,
+                          long long n, int div, cudaStream_t s) {
+  EcSrcs S;
+  uintptr_t bits = (uintptr_t)dst;
+  for (int q = 0; q < EC_MAX_P; ++q) {
+    S.p[q] = q < p ? srcs[q] : nullptr;
+    if (q < p) bits |= (uintptr_t)srcs[q];
+  }
+  const int vec_ok = (bits & 15) == 0;
+  const int V = dtype == 0 ? 4 : 2;
+  const int grid = grid_for(n / V + 1, 256);
+  if (dtype == 0) ec_reduce_kernel<float><<<grid, 256, 0, s>>>(S, p, has, (float*)dst, n, div, vec_ok);
+  else if (dtype == 1) ec_reduce_kernel<double><<<grid, 256, 0, s>>>(S, p, has, (double*)dst, n, div, vec_ok);
+  else ec_reduce_kernel<long long><<<grid, 256, 0, s>>>(S, p, has, (long long*)dst, n, div, vec_ok);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_post(EcReq* rec, unsigned long long seq1, unsigned int type, unsigned int flags,
+                        long long t, long long arg, unsigned int* poison, cudaStream_t s) {
+  ec_post_kernel<<<1, 32, 0, s>>>(rec, seq1, type, flags, t, arg, poison);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_write_u64(unsigned long long* p, unsigned long long v, cudaStream_t s) {
+  ec_write_u64_kernel<<<1, 32, 0, s>>>(p, v);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_spin(unsigned long long ns, cudaStream_t s) {
+  ec_spin_kernel<<<1, 32, 0, s>>>(ns);
+  return cudaGetLastError();
+}

@@ -1,0 +1,125 @@
+"""Replay mode: drive GPU ranks from a recorded reference schedule.
+
+Participation in eager-SGD depends only on timing, never on values, so the
+schedule-level events of a reference run -- which ranks' offers boarded each
+generation and which generation each rank observed at each step -- can be
+forced onto a GPU run.  The device engine then
+snapshots exactly the recorded masks (`ec_comm_set_replay`), every host step
+reads exactly the recorded generation, and the values it computes (stash
+folds, tree-ordered sums, updates, resyncs) must equal the reference's: bit for
+bit in f64, within 1e-6 in fp32, and bit for bit against the fp32 restatement.
+"""
+
+from __future__ import annotations
+
+import threading
+
+import numpy as np
+import torch
+
+from . import _lib
+from ._lib import call
+from .collectives import AllreduceHandle, CollectiveConfig, drive
+from .eagersgd import TrainState, apply_update, attach_delivery_tracking, resync_step
+from .trace import DeliveryLedger
+from .world import EmulatedWorld
+
+
+def replay_training(trace, element: str = "f4", device: int = 0, world=None, ring_slots: int = 4):
+    """Replay a c1_<flavor> trace (tests/golden) on an emulated world.
+
+    trace: mapping with p, steps, epochs, steps_per_epoch, lr, resync_period,
+    masks[g], accepted[r, t], observed[r, t], grads[r, t, :], w0.
+    Returns dict(w=[p, dim] final weights (numpy), accepted=[p, steps],
+    ledger=dict, masks=[steps] observed device masks).
+    """
+    p = int(trace["p"])
+    steps = int(trace["steps"])
+    epochs = int(trace["epochs"])
+    spe = int(trace["steps_per_epoch"])
+    period = int(trace["resync_period"])
+    lr = float(trace["lr"])
+    masks = [int(m) for m in np.asarray(trace["masks"])]
+    observed = np.asarray(trace["observed"]).astype(np.int64)
+    grads_np = np.asarray(trace["grads"])
+    dim = grads_np.shape[-1]
+    cfg = CollectiveConfig(p=p, flavor="solo", vector_len=dim, element=element, seed=0)
+    sync_cfg = CollectiveConfig(p=p, flavor="sync", vector_len=dim, element=element)
+    own = world is None
+    world = world or EmulatedWorld(p, device, ring_slots=ring_slots)
+    handles = [AllreduceHandle(cfg, r, world, cid=0) for r in range(p)]
+    resync = [AllreduceHandle(sync_cfg, r, world, cid=1) for r in range(p)]
+    for r in range(p):
+        handles[r].comm.set_replay(r, masks)
+    dtype = cfg.torch_dtype
+    dev = f"cuda:{device}"
+    grads = torch.as_tensor(grads_np, dtype=dtype, device=dev)
+    w0 = np.asarray(trace["w0"])
+    ledger = DeliveryLedger()
+    states = [TrainState.fresh(torch.as_tensor(w0, dtype=dtype, device=dev), lr, rank=r,
+                               resync_period=period, tau=None) for r in range(p)]
+    acc = np.zeros((p, steps), dtype=np.int8)
+    seen_masks = np.zeros(steps, dtype=np.int64)
+    errors: list = []
+    for r in range(p):
+        call("ec_set_pin", handles[r].comm.ptr, r, int(observed[r, 0]), 0, None)
+    go = threading.Barrier(p)
+
+    def rank_body(r: int):
+        try:
+            h, st = handles[r], states[r]
+            attach_delivery_tracking(h, st, ledger)
+            torch.cuda.set_device(device)
+            go.wait()
+            k = 0
+            for e in range(epochs):
+                for s in range(spe):
+                    t = e * spe + s
+                    ledger.generated(r, t)
+                    with h.engine.lock:
+                        st.send_buf.bind(h)
+                        st.send_buf.fold(grads[r, t], t)
+                        seq = h._post_contribute(t, _lib.EC_CF_FRESH)
+                    status = h._reply(seq)
+                    if status == _lib.R_ACCEPTED:
+                        acc[r, t] = 1
+                        h.contributed_round = t
+                        h._fresh_gens.add(t)
+                    g = int(observed[r, t])
+                    gen, mask, nap = h._wait(g, 60.0, pin=False)
+                    info_mask = _gen_mask(h, g)
+                    if r == 0 or seen_masks[g] == 0:
+                        seen_masks[g] = info_mask
+                    apply_update(st, h._slot(g))
+                    nxt = int(observed[r, t + 1]) if t + 1 < steps else _lib.UINT64_MAX
+                    call("ec_set_pin", h.comm.ptr, h.li, nxt, 1,
+                         torch.cuda.current_stream(device).cuda_stream)
+                    st.t = t + 1
+                if (e + 1) % period == 0:
+                    drive(resync_step(st, resync[r], k))
+                    k += 1
+            torch.cuda.current_stream(device).synchronize()
+        except BaseException as ex:  # surfaced below
+            errors.append(ex)
+
+    threads = [threading.Thread(target=rank_body, args=(r,), daemon=True) for r in range(p)]
+    for th in threads:
+        th.start()
+    for th in threads:
+        th.join()
+    if errors:
+        if own:
+            world.close()
+        raise errors[0]
+    w = np.stack([st.w.detach().cpu().numpy() for st in states])
+    out = {"w": w, "accepted": acc, "ledger": ledger.as_dict(), "masks": seen_masks}
+    if own:
+        world.close()
+    return out
+
+
+def _gen_mask(h: AllreduceHandle, g: int) -> int:
+    import ctypes as C
+    m, hm, nap = C.c_uint64(), C.c_uint64(), C.c_int()
+    call("ec_gen_info", h.comm.ptr, h.li, g, C.byref(m), C.byref(hm), C.byref(nap))
+    return m.value

@@ -1,0 +1,333 @@
+"""The persistent engine on one GPU: P ranks of an EmulatedWorld (one engine
+launch, one CTA group per rank) driven by P host threads.  Ports the
+reference's known-answer tests (test_collectives.py, test_eagersgd.py) to the
+device API, and replays the reference's config-1 schedules (tests/golden/c1_*)
+bit for bit."""
+
+import json
+import os
+import threading
+import time
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+if not torch.cuda.is_available():
+    pytest.skip("needs a CUDA device", allow_module_level=True)
+
+from oracle import restated as R  # noqa: E402
+from paper_1908_04207_b200 import (  # noqa: E402
+    AllreduceHandle, CollectiveConfig, EmulatedWorld, TraceRecorder, TrainState,
+    attach_delivery_tracking, drive, initiator_for_round, run_allreduce, staleness_guard,
+    train_step,
+)
+from paper_1908_04207_b200.replay import replay_training  # noqa: E402
+from paper_1908_04207_b200.trace import DeliveryLedger  # noqa: E402
+
+
+def _ka(golden_dir):
+    with open(os.path.join(golden_dir, "known_answers.json")) as f:
+        return json.load(f)
+
+
+def _np(t):
+    return t.detach().cpu().numpy()
+
+
+def test_sync_pair_frozen_example():
+    cfg = CollectiveConfig(p=2, flavor="sync", vector_len=2)
+    res, _, world = run_allreduce(cfg, np.array([[2.0, 4.0], [4.0, 8.0]]))
+    for r in range(2):
+        assert _np(res[(r, 0)].u).tolist() == [3.0, 6.0]
+        assert res[(r, 0)].included == 0b11 and res[(r, 0)].nap == 2
+    world.close()
+
+
+@pytest.mark.parametrize("p", [1, 2, 3, 4, 5, 6, 7, 8, 13])
+def test_sync_matches_reference_bitwise(golden_dir, p):
+    g = np.load(os.path.join(golden_dir, "tree_sums.npz"))
+    contrib = g[f"sync_in_p{p}"]
+    cfg = CollectiveConfig(p=p, flavor="sync", vector_len=8)
+    res, _, world = run_allreduce(cfg, contrib, rounds=2)
+    for r in range(p):
+        for t in range(2):
+            assert _np(res[(r, t)].u).tobytes() == g[f"sync_u_p{p}"].tobytes()
+            assert res[(r, t)].nap == p
+    world.close()
+
+
+@pytest.mark.parametrize("p", [2, 3, 8])
+@pytest.mark.parametrize("n", [1, 5, 1027, 300_001])
+def test_sync_f32_matches_oracle(p, n):
+    rng = np.random.default_rng(p * 1000 + n)
+    contrib = rng.standard_normal((p, n)).astype(np.float32)
+    cfg = CollectiveConfig(p=p, flavor="sync", vector_len=n, element="f4")
+    res, _, world = run_allreduce(cfg, contrib, rounds=3)
+    want, inc, nap = R.allreduce_round(list(contrib), [True] * p, np.float32)
+    for r in range(p):
+        for t in range(3):
+            assert _np(res[(r, t)].u).tobytes() == want.tobytes()
+            assert res[(r, t)].included == inc
+    world.close()
+
+
+def test_integer_element_divides_exactly(golden_dir):
+    g = np.load(os.path.join(golden_dir, "tree_sums.npz"))
+    cfg = CollectiveConfig(p=4, flavor="sync", vector_len=4, element="i8")
+    res, _, world = run_allreduce(cfg, g["i8_in_p4"])
+    assert res[(0, 0)].u.dtype == torch.int64
+    assert _np(res[(0, 0)].u).tobytes() == g["i8_u_p4"].tobytes()
+    world.close()
+
+
+def test_solo_first_arrival_defines_the_round(golden_dir):
+    ka = _ka(golden_dir)["solo_first_arrival"]
+    contrib = np.array(ka["contrib"])
+    cfg = CollectiveConfig(p=4, flavor="solo", vector_len=4)
+    res, _, world = run_allreduce(cfg, contrib, delay_us=lambda r, t: 1000 * r, time_scale=20)
+    for r in range(4):
+        assert res[(r, 0)].included == ka["included"][r] == 0b0001
+        assert _np(res[(r, 0)].u).tobytes() == np.array(ka["u"]).tobytes()
+    world.close()
+
+
+def test_solo_earliest_rank_need_not_be_rank_zero(golden_dir):
+    ka = _ka(golden_dir)["solo_earliest_not_zero"]
+    cfg = CollectiveConfig(p=4, flavor="solo", vector_len=2)
+    contrib = np.random.default_rng(2).standard_normal((4, 2))
+    res, _, world = run_allreduce(cfg, contrib, delay_us=lambda r, t: ka["delays_us"][r],
+                                  time_scale=20)
+    for r in range(4):
+        assert res[(r, 0)].included == ka["included"] == 0b0100
+    world.close()
+
+
+def test_majority_round_zero_mask_is_an_arrival_prefix(golden_dir):
+    ka = _ka(golden_dir)["majority_prefix"]
+    for seed in (31, 32, 33, 34):
+        p = 4
+        cfg = CollectiveConfig(p=p, flavor="majority", vector_len=4, seed=seed)
+        res, _, world = run_allreduce(cfg, lambda r, t: np.full(4, float(10 * r + t)),
+                                      delay_us=lambda r, t: 1000 * r, time_scale=20)
+        want = ka[str(seed)]
+        assert initiator_for_round(seed, 0, p) == want["initiator"]
+        for r in range(p):
+            assert res[(r, 0)].included == want["included"]
+            assert _np(res[(r, 0)].u).tolist() == want["u"]
+        world.close()
+
+
+def test_majority_multiround_agreement_and_initiator_freshness():
+    p, rounds, seed = 4, 6, 31
+    cfg = CollectiveConfig(p=p, flavor="majority", vector_len=4, seed=seed)
+    rec = TraceRecorder()
+    res, _, world = run_allreduce(cfg, lambda r, t: np.full(4, float(10 * r + t)), rounds=rounds,
+                                  delay_us=lambda r, t: 1000 * r, recorder=rec, time_scale=5)
+    by_gen = {}
+    for row in rec.rounds:
+        by_gen.setdefault(row.rnd, []).append(row)
+    for g, rows in by_gen.items():
+        init = initiator_for_round(seed, g, p)
+        ref = rows[0]
+        assert (ref.included >> init) & 1
+        assert 1 <= ref.nap == bin(ref.included).count("1") <= p
+        assert all(row.included == ref.included for row in rows)
+        assert all(_np(row.u).tobytes() == _np(ref.u).tobytes() for row in rows)
+    for r in range(p):
+        gens = [res[(r, t)].rnd for t in range(rounds)]
+        assert all(g >= t for t, g in enumerate(gens)) and gens == sorted(gens)
+    world.close()
+
+
+def test_solo_zero_skew_all_arrive():
+    """With the bench's all-arrive barrier every contribution boards (nap = P)."""
+    p = 8
+    world = EmulatedWorld(p)
+    cfg = CollectiveConfig(p=p, flavor="solo", vector_len=1000, element="f4")
+    hs = [AllreduceHandle(cfg, r, world) for r in range(p)]
+    contrib = np.random.default_rng(3).standard_normal((p, 1000)).astype(np.float32)
+    want, _, _ = R.allreduce_round(list(contrib), [True] * p, np.float32)
+    out = {}
+
+    def body(r):
+        for t in range(3):
+            hs[r]._contribute(t, contrib[r], fresh=True, activate=True, all_arrive=True)
+            out[(r, t)] = hs[r].wait_blocking(t)
+
+    th = [threading.Thread(target=body, args=(r,)) for r in range(p)]
+    [x.start() for x in th]
+    [x.join() for x in th]
+    for r in range(p):
+        for t in range(3):
+            gen, res = out[(r, t)]
+            assert gen == t and res.nap == p
+            assert _np(res.u).tobytes() == want.tobytes()
+    world.close()
+
+
+def test_late_contribution_is_refused(golden_dir):
+    ka = _ka(golden_dir)["late_refused"]
+    world = EmulatedWorld(2)
+    cfg = CollectiveConfig(p=2, flavor="solo", vector_len=2)
+    hs = [AllreduceHandle(cfg, r, world) for r in range(2)]
+    assert hs[0].try_contribute(0, np.array([1.0, 2.0])) is ka["accept0"] is True
+    hs[0].activate(0)
+    hs[0].wait_blocking(0)
+    assert hs[0].round_done(0)
+    assert hs[1].try_contribute(0, np.array([5.0, 5.0])) is ka["accept1"] is False
+    gen, res = hs[1].latest_result()
+    assert gen == ka["gen"] == 0 and res.included == ka["included"]
+    assert _np(res.u).tolist() == ka["u"]
+    world.close()
+
+
+def test_out_of_order_round_is_an_error():
+    world = EmulatedWorld(2)
+    cfg = CollectiveConfig(p=2, flavor="solo", vector_len=2)
+    hs = [AllreduceHandle(cfg, r, world) for r in range(2)]
+    with pytest.raises(AssertionError):
+        hs[0].try_contribute(1, np.array([1.0, 2.0]))
+    world.close()
+
+
+def test_wait_done_fast_path_returns_latest():
+    cfg = CollectiveConfig(p=2, flavor="sync", vector_len=2)
+    _, handles, world = run_allreduce(cfg, np.ones((2, 2)), rounds=3)
+    world.resume()
+    g = handles[0].wait_done(1)
+    with pytest.raises(StopIteration) as ei:
+        next(g)
+    gen, res = ei.value.value
+    assert gen == 2 and res.nap == 2
+    world.close()
+
+
+def test_pause_resume_allows_device_sync():
+    world = EmulatedWorld(2)
+    cfg = CollectiveConfig(p=2, flavor="sync", vector_len=16, element="f4")
+    hs = [AllreduceHandle(cfg, r, world) for r in range(2)]
+    out = {}
+
+    def body(r, t):
+        out[(r, t)] = drive(hs[r].call_round(t, np.full(16, r + 1.0, np.float32)))
+
+    for t in range(2):
+        th = [threading.Thread(target=body, args=(r, t)) for r in range(2)]
+        [x.start() for x in th]
+        [x.join() for x in th]
+        world.synchronize()          # pause -> torch.cuda.synchronize -> resume
+    assert _np(out[(0, 1)].u).tolist() == [1.5] * 16
+    world.close()
+
+
+def test_missed_round_folds_into_the_next_sum(golden_dir):
+    """Fig. 7 (test_eagersgd.py:60-121): the slow rank misses round 0 and
+    delivers both of its gradients in round 1."""
+    ka = _ka(golden_dir)["fig7"]
+    world = EmulatedWorld(2)
+    cfg = CollectiveConfig(p=2, flavor="solo", vector_len=3)
+    hs = [AllreduceHandle(cfg, r, world) for r in range(2)]
+    states = [TrainState.fresh(np.zeros(3), lr=1.0, rank=r, dtype=torch.float64) for r in range(2)]
+    ledger = DeliveryLedger()
+    for r in range(2):
+        attach_delivery_tracking(hs[r], states[r], ledger)
+    gf = [torch.tensor(v, dtype=torch.float64, device="cuda") for v in ka["gf"]]
+    gs = [torch.tensor(v, dtype=torch.float64, device="cuda") for v in ka["gs"]]
+    seen = {}
+    r0_done = threading.Event()
+    slow_offered_1 = threading.Event()
+
+    def fast():
+        for t in range(2):
+            if t == 1:
+                slow_offered_1.wait(10)
+            ledger.generated(0, t)
+            _, res, gen = drive(train_step(states[0], None, hs[0], grad=gf[t], keep_u=True))
+            seen[(0, t)] = res
+            if t == 0:
+                r0_done.set()
+
+    def slow():
+        r0_done.wait(10)          # round 0 completed: the bus is gone
+        ledger.generated(1, 0)
+        _, res, gen = drive(train_step(states[1], None, hs[1], grad=gs[0], keep_u=True))
+        seen[(1, 0)] = res
+        # round 1: fold g_s1 into the stash and offer it without activating; the
+        # fast rank's offer boards before anyone activates (the link window)
+        ledger.generated(1, 1)
+        st = states[1]
+        with hs[1].engine.lock:
+            st.send_buf.fold(gs[1], 1)
+            seq = hs[1]._post_contribute(1, 1)   # fresh, no activation
+        assert hs[1]._reply(seq) == 1
+        hs[1].contributed_round = 1
+        hs[1]._fresh_gens.add(1)
+        slow_offered_1.set()
+        gen, res = hs[1].wait_blocking(1)
+        seen[(1, 1)] = res
+
+    th = [threading.Thread(target=fast), threading.Thread(target=slow)]
+    [x.start() for x in th]
+    [x.join() for x in th]
+    r0 = seen[(0, 0)]
+    assert r0.included == ka["r0_included"] and (_np(r0.u) * 2).tolist() == ka["r0_u_times_2"]
+    for rank in range(2):
+        r1 = seen[(rank, 1)]
+        assert r1.included == ka["r1_included"]
+        assert (_np(r1.u) * 2).tolist() == ka["r1_u_times_2"]
+    assert ledger.staleness_of(1, 0) == 1
+    assert ledger.staleness_of(1, 1) == 0
+    assert ledger.staleness_of(0, 0) == 0
+    assert not ledger.audit(tau=1)
+    world.close()
+
+
+@pytest.mark.parametrize("flavor", ["sync", "solo", "majority"])
+def test_replay_c1_f64_bit_exact_vs_reference(golden_dir, flavor):
+    tr = dict(np.load(os.path.join(golden_dir, f"c1_{flavor}.npz")))
+    out = replay_training(tr, element="f8")
+    assert out["accepted"].tolist() == tr["accepted"].tolist()
+    assert out["masks"].tolist() == tr["masks"].tolist()
+    assert out["w"].tobytes() == tr["final_w"].tobytes()
+    led = {(int(r), int(g)): (None if d < 0 else int(d)) for r, g, d in tr["ledger"]}
+    assert out["ledger"] == led
+
+
+@pytest.mark.parametrize("flavor", ["sync", "solo", "majority"])
+def test_replay_c1_f32_vs_oracle_and_reference(golden_dir, flavor):
+    tr = dict(np.load(os.path.join(golden_dir, f"c1_{flavor}.npz")))
+    out = replay_training(tr, element="f4")
+    want = R.replay_run(tr, np.float32)
+    assert out["w"].tobytes() == want["w"].tobytes()          # fixed order: bit-exact
+    ref = tr["final_w"]
+    rel = np.linalg.norm(out["w"].astype(np.float64) - ref) / np.linalg.norm(ref)
+    assert rel < 1e-6                                          # north_star tolerance
+
+
+def test_staleness_guard_holds_external_activation():
+    """tau=1: rank 1 has a pending gradient of round 0; an external activation of
+    round 1 is held until rank 1 itself contributes (eagersgd.py:89-110)."""
+    world = EmulatedWorld(2)
+    cfg = CollectiveConfig(p=2, flavor="solo", vector_len=4, element="f4")
+    hs = [AllreduceHandle(cfg, r, world) for r in range(2)]
+    st1 = TrainState.fresh(np.zeros(4), lr=0.1, rank=1, tau=1)
+    staleness_guard(hs[1], st1)
+    st1.send_buf.bind(hs[1])
+    st1.send_buf.fold(torch.ones(4, device="cuda"), 0)   # pending round 0
+    from paper_1908_04207_b200.eagersgd import _sync_hold
+    _sync_hold(hs[1])                                    # hold generations >= 1
+    # round 0 runs with rank 0 alone (not held: 0 + tau > 0)
+    assert hs[0]._contribute(0, np.ones(4, np.float32), True, True)
+    g, r0 = hs[0].wait_blocking(0)
+    assert r0.included == 0b01
+    # round 1: rank 0 activates, rank 1 holds
+    assert hs[0]._contribute(1, np.ones(4, np.float32), True, True)
+    time.sleep(0.05)
+    assert not hs[0].round_done(1)
+    assert hs[1]._contribute(1, np.full(4, 2.0, np.float32), True, False)
+    g, r1 = hs[0].wait_blocking(1)
+    assert r1.included == 0b11 and _np(r1.u).tolist() == [1.5] * 4
+    world.close()
