@@ -1,0 +1,406 @@
+#!/usr/bin/env python
+"""bench.py -- eager-SGD partial allreduce on B200 (BASELINE.json metric).
+
+One "step" is one eager-SGD step of the hot path over a ResNet-50-sized fp32
+gradient (N = 25,559,081, BASELINE config 2): fold the gradient into the
+device stash, offer it (stream-ordered request), solo partial allreduce over
+NVLink peer memory (persistent sm_100a engine; a plain kernel for a world of
+one), and the SGD update from the result slot.  The timed loop runs in
+all-arrive mode (every rank boards every round, nap = P), so the bus bytes
+are real and nothing is skipped.
+
+    python bench.py                                   # N=1
+    torchrun --nproc-per-node N bench.py --gpus N     # one rank per GPU
+    python bench.py --impl reference                  # CPU reference arm
+
+Rank 0 prints ONE JSON line.  `value` = aggregate eager-SGD steps/s over all
+ranks (rank-steps / max-over-ranks device time); `e2e` is the same through the
+public API with the gradient copied from pinned host memory every step.
+Extra keys: `roofline` (HBM, the dominant local kernel), `allreduce` (NVLink
+bus GB/s of the partial allreduce at 100 MB, solo and majority, N > 1),
+`imbalance` (steps/s of sync / solo / majority under the reference's seeded
+random_subset delay, N > 1), `cpu_baseline`, `clocks`, `gpu_launches`.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import sys
+import threading
+import time
+
+os.environ.setdefault("CUDA_MODULE_LOADING", "EAGER")
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+RESNET50_N = 25_559_081          # PAPER.md:664, BASELINE config 2
+ALLREDUCE_100MB_N = 25_000_000   # north_star: 100 MB fp32
+LR = 0.05
+
+
+def _env_world():
+    return (int(os.environ.get("RANK", 0)), int(os.environ.get("LOCAL_RANK", 0)),
+            int(os.environ.get("WORLD_SIZE", 1)))
+
+
+def _peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            pk = json.load(f)
+        return float(pk["hbm_gbs"]), "measured"
+    except Exception:
+        return 6650.0, "fallback"
+
+
+def _traffic(kernel: str):
+    try:
+        with open(os.path.join(ROOT, "profiles", "ncu_summary.json")) as f:
+            return json.load(f)["kernels"][kernel]["dram_bytes_per_launch"]
+    except Exception:
+        return None
+
+
+class ClockSampler:
+    """NVML clocks / throttle reasons sampled while the timed region runs."""
+
+    def __init__(self, device: int, period_s: float = 0.01):
+        self.samples, self.reasons, self.max_mhz = [], set(), None
+        self.period = period_s
+        self._stop = threading.Event()
+        try:
+            import pynvml as N
+            N.nvmlInit()
+            self.N = N
+            self.h = N.nvmlDeviceGetHandleByIndex(device)
+            self.max_mhz = N.nvmlDeviceGetMaxClockInfo(self.h, N.NVML_CLOCK_SM)
+        except Exception:
+            self.N = None
+
+    def _run(self):
+        N = self.N
+        names = {
+            "hw_slowdown": getattr(N, "nvmlClocksEventReasonHwSlowdown", 0x8),
+            "hw_thermal_slowdown": getattr(N, "nvmlClocksEventReasonHwThermalSlowdown", 0x40),
+            "sw_thermal_slowdown": getattr(N, "nvmlClocksEventReasonSwThermalSlowdown", 0x20),
+            "sw_power_cap": getattr(N, "nvmlClocksEventReasonSwPowerCap", 0x4),
+            "hw_power_brake": getattr(N, "nvmlClocksEventReasonHwPowerBrakeSlowdown", 0x80),
+        }
+        while not self._stop.is_set():
+            try:
+                self.samples.append(N.nvmlDeviceGetClockInfo(self.h, N.NVML_CLOCK_SM))
+                r = N.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+                for k, bit in names.items():
+                    if r & bit:
+                        self.reasons.add(k)
+            except Exception:
+                pass
+            time.sleep(self.period)
+
+    def __enter__(self):
+        if self.N is not None:
+            self.t = threading.Thread(target=self._run, daemon=True)
+            self.t.start()
+        return self
+
+    def __exit__(self, *exc):
+        if self.N is not None:
+            self._stop.set()
+            self.t.join()
+        return False
+
+    def summary(self):
+        import statistics
+        return {"sm_mhz": statistics.median(self.samples) if self.samples else None,
+                "sm_max_mhz": self.max_mhz, "reasons": sorted(self.reasons),
+                "samples": len(self.samples)}
+
+
+# ---------------------------------------------------------------------------
+# reference arm (CPU)
+
+
+def run_reference(args, rank, world):
+    if rank != 0:
+        return 0
+    from oracle import cpu_baseline as cb
+    p = max(1, world)
+    res = cb.time_steps(p, args.n, budget_s=args.cpu_budget, max_steps=args.steps + args.warmup)
+    line = {
+        "metric": "eager-SGD steps/s (fold + solo partial allreduce + SGD update), "
+                  "ResNet-50-sized fp32 gradient",
+        "value": res["rank_steps_per_s"], "unit": "steps/s", "n_gpus": world,
+        "steps": res["steps"], "warmup": 1, "ms_per_step": res["ms_per_step"],
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
+        "data": "synthetic",
+        "config": {"workload": f"resnet50-gradient eager-SGD step, P={p} ranks emulated on host",
+                   "n_elems": args.n, "p": p},
+        "impl": "reference",
+        "cpu_baseline": {"value": res["rank_steps_per_s"], "unit": "steps/s",
+                         "cores": res["threads"], "kind": "port",
+                         "sample": f"{res['steps']} whole steps of P={p} ranks x {args.n} fp32 "
+                                   f"({res['seconds']:.1f} s)"},
+        "e2e": {"value": res["rank_steps_per_s"], "unit": "steps/s", "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+# ---------------------------------------------------------------------------
+# our arm
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=50)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="ours", choices=("ours", "reference"))
+    ap.add_argument("--n", type=int, default=RESNET50_N)
+    ap.add_argument("--no-extras", action="store_true", help="skip allreduce/imbalance/cpu legs")
+    ap.add_argument("--cpu-budget", type=float, default=12.0)
+    ap.add_argument("--imb-unit-ms", type=float, default=1.0)
+    ap.add_argument("--imb-steps", type=int, default=32)
+    args = ap.parse_args()
+    args.warmup = max(args.warmup, 3)
+    rank, local_rank, world = _env_world()
+    if args.impl == "reference":
+        return run_reference(args, rank, world)
+
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+
+    torch.cuda.set_device(local_rank)
+    dev = torch.device("cuda", local_rank)
+    if world > 1:
+        dist.init_process_group("gloo", rank=rank, world_size=world)
+    from paper_1908_04207_b200 import (AllreduceHandle, CollectiveConfig, ProcessWorld,
+                                       TrainState, _lib, drive, train_step)
+    from paper_1908_04207_b200.transport import DelayModel, device_delay, inject_delay
+
+    pw = ProcessWorld(rank=rank, p=world, device=local_rank)
+    n = args.n
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+
+    def max_over_ranks(x: float) -> float:
+        if world == 1:
+            return x
+        t = torch.tensor([x], dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    def quiesce():
+        barrier()
+        pw.pause()
+        torch.cuda.synchronize()
+        pw.resume()
+        barrier()
+
+    gen = torch.Generator(device=dev)
+    gen.manual_seed(1234 + rank)
+    grads = [torch.randn(n, device=dev, generator=gen) for _ in range(2)]
+    w0 = torch.randn(n, device=dev, generator=gen) * 0.01
+    cfg = CollectiveConfig(p=world, flavor="solo", vector_len=n, element="f4", seed=1234)
+    h = AllreduceHandle(cfg, rank, pw, cid=0)
+    st = TrainState.fresh(w0, LR, rank=rank, tau=None)
+    all_arrive = world > 1
+
+    def step(t, timers=None, g=None):
+        return drive(train_step(st, None, h, grad=grads[t % 2] if g is None else g,
+                                all_arrive=all_arrive, timers=timers))
+
+    # ---- main timed loop: inputs resident in HBM (working set >> 126 MB L2)
+    t = 0
+    for _ in range(args.warmup):
+        step(t)
+        t += 1
+    quiesce()
+    timers: dict = {}
+    launches0 = _lib.lib.ec_launch_count()
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    naps = []
+    with ClockSampler(local_rank) as clk:
+        ev0.record()
+        for _ in range(args.steps):
+            _, res, _g = step(t, timers)
+            naps.append(res.nap)
+            t += 1
+        ev1.record()
+        ev1.synchronize()
+    launches = _lib.lib.ec_launch_count() - launches0
+    ms = ev0.elapsed_time(ev1)
+    quiesce()
+    ms_max = max_over_ranks(ms)
+    value = world * args.steps / (ms_max / 1e3)
+
+    def kernel_ms(name):
+        evs = timers.get(name, [])
+        return sum(a.elapsed_time(b) for a, b in evs) / max(1, len(evs))
+
+    upd_ms, fold_ms = kernel_ms("update"), kernel_ms("fold")
+    peak, peak_kind = _peaks()
+    upd_gbs = 12 * n / (upd_ms / 1e3) / 1e9
+    fold_bytes = 8 * n            # every round is fresh: the fold writes 0 + g into a null stash
+    fold_gbs = fold_bytes / (fold_ms / 1e3) / 1e9
+
+    # ---- e2e: gradient from pinned host memory every step, result read back
+    host_grad = torch.randn(n, generator=torch.Generator().manual_seed(7 + rank)).pin_memory()
+    dgrad = torch.empty(n, device=dev)
+    for _ in range(2):
+        dgrad.copy_(host_grad, non_blocking=True)
+        step(t, g=dgrad)
+        t += 1
+    quiesce()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e2e_steps = max(5, args.steps // 2)
+    e0.record()
+    for _ in range(e2e_steps):
+        dgrad.copy_(host_grad, non_blocking=True)
+        _, res, _g = step(t, g=dgrad)           # res.included / res.nap: read back over PCIe
+        t += 1
+    e1.record()
+    e1.synchronize()
+    quiesce()
+    e2e_ms = max_over_ranks(e0.elapsed_time(e1))
+    e2e_value = world * e2e_steps / (e2e_ms / 1e3)
+
+    extras = {}
+    if not args.no_extras and world > 1:
+        extras.update(bench_allreduce(args, pw, rank, world, dev, barrier, max_over_ranks, quiesce))
+        extras.update(bench_imbalance(args, pw, rank, world, dev, barrier, max_over_ranks, quiesce))
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_extras:
+        from oracle import cpu_baseline as cb
+        r = cb.time_steps(1, n, budget_s=args.cpu_budget, max_steps=200)
+        cpu = {"value": r["rank_steps_per_s"], "unit": "steps/s", "cores": r["threads"],
+               "kind": "port",
+               "sample": f"{r['steps']} whole P=1 steps of {n} fp32 ({r['seconds']:.1f} s, "
+                         f"oracle restatement, numpy over {r['threads']} threads)"}
+
+    if rank == 0:
+        line = {
+            "metric": "eager-SGD steps/s (fold + solo partial allreduce + SGD update), "
+                      "ResNet-50-sized fp32 gradient",
+            "value": value, "unit": "steps/s", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms_max / args.steps,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
+            "data": "synthetic",
+            "config": {"workload": "resnet50-gradient eager-SGD solo step (BASELINE config 2)",
+                       "n_elems": n, "p": world, "flavor": "solo",
+                       "mode": "all-arrive" if world > 1 else "world of one (direct)",
+                       "l2": "inputs larger than L2 (grad+stash+w+slot = 409 MB/rank)",
+                       "mean_nap": float(np.mean(naps))},
+            "e2e": {"value": e2e_value, "unit": "steps/s", "h2d_bytes_per_step": 4 * n,
+                    "d2h_bytes_per_step": 16},
+            "roofline": {"bound": "hbm", "kernel": "ec_update_kernel<float>",
+                         "achieved": upd_gbs, "peak": peak, "unit": "GB/s",
+                         "frac": upd_gbs / peak, "traffic": _traffic("update"),
+                         "bytes_per_launch": 12 * n, "avg_launch_ms": upd_ms,
+                         "peak_source": peak_kind},
+            "local_kernels": {
+                "fold": {"bytes_per_launch": fold_bytes, "avg_launch_ms": fold_ms,
+                         "gbs": fold_gbs, "frac": fold_gbs / peak, "traffic": _traffic("fold")},
+                "update": {"bytes_per_launch": 12 * n, "avg_launch_ms": upd_ms, "gbs": upd_gbs,
+                           "frac": upd_gbs / peak},
+            },
+            "cpu_baseline": cpu,
+            "clocks": clk.summary(),
+            "gpu_launches": int(launches),
+        }
+        line.update(extras)
+        print(json.dumps(line), flush=True)
+    pw.close()
+    if world > 1:
+        dist.destroy_process_group()
+    return 0
+
+
+def bench_allreduce(args, pw, rank, world, dev, barrier, max_over_ranks, quiesce):
+    """NVLink bus GB/s of the partial allreduce at 100 MB (all-arrive, nap = P):
+    busbw = 2(P-1)/P * 4N / t_round."""
+    import torch
+
+    from paper_1908_04207_b200 import AllreduceHandle, CollectiveConfig, _lib
+    n = ALLREDUCE_100MB_N
+    out = {}
+    for cid, flavor in ((10, "solo"), (11, "majority")):
+        cfg = CollectiveConfig(p=world, flavor=flavor, vector_len=n, element="f4", seed=1234)
+        h = AllreduceHandle(cfg, rank, pw, cid=cid)
+        h.send_buffer().normal_()
+        rounds = max(10, args.steps)
+
+        def rnd(t):
+            flags = _lib.EC_CF_FRESH | _lib.EC_CF_ALL_ARRIVE | \
+                (_lib.EC_CF_ACTIVATE if h._may_activate(t) else 0)
+            seq = h._post_contribute(t, flags)
+            h._reply(seq)
+            h._wait(t, 60.0, pin=False)
+
+        for t in range(3):
+            rnd(t)
+        quiesce()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        for t in range(3, 3 + rounds):
+            rnd(t)
+        e1.record()
+        e1.synchronize()
+        ms = max_over_ranks(e0.elapsed_time(e1)) / rounds
+        busbw = 2 * (world - 1) / world * 4 * n / (ms / 1e3) / 1e9
+        out[flavor] = {"busbw_gbs": busbw, "us_per_round": ms * 1e3, "bytes": 4 * n,
+                       "frac_of_900": busbw / 900.0, "frac_of_770_measured_peer": busbw / 770.0}
+        quiesce()
+    return {"allreduce": out}
+
+
+def bench_imbalance(args, pw, rank, world, dev, barrier, max_over_ranks, quiesce):
+    """Eager-SGD steps/s under the reference's seeded random_subset delay
+    (transport.py:101-149; one rank per round spins imb_unit_ms on its GPU),
+    for sync / solo / majority on the same ResNet-50-sized gradient."""
+    import numpy as np
+    import torch
+
+    from paper_1908_04207_b200 import (AllreduceHandle, CollectiveConfig, TrainState,
+                                       attach_delivery_tracking, drive, train_step)
+    from paper_1908_04207_b200.transport import DelayModel, device_delay, inject_delay
+    n = args.n
+    model = DelayModel("random_subset", unit_ms=args.imb_unit_ms, k=1, seed=11)
+    gen = torch.Generator(device=dev)
+    gen.manual_seed(99 + rank)
+    g = torch.randn(n, device=dev, generator=gen)
+    out = {"delay": {"kind": "random_subset", "unit_ms": args.imb_unit_ms, "k": 1, "seed": 11},
+           "steps": args.imb_steps}
+    for cid, flavor in ((20, "sync"), (21, "solo"), (22, "majority")):
+        cfg = CollectiveConfig(p=world, flavor=flavor, vector_len=n, element="f4", seed=1234)
+        h = AllreduceHandle(cfg, rank, pw, cid=cid)
+        st = TrainState.fresh(torch.zeros(n, device=dev), LR, rank=rank, tau=None)
+        attach_delivery_tracking(h, st)
+        naps = []
+        quiesce()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        for t in range(args.imb_steps):
+            device_delay(inject_delay(rank, t, model, world))
+            _, res, _g = drive(train_step(st, None, h, grad=g))
+            naps.append(res.nap)
+        e1.record()
+        e1.synchronize()
+        ms = max_over_ranks(e0.elapsed_time(e1))
+        out[flavor] = {"steps_per_s": world * args.imb_steps / (ms / 1e3),
+                       "mean_nap": float(np.mean(naps))}
+        quiesce()
+    base = out["sync"]["steps_per_s"]
+    for f in ("solo", "majority"):
+        out[f]["speedup_vs_sync"] = out[f]["steps_per_s"] / base
+    return {"imbalance": out}
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -57,6 +57,8 @@ typedef struct ec_comm ec_comm_t;
 /* Library identity. */
 int ec_version(void);
 const char* ec_last_error(void);
+/* Number of kernels this library has launched in the process (instrumentation). */
+uint64_t ec_launch_count(void);
 
 /* ---- communicator lifecycle ------------------------------------------------
  * Replaces AllreduceHandle.__init__ + Engine(...) + commit()
@@ -82,6 +84,8 @@ int ec_comm_start(ec_comm_t* c);
 int ec_comm_pause(ec_comm_t* c, int timeout_ms);
 int ec_comm_destroy(ec_comm_t* c);
 int ec_comm_error(ec_comm_t* c, int local_idx, uint64_t* code, uint64_t* info);
+/* Diagnostics snapshot of a local rank's engine (16 int64 words, see ec_host.cu). */
+int ec_debug_state(ec_comm_t* c, int local_idx, int64_t* out16);
 
 /* device addresses of the local rank's send buffer and of result slot `gen % R` */
 void* ec_send_ptr(ec_comm_t* c, int local_idx);

@@ -9,6 +9,21 @@ reference package `eagercoll`, behind the same Python API.  See DESIGN.md.
 
 __version__ = "0.1.0"
 
+import os as _os
+import warnings as _warnings
+
+# The persistent engine is resident while other kernels launch.  Under CUDA's
+# lazy module loading a kernel's first launch loads its code and waits for the
+# device's running kernels -- i.e. forever.  Load eagerly (must precede CUDA
+# initialisation; bench.py and the tests set it before importing torch).
+if _os.environ.get("CUDA_MODULE_LOADING") != "EAGER":
+    import torch as _torch
+    if _torch.cuda.is_initialized():
+        _warnings.warn("CUDA was initialised with lazy module loading; a kernel first "
+                       "launched while an engine runs will block. Set "
+                       "CUDA_MODULE_LOADING=EAGER before initialising CUDA.", RuntimeWarning)
+    _os.environ["CUDA_MODULE_LOADING"] = "EAGER"
+
 from .collectives import (  # noqa: E402,F401
     FLAVORS, MAJORITY, SOLO, SYNC, AllreduceHandle, CollectiveConfig, CollectiveResult,
     ceil_log2, drive, floor_pow2, initiator_for_round, run_allreduce, tree_order_sum,

@@ -32,6 +32,7 @@ _P = C.POINTER
 _SIGS = {
     "ec_version": (_i32, []),
     "ec_last_error": (C.c_char_p, []),
+    "ec_launch_count": (_u64, []),
     "ec_comm_create": (_i32, [_i32, _i32, _i32, _i32, _i64, _i32, _i32, _i32, _i32, _P(_vp)]),
     "ec_comm_export": (_i32, [_vp, _i32, _vp, C.c_size_t, _P(C.c_size_t)]),
     "ec_comm_import": (_i32, [_vp, _i32, _vp, C.c_size_t]),
@@ -40,6 +41,7 @@ _SIGS = {
     "ec_comm_pause": (_i32, [_vp, _i32]),
     "ec_comm_destroy": (_i32, [_vp]),
     "ec_comm_error": (_i32, [_vp, _i32, _P(_u64), _P(_u64)]),
+    "ec_debug_state": (_i32, [_vp, _i32, _P(_i64)]),
     "ec_send_ptr": (_vp, [_vp, _i32]),
     "ec_slot_ptr": (_vp, [_vp, _i32, _i64]),
     "ec_n_elems": (_i64, [_vp]),
@@ -75,7 +77,7 @@ def header_symbols() -> list[str]:
     """Every function the public header declares (the ABI contract)."""
     with open(HEADER) as f:
         text = f.read()
-    return sorted(set(re.findall(r"^\s*(?:int|int64_t|void\*|const char\*)\s+(ec_\w+)\s*\(",
+    return sorted(set(re.findall(r"^\s*(?:int|int64_t|uint64_t|void\*|const char\*)\s+(ec_\w+)\s*\(",
                                  text, flags=re.M)))
 
 

@@ -30,7 +30,12 @@ cudaError_t launch_reduce(int dtype, const void* const* srcs, int p, unsigned lo
 cudaError_t launch_post(EcReq* rec, unsigned long long seq1, unsigned int type, unsigned int flags,
                         long long t, long long arg, unsigned int* poison, cudaStream_t s);
 cudaError_t launch_write_u64(unsigned long long* p, unsigned long long v, cudaStream_t s);
+cudaError_t launch_direct(int dtype, const EcDesc* d_desc, long long nvec, unsigned long long seq,
+                          unsigned int type, unsigned int flags, long long t, long long arg,
+                          cudaStream_t s);
 cudaError_t launch_spin(unsigned long long ns, cudaStream_t s);
+cudaError_t preload_kernels();
+extern unsigned long long g_ec_launches;
 
 #define EC_VERSION 10000
 #define BLOB_MAGIC 0x45434231u  // "ECB1"
@@ -120,6 +125,8 @@ struct ec_comm {
   EcDesc* d_descs = nullptr;
   cudaStream_t es = nullptr;
   bool running = false;
+  bool direct = false;          // world of one rank: no persistent kernel (see ec_kernels.cu)
+  void* last_stream = nullptr;  // direct mode orders host-posted requests on it
   unsigned long long epoch = 0;
 };
 
@@ -141,6 +148,7 @@ static int device_error(EcRankHost* r) {
 extern "C" {
 
 int ec_version(void) { return EC_VERSION; }
+uint64_t ec_launch_count(void) { return __atomic_load_n(&g_ec_launches, __ATOMIC_RELAXED); }
 const char* ec_last_error(void) { return g_err.c_str(); }
 
 int ec_comm_create(int world_size, int rank_lo, int n_local, int device, int64_t n_elems,
@@ -156,6 +164,7 @@ int ec_comm_create(int world_size, int rank_lo, int n_local, int device, int64_t
   if (flavor < EC_SYNC || flavor > EC_MAJORITY) return fail(EC_E_ARG, "bad flavor %d", flavor);
   if (ring_slots < 2) return fail(EC_E_ARG, "ring_slots must be >= 2");
   CK(cudaSetDevice(device));
+  CK(preload_kernels());
   ec_comm* c = new ec_comm();
   c->P = world_size;
   c->rank_lo = rank_lo;
@@ -172,11 +181,16 @@ int ec_comm_create(int world_size, int rank_lo, int n_local, int device, int64_t
     workers_per_rank = env ? atoi(env) : 0;
   }
   if (workers_per_rank <= 0) {
-    workers_per_rank = n_local == 1 ? 64 : (144 / n_local) - 1;
-    if (workers_per_rank > 16) workers_per_rank = 16;
-    if (workers_per_rank < 1) workers_per_rank = 1;
+    if (n_local == 1) {
+      workers_per_rank = 64;
+    } else {  // emulated world: all ranks' CTA groups share one GPU
+      workers_per_rank = (144 / n_local) - 1;
+      if (workers_per_rank > 16) workers_per_rank = 16;
+      if (workers_per_rank < 1) workers_per_rank = 1;
+    }
   }
   c->W = workers_per_rank;
+  c->direct = world_size == 1 && !getenv("EC_FORCE_ENGINE");
   if (const char* env = getenv("EC_TIMEOUT_S")) c->timeout_ns = (unsigned long long)(atof(env) * 1e9);
   c->ctrl.assign(world_size, nullptr);
   c->send.assign(world_size, nullptr);
@@ -280,6 +294,7 @@ int ec_comm_set_replay(ec_comm_t* c, int li, const uint64_t* masks, int64_t n) {
   int rc = check_li(c, li);
   if (rc) return rc;
   if (c->running) return fail(EC_E_STATE, "set_replay while the engine runs");
+  if (c->direct) return fail(EC_E_STATE, "replay needs the persistent engine (world_size > 1)");
   EcRankHost* r = c->L[li];
   CK(cudaSetDevice(c->device));
   if (r->forced) {
@@ -295,9 +310,7 @@ int ec_comm_set_replay(ec_comm_t* c, int li, const uint64_t* masks, int64_t n) {
   return EC_OK;
 }
 
-int ec_comm_start(ec_comm_t* c) {
-  if (!c) return fail(EC_E_ARG, "null communicator");
-  if (c->running) return EC_OK;
+static int upload_descs(ec_comm_t* c) {
   for (int q = 0; q < c->P; ++q)
     if (!c->ctrl[q]) return fail(EC_E_STATE, "rank %d's buffers are not mapped (import first)", q);
   CK(cudaSetDevice(c->device));
@@ -331,6 +344,18 @@ int ec_comm_start(ec_comm_t* c) {
     astore(&r->h->stop, 0ull);
   }
   CK(cudaMemcpy(c->d_descs, d.data(), sizeof(EcDesc) * c->n_local, cudaMemcpyHostToDevice));
+  return EC_OK;
+}
+
+int ec_comm_start(ec_comm_t* c) {
+  if (!c) return fail(EC_E_ARG, "null communicator");
+  if (c->running) return EC_OK;
+  int rc = upload_descs(c);
+  if (rc) return rc;
+  if (c->direct) {
+    c->running = true;
+    return EC_OK;
+  }
   c->epoch += 1;
   CK(launch_engine(c->dtype, c->d_descs, c->n_local, 1 + c->W, c->epoch, c->es));
   c->running = true;
@@ -340,6 +365,10 @@ int ec_comm_start(ec_comm_t* c) {
 int ec_comm_pause(ec_comm_t* c, int timeout_ms) {
   if (!c) return fail(EC_E_ARG, "null communicator");
   if (!c->running) return EC_OK;
+  if (c->direct) {
+    c->running = false;
+    return EC_OK;
+  }
   for (EcRankHost* r : c->L) astore(&r->h->stop, 1ull);
   Backoff bo;
   for (EcRankHost* r : c->L) {
@@ -446,6 +475,13 @@ static int host_post(ec_comm_t* c, int li, unsigned type, unsigned flags, long l
   std::lock_guard<std::mutex> g(r->mu);
   unsigned long long seq;
   if ((rc = reserve_seq(c, r, &seq))) return rc;
+  if (c->direct) {
+    if (!c->running && (rc = ec_comm_start(c))) return rc;
+    CK(launch_direct(c->dtype, c->d_descs + li, c->n / (16 / c->elem), seq, type, flags, t, arg,
+                     (cudaStream_t)c->last_stream));
+    if (seq_out) *seq_out = seq;
+    return EC_OK;
+  }
   EcReq* q = &r->h->req[seq % EC_REQ_RING];
   q->type = type;
   q->flags = flags;
@@ -464,6 +500,14 @@ int ec_post_contribute(ec_comm_t* c, int li, int64_t t, uint32_t flags, void* st
   std::lock_guard<std::mutex> g(r->mu);
   unsigned long long seq;
   if ((rc = reserve_seq(c, r, &seq))) return rc;
+  if (c->direct) {
+    if (!c->running && (rc = ec_comm_start(c))) return rc;
+    c->last_stream = stream;
+    CK(launch_direct(c->dtype, c->d_descs + li, c->n / (16 / c->elem), seq, EC_REQ_CONTRIB,
+                     flags & 7u, t, 0, (cudaStream_t)stream));
+    if (seq_out) *seq_out = seq;
+    return EC_OK;
+  }
   EcReq* dq = &r->hd->req[seq % EC_REQ_RING];
   CK(launch_post(dq, seq + 1, EC_REQ_CONTRIB, flags & 7u, t, 0, &r->local->poison, (cudaStream_t)stream));
   if (seq_out) *seq_out = seq;
@@ -612,6 +656,42 @@ int ec_local_reduce(const void* const* srcs, int p, uint64_t has, void* dst, int
 
 int ec_spin(uint64_t ns, void* stream) {
   CK(launch_spin(ns, (cudaStream_t)stream));
+  return EC_OK;
+}
+
+/* Diagnostics: host-visible words, the engine stream's status and a copy of
+ * the engine's private state (read on a side stream while the engine runs).
+ * out[0..15]: done_gen1, req_done, error, error_info, exited, snap_gen1, stop,
+ * pin_lo, stream_status, L.g, L.snapped, L.contrib, L.internal_act,
+ * L.cmd_seq, L.round_done, L.next_req */
+int ec_debug_state(ec_comm_t* c, int li, int64_t* out) {
+  int rc = check_li(c, li);
+  if (rc) return rc;
+  EcRankHost* r = c->L[li];
+  out[0] = aload(&r->h->done_gen1);
+  out[1] = aload(&r->h->req_done);
+  out[2] = aload(&r->h->error);
+  out[3] = aload(&r->h->error_info);
+  out[4] = aload(&r->h->exited);
+  out[5] = aload(&r->h->snap_gen1);
+  out[6] = aload(&r->h->stop);
+  out[7] = aload(&r->h->pin_lo);
+  out[8] = c->es ? (int64_t)cudaStreamQuery(c->es) : -1;
+  EcLocal loc;
+  cudaStream_t s;
+  CK(cudaSetDevice(c->device));
+  CK(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
+  cudaError_t e = cudaMemcpyAsync(&loc, r->local, sizeof(loc), cudaMemcpyDeviceToHost, s);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+  cudaStreamDestroy(s);
+  if (e != cudaSuccess) return fail(EC_E_CUDA, "debug copy: %s", cudaGetErrorString(e));
+  out[9] = loc.g;
+  out[10] = loc.snapped;
+  out[11] = loc.contrib;
+  out[12] = loc.internal_act;
+  out[13] = (int64_t)loc.cmd_seq;
+  out[14] = (int64_t)loc.round_done;
+  out[15] = (int64_t)loc.next_req;
   return EC_OK;
 }
 

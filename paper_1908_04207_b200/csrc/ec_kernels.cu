@@ -14,6 +14,7 @@
 // buffers with ld.global.cg so it never serves a stale L1 line.
 #include <cuda_runtime.h>
 #include <stdint.h>
+#include <stdlib.h>
 
 #include "ec_common.cuh"
 #include "ec_ops.cuh"
@@ -457,6 +458,87 @@ template __global__ void ec_engine<double>(const EcDesc*, int, unsigned long lon
 template __global__ void ec_engine<long long>(const EcDesc*, int, unsigned long long);
 
 // ---------------------------------------------------------------------------
+// direct mode: a world of ONE rank.  With no peers there is no external
+// activation, no snapshot race and nothing to pull, so the controller's request
+// handling runs as a one-thread kernel in stream order and the round is an
+// ordinary grid launch right behind it: no persistent kernel holds SMs and the
+// whole step is profilable with ncu.  Same state words, replies and log as the
+// engine (EcLocal / EcHostCtl), so the host API cannot tell the difference.
+
+__global__ void ec_direct_decide(const EcDesc* __restrict__ dp, unsigned long long seq,
+                                 unsigned int type, unsigned int flags, long long t, long long arg) {
+  if (threadIdx.x != 0) return;
+  const EcDesc& d = *dp;
+  EcLocal* L = d.local;
+  EcHostCtl* H = d.hctl;
+  const long long g = L->g;
+  unsigned long long status = 3;
+  if (type == EC_REQ_CONTRIB) {
+    const unsigned int poison = *(volatile unsigned int*)&L->poison;
+    *(volatile unsigned int*)&L->poison = 0u;
+    if (poison) {
+      status = 4;
+    } else if (t < g || (t == g && L->snapped)) {
+      status = 2;
+    } else if (t > g) {
+      status = 5;
+      st_release_sys(&H->error_info, (unsigned long long)t);
+      st_release_sys(&H->error, EC_DERR_ORDER);
+    } else {
+      L->contrib = (int)(EC_SNAP_DATA | ((flags & 1u) ? EC_SNAP_FRESH : 0ull));
+      L->contributed_round = t;
+      status = 1;
+      if (flags & 2u) L->snapped = 1;  // own activation: P == 1, everyone has arrived
+    }
+  } else if (type == EC_REQ_ACTIVATE) {
+    if (t == g) L->snapped = 1;
+  } else if (type == EC_REQ_HOLD) {
+    L->hold_from = arg;
+  }
+  __threadfence();
+  st_release_sys(&H->reply[seq % EC_REQ_RING], ((seq + 1) << 8) | status);
+  st_release_sys(&H->req_done, seq + 1);
+}
+
+template <typename T>
+__global__ void __launch_bounds__(256)
+ec_direct_round(const EcDesc* __restrict__ dp) {
+  const EcDesc& d = *dp;
+  EcLocal* L = d.local;
+  if (!*(volatile int*)&L->snapped) return;   // nothing activated: no round
+  const long long g = L->g;
+  const int contrib = L->contrib;
+  const unsigned long long has = (contrib & (int)EC_SNAP_DATA) ? 1ull : 0ull;
+  char* slot = d.ring[d.rank] + (g % d.R) * d.slot_bytes;
+  const long long start = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  const long long stride = (long long)gridDim.x * blockDim.x;
+  rs_fixed<T, 1, 4>(d, has, 0, d.nvec, slot, start, stride, (T)1, true);
+  if (blockIdx.x == 0 && threadIdx.x < Ops<T>::V) rs_tail<T>(d, has, slot, threadIdx.x);
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence();
+    const unsigned long long old = atomicAdd(&L->rs_count, 1ull);
+    if (old + 1 == gridDim.x) {
+      L->rs_count = 0;
+      EcHostCtl* H = d.hctl;
+      const unsigned long long fresh = (contrib & (int)EC_SNAP_FRESH) ? 1ull : 0ull;
+      EcLog* lg = &H->log[g % EC_LOG_RING];
+      st_relaxed_sys(&lg->mask, fresh);
+      st_relaxed_sys(&lg->has, has);
+      st_relaxed_sys(&lg->nap, fresh);
+      st_release_sys(&lg->gen1, (unsigned long long)g + 1);
+      if (fresh) L->hold_from = EC_INF_GEN;
+      L->g = g + 1;
+      L->snapped = 0;
+      L->contrib = 0;
+      __threadfence();
+      st_release_sys(&H->snap_gen1, (unsigned long long)g + 1);
+      st_release_sys(&H->done_gen1, (unsigned long long)g + 1);
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
 // standalone streaming kernels
 
 template <typename T, int MODE>
@@ -679,12 +761,42 @@ __global__ void ec_spin_kernel(unsigned long long ns) {
 // ---------------------------------------------------------------------------
 // host-side launch helpers (C++ linkage, used by ec_host.cu)
 
+// Launches issued by this library (bench.py reports the count for its timed region).
+unsigned long long g_ec_launches = 0;
+static inline void counted(int n = 1) { __atomic_add_fetch(&g_ec_launches, (unsigned long long)n, __ATOMIC_RELAXED); }
+
 static inline int grid_for(long long work, int threads) {
   long long b = (work + threads - 1) / threads;
   const long long cap = 148LL * 8;
   if (b > cap) b = cap;
   if (b < 1) b = 1;
   return (int)b;
+}
+
+// Force-load every kernel of this library.  With CUDA lazy loading a kernel's
+// first launch loads its code, and that load waits for running kernels -- which
+// never happens while the persistent engine is resident.  Called before the
+// engine first starts.
+cudaError_t preload_kernels() {
+  const void* fns[] = {
+      (const void*)ec_engine<float>, (const void*)ec_engine<double>, (const void*)ec_engine<long long>,
+      (const void*)ec_fold_kernel<float, 0>, (const void*)ec_fold_kernel<float, 1>,
+      (const void*)ec_fold_kernel<double, 0>, (const void*)ec_fold_kernel<double, 1>,
+      (const void*)ec_fold_kernel<long long, 0>, (const void*)ec_fold_kernel<long long, 1>,
+      (const void*)ec_update_kernel<float>, (const void*)ec_update_kernel<double>,
+      (const void*)ec_momentum_kernel<float>, (const void*)ec_momentum_kernel<double>,
+      (const void*)ec_reduce_kernel<float>, (const void*)ec_reduce_kernel<double>,
+      (const void*)ec_reduce_kernel<long long>,
+      (const void*)ec_direct_decide, (const void*)ec_direct_round<float>,
+      (const void*)ec_direct_round<double>, (const void*)ec_direct_round<long long>,
+      (const void*)ec_post_kernel, (const void*)ec_write_u64_kernel, (const void*)ec_spin_kernel,
+  };
+  for (const void* f : fns) {
+    cudaFuncAttributes a;
+    cudaError_t e = cudaFuncGetAttributes(&a, f);
+    if (e != cudaSuccess) return e;
+  }
+  return cudaSuccess;
 }
 
 cudaError_t launch_engine(int dtype, const EcDesc* d_descs, int n_local, int blocks_per_rank,
@@ -694,11 +806,14 @@ cudaError_t launch_engine(int dtype, const EcDesc* d_descs, int n_local, int blo
   const void* fn = dtype == 0 ? (const void*)ec_engine<float>
                   : dtype == 1 ? (const void*)ec_engine<double>
                                : (const void*)ec_engine<long long>;
+  counted();
+  if (getenv("EC_NONCOOP")) return cudaLaunchKernel(fn, grid, block, args, 0, s);
   return cudaLaunchCooperativeKernel(fn, grid, block, args, 0, s);
 }
 
 cudaError_t launch_fold(int dtype, void* stash, const void* grad, long long n, int mode,
                         unsigned int* nonfinite, cudaStream_t s) {
+  counted();
   const int vec_ok = ((((uintptr_t)stash) | ((uintptr_t)grad)) & 15) == 0;
   const int V = dtype == 0 ? 4 : 2;
   const int grid = grid_for((n / V + 3) / 4 + 1, 256);
@@ -716,6 +831,7 @@ cudaError_t launch_fold(int dtype, void* stash, const void* grad, long long n, i
 }
 
 cudaError_t launch_update(int dtype, void* w, const void* u, double lr, long long n, cudaStream_t s) {
+  counted();
   const int vec_ok = ((((uintptr_t)w) | ((uintptr_t)u)) & 15) == 0;
   const int V = dtype == 0 ? 4 : 2;
   const int grid = grid_for((n / V + 3) / 4 + 1, 256);
@@ -727,6 +843,7 @@ cudaError_t launch_update(int dtype, void* w, const void* u, double lr, long lon
 
 cudaError_t launch_momentum(int dtype, void* w, void* buf, const void* u, double lr, double mu,
                             long long n, cudaStream_t s) {
+  counted();
   const int vec_ok = ((((uintptr_t)w) | ((uintptr_t)u) | ((uintptr_t)buf)) & 15) == 0;
   const int V = dtype == 0 ? 4 : 2;
   const int grid = grid_for(n / V + 1, 256);
@@ -738,6 +855,7 @@ cudaError_t launch_momentum(int dtype, void* w, void* buf, const void* u, double
 
 cudaError_t launch_reduce(int dtype, const void* const* srcs, int p, unsigned long long has, void* dst,
                           long long n, int div, cudaStream_t s) {
+  counted();
   EcSrcs S;
   uintptr_t bits = (uintptr_t)dst;
   for (int q = 0; q < EC_MAX_P; ++q) {
@@ -755,16 +873,32 @@ cudaError_t launch_reduce(int dtype, const void* const* srcs, int p, unsigned lo
 
 cudaError_t launch_post(EcReq* rec, unsigned long long seq1, unsigned int type, unsigned int flags,
                         long long t, long long arg, unsigned int* poison, cudaStream_t s) {
+  counted();
   ec_post_kernel<<<1, 32, 0, s>>>(rec, seq1, type, flags, t, arg, poison);
   return cudaGetLastError();
 }
 
+cudaError_t launch_direct(int dtype, const EcDesc* d_desc, long long nvec, unsigned long long seq,
+                          unsigned int type, unsigned int flags, long long t, long long arg,
+                          cudaStream_t s) {
+  counted(type == EC_REQ_HOLD ? 1 : 2);
+  ec_direct_decide<<<1, 32, 0, s>>>(d_desc, seq, type, flags, t, arg);
+  if (type == EC_REQ_HOLD) return cudaGetLastError();
+  const int grid = grid_for((nvec + 3) / 4 + 1, 256);
+  if (dtype == 0) ec_direct_round<float><<<grid, 256, 0, s>>>(d_desc);
+  else if (dtype == 1) ec_direct_round<double><<<grid, 256, 0, s>>>(d_desc);
+  else ec_direct_round<long long><<<grid, 256, 0, s>>>(d_desc);
+  return cudaGetLastError();
+}
+
 cudaError_t launch_write_u64(unsigned long long* p, unsigned long long v, cudaStream_t s) {
+  counted();
   ec_write_u64_kernel<<<1, 32, 0, s>>>(p, v);
   return cudaGetLastError();
 }
 
 cudaError_t launch_spin(unsigned long long ns, cudaStream_t s) {
+  counted();
   ec_spin_kernel<<<1, 32, 0, s>>>(ns);
   return cudaGetLastError();
 }

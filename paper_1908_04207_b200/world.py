@@ -154,12 +154,32 @@ class _WorldBase:
             comm.start()
 
     def close(self) -> None:
-        for comm in list(self.comms.values()):
+        # Park every engine before freeing anything: cudaFree synchronises the
+        # whole device and would wait forever on a still-resident engine.
+        comms = list(self.comms.values())
+        for comm in comms:
+            try:
+                comm.pause(10000)
+            except Exception:
+                pass
+        for comm in comms:
             try:
                 comm.close()
             except Exception:
                 pass
         self.comms.clear()
+
+    def _new_comm(self, cfg, rank_lo: int, n_local: int) -> "Comm":
+        """Create a communicator with the world's engines parked (allocation and
+        IPC registration may synchronise the device)."""
+        running = [c for c in self.comms.values() if c.running]
+        for c in running:
+            c.pause()
+        try:
+            return Comm(self, cfg, rank_lo, n_local)
+        finally:
+            for c in running:
+                c.start()
 
     def quiesced(self):
         """Context manager: engines parked inside (device-wide syncs are safe)."""
@@ -203,7 +223,7 @@ class EmulatedWorld(_WorldBase):
         with self._lock:
             comm = self.comms.get(cid)
             if comm is None:
-                comm = Comm(self, cfg, 0, self.p)
+                comm = self._new_comm(cfg, 0, self.p)
                 self.comms[cid] = comm
                 self._attached[cid] = set()
             elif comm.cfg != cfg:
@@ -249,7 +269,7 @@ class ProcessWorld(_WorldBase):
             raise ValueError(f"config p={cfg.p} does not match world size {self.p}")
         if cid in self.comms:
             raise ValueError(f"cid {cid} already has a handle in this process")
-        comm = Comm(self, cfg, self.rank, 1)
+        comm = self._new_comm(cfg, self.rank, 1)
         blobs = self._all_gather(comm.export(0))
         for q, blob in enumerate(blobs):
             comm.import_peer(q, blob)

@@ -8,7 +8,10 @@ vectors, host-side logic, the C-ABI export check and world_size-2 gloo tests.
 import os
 import sys
 
-import pytest
+# before anything initialises CUDA (see paper_1908_04207_b200/__init__.py)
+os.environ.setdefault("CUDA_MODULE_LOADING", "EAGER")
+
+import pytest  # noqa: E402
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 if ROOT not in sys.path:
