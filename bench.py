@@ -356,7 +356,7 @@ def bench_allreduce(args, pw, rank, world, dev, barrier, max_over_ranks, quiesce
         busbw = 2 * (world - 1) / world * 4 * n / (ms / 1e3) / 1e9
         out[flavor] = {"busbw_gbs": busbw, "us_per_round": ms * 1e3, "bytes": 4 * n,
                        "frac_of_900": busbw / 900.0, "frac_of_770_measured_peer": busbw / 770.0}
-        quiesce()
+        h.close()
     return {"allreduce": out}
 
 
@@ -395,7 +395,7 @@ def bench_imbalance(args, pw, rank, world, dev, barrier, max_over_ranks, quiesce
         ms = max_over_ranks(e0.elapsed_time(e1))
         out[flavor] = {"steps_per_s": world * args.imb_steps / (ms / 1e3),
                        "mean_nap": float(np.mean(naps))}
-        quiesce()
+        h.close()
     base = out["sync"]["steps_per_s"]
     for f in ("solo", "majority"):
         out[f]["speedup_vs_sync"] = out[f]["steps_per_s"] / base

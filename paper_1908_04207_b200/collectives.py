@@ -175,6 +175,11 @@ class AllreduceHandle:
         self._hold_posted = _lib.INT64_MAX
         self._pinned = False
 
+    def close(self) -> None:
+        """Destroy this collective instance on every rank of the world (the
+        engines park first; collective for a ProcessWorld)."""
+        self.transport.release(self.cid)
+
     # -- buffers ------------------------------------------------------------
     def send_buffer(self) -> torch.Tensor:
         """The device send buffer (also the eager-SGD stash, eagersgd.py:68)."""

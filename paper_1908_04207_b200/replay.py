@@ -25,97 +25,111 @@ from .trace import DeliveryLedger
 from .world import EmulatedWorld
 
 
-def replay_training(trace, element: str = "f4", device: int = 0, world=None, ring_slots: int = 4):
-    """Replay a c1_<flavor> trace (tests/golden) on an emulated world.
-
-    trace: mapping with p, steps, epochs, steps_per_epoch, lr, resync_period,
-    masks[g], accepted[r, t], observed[r, t], grads[r, t, :], w0.
-    Returns dict(w=[p, dim] final weights (numpy), accepted=[p, steps],
-    ledger=dict, masks=[steps] observed device masks).
-    """
-    p = int(trace["p"])
+def replay_rank(r: int, h: AllreduceHandle, resync_h: AllreduceHandle, st: TrainState, trace,
+                grads_r: torch.Tensor, ledger, acc: np.ndarray, seen_masks: np.ndarray) -> None:
+    """One rank's replayed training loop (training_process, eagersgd.py:187-226,
+    with the offers' outcomes and the observed generations forced by `trace`)."""
     steps = int(trace["steps"])
     epochs = int(trace["epochs"])
     spe = int(trace["steps_per_epoch"])
     period = int(trace["resync_period"])
-    lr = float(trace["lr"])
+    observed = np.asarray(trace["observed"]).astype(np.int64)
+    attach_delivery_tracking(h, st, ledger)
+    k = 0
+    for e in range(epochs):
+        for s in range(spe):
+            t = e * spe + s
+            ledger.generated(r, t)
+            with h.engine.lock:
+                st.send_buf.bind(h)
+                st.send_buf.fold(grads_r[t], t)
+                seq = h._post_contribute(t, _lib.EC_CF_FRESH)
+            if h._reply(seq) == _lib.R_ACCEPTED:
+                acc[r, t] = 1
+                h.contributed_round = t
+                h._fresh_gens.add(t)
+            g = int(observed[r, t])
+            h._wait(g, 60.0, pin=False)
+            m = _gen_mask(h, g)
+            if seen_masks[g] == 0:
+                seen_masks[g] = m
+            elif seen_masks[g] != m:
+                raise AssertionError(f"generation {g}: rank {r} saw mask {m:#x}, "
+                                     f"another rank {int(seen_masks[g]):#x}")
+            apply_update(st, h._slot(g))
+            nxt = int(observed[r, t + 1]) if t + 1 < steps else _lib.UINT64_MAX
+            call("ec_set_pin", h.comm.ptr, h.li, nxt, 1,
+                 torch.cuda.current_stream(h.device).cuda_stream)
+            st.t = t + 1
+        if (e + 1) % period == 0:
+            drive(resync_step(st, resync_h, k))
+            k += 1
+    torch.cuda.current_stream(h.device).synchronize()
+
+
+def replay_configs(trace, element: str):
+    p = int(trace["p"])
+    dim = np.asarray(trace["grads"]).shape[-1]
+    return (CollectiveConfig(p=p, flavor="solo", vector_len=dim, element=element, seed=0),
+            CollectiveConfig(p=p, flavor="sync", vector_len=dim, element=element))
+
+
+def replay_training(trace, element: str = "f4", device: int = 0, world=None, ring_slots: int = 4):
+    """Replay a c1_<flavor> trace (tests/golden) on an emulated world (P ranks,
+    P host threads, one GPU).
+
+    trace: mapping with p, steps, epochs, steps_per_epoch, lr, resync_period,
+    masks[g], accepted[r, t], observed[r, t], grads[r, t, :], w0.
+    Returns dict(w=[p, dim] final weights (numpy), accepted=[p, steps],
+    ledger=dict, masks=[steps] device masks).
+    """
+    p = int(trace["p"])
+    steps = int(trace["steps"])
     masks = [int(m) for m in np.asarray(trace["masks"])]
     observed = np.asarray(trace["observed"]).astype(np.int64)
-    grads_np = np.asarray(trace["grads"])
-    dim = grads_np.shape[-1]
-    cfg = CollectiveConfig(p=p, flavor="solo", vector_len=dim, element=element, seed=0)
-    sync_cfg = CollectiveConfig(p=p, flavor="sync", vector_len=dim, element=element)
+    cfg, sync_cfg = replay_configs(trace, element)
     own = world is None
     world = world or EmulatedWorld(p, device, ring_slots=ring_slots)
     handles = [AllreduceHandle(cfg, r, world, cid=0) for r in range(p)]
     resync = [AllreduceHandle(sync_cfg, r, world, cid=1) for r in range(p)]
     for r in range(p):
         handles[r].comm.set_replay(r, masks)
+        call("ec_set_pin", handles[r].comm.ptr, r, int(observed[r, 0]), 0, None)
     dtype = cfg.torch_dtype
     dev = f"cuda:{device}"
-    grads = torch.as_tensor(grads_np, dtype=dtype, device=dev)
-    w0 = np.asarray(trace["w0"])
+    grads = torch.as_tensor(np.asarray(trace["grads"]), dtype=dtype, device=dev)
+    w0 = torch.as_tensor(np.asarray(trace["w0"]), dtype=dtype, device=dev)
     ledger = DeliveryLedger()
-    states = [TrainState.fresh(torch.as_tensor(w0, dtype=dtype, device=dev), lr, rank=r,
-                               resync_period=period, tau=None) for r in range(p)]
+    states = [TrainState.fresh(w0, float(trace["lr"]), rank=r,
+                               resync_period=int(trace["resync_period"]), tau=None)
+              for r in range(p)]
     acc = np.zeros((p, steps), dtype=np.int8)
     seen_masks = np.zeros(steps, dtype=np.int64)
     errors: list = []
-    for r in range(p):
-        call("ec_set_pin", handles[r].comm.ptr, r, int(observed[r, 0]), 0, None)
     go = threading.Barrier(p)
 
-    def rank_body(r: int):
+    def body(r: int):
         try:
-            h, st = handles[r], states[r]
-            attach_delivery_tracking(h, st, ledger)
             torch.cuda.set_device(device)
             go.wait()
-            k = 0
-            for e in range(epochs):
-                for s in range(spe):
-                    t = e * spe + s
-                    ledger.generated(r, t)
-                    with h.engine.lock:
-                        st.send_buf.bind(h)
-                        st.send_buf.fold(grads[r, t], t)
-                        seq = h._post_contribute(t, _lib.EC_CF_FRESH)
-                    status = h._reply(seq)
-                    if status == _lib.R_ACCEPTED:
-                        acc[r, t] = 1
-                        h.contributed_round = t
-                        h._fresh_gens.add(t)
-                    g = int(observed[r, t])
-                    gen, mask, nap = h._wait(g, 60.0, pin=False)
-                    info_mask = _gen_mask(h, g)
-                    if r == 0 or seen_masks[g] == 0:
-                        seen_masks[g] = info_mask
-                    apply_update(st, h._slot(g))
-                    nxt = int(observed[r, t + 1]) if t + 1 < steps else _lib.UINT64_MAX
-                    call("ec_set_pin", h.comm.ptr, h.li, nxt, 1,
-                         torch.cuda.current_stream(device).cuda_stream)
-                    st.t = t + 1
-                if (e + 1) % period == 0:
-                    drive(resync_step(st, resync[r], k))
-                    k += 1
-            torch.cuda.current_stream(device).synchronize()
+            replay_rank(r, handles[r], resync[r], states[r], trace, grads[r], ledger, acc,
+                        seen_masks)
         except BaseException as ex:  # surfaced below
             errors.append(ex)
 
-    threads = [threading.Thread(target=rank_body, args=(r,), daemon=True) for r in range(p)]
+    threads = [threading.Thread(target=body, args=(r,), daemon=True) for r in range(p)]
     for th in threads:
         th.start()
     for th in threads:
         th.join()
-    if errors:
+    try:
+        if errors:
+            raise errors[0]
+        w = np.stack([st.w.detach().cpu().numpy() for st in states])
+        return {"w": w, "accepted": acc, "ledger": ledger.as_dict(), "masks": seen_masks}
+    finally:
         if own:
             world.close()
-        raise errors[0]
-    w = np.stack([st.w.detach().cpu().numpy() for st in states])
-    out = {"w": w, "accepted": acc, "ledger": ledger.as_dict(), "masks": seen_masks}
-    if own:
-        world.close()
-    return out
 
 
 def _gen_mask(h: AllreduceHandle, g: int) -> int:

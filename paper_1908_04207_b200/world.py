@@ -169,6 +169,28 @@ class _WorldBase:
                 pass
         self.comms.clear()
 
+    def release(self, cid: int) -> None:
+        """Destroy one collective instance.  Every engine of the world parks first
+        (cudaFree synchronises the device); collective in a ProcessWorld."""
+        comm = self.comms.get(cid)
+        if comm is None:
+            return
+        running = [c for c in self.comms.values() if c.running and c is not comm]
+        self.pause()
+        self._barrier()
+        comm.close()
+        del self.comms[cid]
+        self._release_attached(cid)
+        self._barrier()
+        for c in running:
+            c.start()
+
+    def _barrier(self) -> None:
+        pass
+
+    def _release_attached(self, cid: int) -> None:
+        pass
+
     def _new_comm(self, cfg, rank_lo: int, n_local: int) -> "Comm":
         """Create a communicator with the world's engines parked (allocation and
         IPC registration may synchronise the device)."""
@@ -233,6 +255,9 @@ class EmulatedWorld(_WorldBase):
             self._attached[cid].add(rank)
         return comm, rank
 
+    def _release_attached(self, cid: int) -> None:
+        self._attached.pop(cid, None)
+
 
 class ProcessWorld(_WorldBase):
     """One rank per process/GPU; peers mapped over NVLink with CUDA IPC."""
@@ -261,6 +286,9 @@ class ProcessWorld(_WorldBase):
     def barrier(self) -> None:
         if self.p > 1:
             self.dist.barrier(group=self.group)
+
+    def _barrier(self) -> None:
+        self.barrier()
 
     def attach(self, cfg, cid: int, rank: int):
         if rank != self.rank:

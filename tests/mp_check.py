@@ -1,0 +1,203 @@
+"""Multi-GPU parity checks, one rank per GPU over NVLink (run under torchrun).
+
+    torchrun --nproc-per-node P --master-addr 127.0.0.1 tests/mp_check.py
+
+Each check compares the ProcessWorld path (CUDA IPC peer mapping + persistent
+engine per GPU) with the CPU oracle / the reference's golden outputs.  Rank 0
+prints one JSON object with every check's outcome; the exit code is non-zero
+if any check failed on any rank.  Driven by tests/test_multigpu.py.
+"""
+
+import json
+import os
+import sys
+import time
+import traceback
+
+os.environ.setdefault("CUDA_MODULE_LOADING", "EAGER")
+os.environ.setdefault("EC_TIMEOUT_S", "30")
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+import torch  # noqa: E402
+import torch.distributed as dist  # noqa: E402
+
+
+def main():
+    rank = int(os.environ["RANK"])
+    world = int(os.environ["WORLD_SIZE"])
+    local = int(os.environ.get("LOCAL_RANK", rank))
+    torch.cuda.set_device(local)
+    dist.init_process_group("gloo")
+    from oracle import restated as R
+    from paper_1908_04207_b200 import (AllreduceHandle, CollectiveConfig, ProcessWorld,
+                                       TrainState, drive, initiator_for_round, train_step)
+    from paper_1908_04207_b200.replay import replay_configs, replay_rank
+    from paper_1908_04207_b200.trace import DeliveryLedger
+    from paper_1908_04207_b200 import _lib
+    from paper_1908_04207_b200._lib import call
+
+    pw = ProcessWorld()
+    results = {}
+    cid = [100]
+
+    def next_cid():
+        cid[0] += 1
+        return cid[0]
+
+    def check(name, fn):
+        try:
+            out = fn()
+            results[name] = {"ok": True, **(out or {})}
+        except Exception as e:
+            results[name] = {"ok": False, "error": f"{type(e).__name__}: {e}",
+                             "tb": traceback.format_exc()[-1500:]}
+        dist.barrier()
+
+    golden = np.load(os.path.join(ROOT, "tests", "golden", "tree_sums.npz"))
+
+    def sync_f64_golden():
+        contrib = golden[f"sync_in_p{world}"]
+        cfg = CollectiveConfig(p=world, flavor="sync", vector_len=8, element="f8")
+        h = AllreduceHandle(cfg, rank, pw, cid=next_cid())
+        for t in range(3):
+            res = drive(h.call_round(t, contrib[rank]))
+            assert res.nap == world and res.rnd == t
+            assert res.u.cpu().numpy().tobytes() == golden[f"sync_u_p{world}"].tobytes()
+        h.close()
+
+    def sync_f32_sizes():
+        for n in (1, 7, 1027, 2_000_003, 25_559_081):
+            rng = np.random.default_rng(world * 31 + n)
+            contrib = rng.standard_normal((world, n), dtype=np.float32)
+            want, inc, _ = R.allreduce_round(list(contrib), [True] * world, np.float32)
+            cfg = CollectiveConfig(p=world, flavor="sync", vector_len=n, element="f4")
+            h = AllreduceHandle(cfg, rank, pw, cid=next_cid())
+            vec = torch.as_tensor(contrib[rank], device="cuda")
+            for t in range(2):
+                res = drive(h.call_round(t, vec))
+                assert res.included == inc
+                assert res.u.cpu().numpy().tobytes() == want.tobytes(), f"n={n} t={t}"
+            h.close()
+
+    def solo_first_arrival():
+        cfg = CollectiveConfig(p=world, flavor="solo", vector_len=1000, element="f4")
+        h = AllreduceHandle(cfg, rank, pw, cid=next_cid())
+        contrib = np.random.default_rng(1).standard_normal((world, 1000), dtype=np.float32)
+        dist.barrier()
+        time.sleep(0.05 * rank)
+        res = drive(h.call_round(0, contrib[rank]))
+        want, _, _ = R.allreduce_round([contrib[0]] + [None] * (world - 1),
+                                       [True] + [False] * (world - 1), np.float32)
+        h.close()
+        assert res.included == 1, f"mask {res.included:#x}"
+        assert res.u.cpu().numpy().tobytes() == want.tobytes()
+        return {"included": res.included}
+
+    def majority_prefix():
+        seeds = []
+        for seed in (31, 32, 33, 34):
+            cfg = CollectiveConfig(p=world, flavor="majority", vector_len=16, element="f8", seed=seed)
+            h = AllreduceHandle(cfg, rank, pw, cid=next_cid())
+            dist.barrier()
+            time.sleep(0.05 * rank)
+            res = drive(h.call_round(0, np.full(16, 10.0 * rank)))
+            h.close()
+            init = initiator_for_round(seed, 0, world)
+            assert res.included == (1 << (init + 1)) - 1, (seed, init, res.included)
+            vecs = [np.full(16, 10.0 * r) if r <= init else None for r in range(world)]
+            want, _, _ = R.allreduce_round(vecs, [v is not None for v in vecs])
+            assert res.u.cpu().numpy().tobytes() == want.tobytes()
+            seeds.append((seed, init, res.included))
+        return {"seeds": seeds}
+
+    def eager_sgd_all_arrive():
+        n, lr = 1_000_003, 0.05
+        rng = np.random.default_rng(5)
+        grads = rng.standard_normal((3, world, n), dtype=np.float32)
+        w0 = rng.standard_normal(n, dtype=np.float32)
+        cfg = CollectiveConfig(p=world, flavor="solo", vector_len=n, element="f4")
+        h = AllreduceHandle(cfg, rank, pw, cid=next_cid())
+        st = TrainState.fresh(w0, lr, rank=rank, tau=None)
+        from paper_1908_04207_b200.eagersgd import attach_delivery_tracking
+        attach_delivery_tracking(h, st)
+        w = w0.copy()
+        for t in range(3):
+            g = torch.as_tensor(grads[t, rank], device="cuda")
+            _, res, gen = drive(train_step(st, None, h, grad=g, all_arrive=True))
+            assert gen == t and res.nap == world
+            u, _, _ = R.allreduce_round(list(grads[t]), [True] * world, np.float32)
+            w = R.sgd_update(w, u, lr)
+        h.close()
+        assert st.w.cpu().numpy().tobytes() == w.tobytes()
+
+    def replay_c1():
+        if world != 4:
+            return {"skipped": f"c1 traces have p=4, world={world}"}
+        out = {}
+        for flavor in ("sync", "solo", "majority"):
+            for element in ("f8", "f4"):
+                tr = dict(np.load(os.path.join(ROOT, "tests", "golden", f"c1_{flavor}.npz")))
+                cfg, sync_cfg = replay_configs(tr, element)
+                h = AllreduceHandle(cfg, rank, pw, cid=next_cid())
+                hr = AllreduceHandle(sync_cfg, rank, pw, cid=next_cid())
+                pw.pause()
+                h.comm.set_replay(0, [int(m) for m in tr["masks"]])
+                call("ec_set_pin", h.comm.ptr, 0, int(tr["observed"][rank, 0]), 0, None)
+                pw.resume()
+                dt = cfg.torch_dtype
+                grads = torch.as_tensor(tr["grads"][rank], dtype=dt, device="cuda")
+                st = TrainState.fresh(torch.as_tensor(tr["w0"], dtype=dt, device="cuda"),
+                                      float(tr["lr"]), rank=rank,
+                                      resync_period=int(tr["resync_period"]), tau=None)
+                steps = int(tr["steps"])
+                acc = np.zeros((4, steps), np.int8)
+                masks = np.zeros(steps, np.int64)
+                ledger = DeliveryLedger()
+                dist.barrier()
+                replay_rank(rank, h, hr, st, tr, grads, ledger, acc, masks)
+                h.close()
+                hr.close()
+                assert acc[rank].tolist() == tr["accepted"][rank].tolist()
+                seen = masks != 0
+                assert masks[seen].tolist() == tr["masks"][seen].tolist()
+                w = st.w.cpu().numpy()
+                if element == "f8":
+                    assert w.tobytes() == tr["final_w"][rank].tobytes(), f"{flavor} f64"
+                else:
+                    want = R.replay_run(tr, np.float32)["w"][rank]
+                    assert w.tobytes() == want.tobytes(), f"{flavor} f32"
+                led = {(int(r), int(g)): (None if d < 0 else int(d)) for r, g, d in tr["ledger"]
+                       if int(r) == rank}
+                assert ledger.as_dict() == led
+                out[f"{flavor}_{element}"] = "bit-exact"
+        return out
+
+    check("sync_f64_golden", sync_f64_golden)
+    check("sync_f32_sizes", sync_f32_sizes)
+    check("solo_first_arrival", solo_first_arrival)
+    check("majority_prefix", majority_prefix)
+    check("eager_sgd_all_arrive", eager_sgd_all_arrive)
+    check("replay_c1", replay_c1)
+
+    gathered = [None] * world
+    dist.all_gather_object(gathered, results)
+    ok = all(all(v["ok"] for v in r.values()) for r in gathered)
+    if rank == 0:
+        summary = {"world": world, "ok": ok,
+                   "checks": {k: {"ok": all(g[k]["ok"] for g in gathered),
+                                  **{kk: vv for kk, vv in gathered[0][k].items() if kk != "ok"}}
+                              for k in results}}
+        failures = {f"r{r}:{k}": v for r, g in enumerate(gathered) for k, v in g.items()
+                    if not v["ok"]}
+        if failures:
+            summary["failures"] = failures
+        print(json.dumps(summary, indent=1), flush=True)
+    pw.close()
+    dist.destroy_process_group()
+    return 0 if ok else 1
+
+
+if __name__ == "__main__":
+    sys.exit(main())
