@@ -120,6 +120,10 @@ int ec_wait(ec_comm_t* c, int local_idx, int64_t t, int timeout_ms, int pin,
 /* Mask / nap of an earlier generation from the device log (RoundRecord source). */
 int ec_gen_info(ec_comm_t* c, int local_idx, int64_t gen, uint64_t* mask,
                 uint64_t* has_data, int* nap);
+/* Device timestamps (%globaltimer ns) of a completed generation at this rank:
+ * t4 = {snapshot taken, reduction issued (all snapshots in), own shard reduced,
+ * published}. */
+int ec_gen_times(ec_comm_t* c, int local_idx, int64_t gen, uint64_t* t4);
 /* Lowest generation the host may still read: the engine never overwrites the
  * slot of generation h unless h < pin_lo.  ordered != 0 performs the store in
  * `stream` order (release after the update kernel read the slot); ordered == 0

@@ -55,6 +55,7 @@ _SIGS = {
     "ec_wait": (_i32, [_vp, _i32, _i64, _i32, _i32, _P(_i64), _P(_u64), _P(_i32)]),
     "ec_gen_info": (_i32, [_vp, _i32, _i64, _P(_u64), _P(_u64), _P(_i32)]),
     "ec_set_pin": (_i32, [_vp, _i32, _u64, _i32, _vp]),
+    "ec_gen_times": (_i32, [_vp, _i32, _i64, _P(_u64)]),
     "ec_fold_raw": (_i32, [_vp, _vp, _i64, _i32, _i32, _P(_u32), _vp]),
     "ec_sgd_update": (_i32, [_vp, _vp, C.c_double, _i64, _i32, _vp]),
     "ec_momentum_update": (_i32, [_vp, _vp, _vp, C.c_double, C.c_double, _i64, _i32, _vp]),

@@ -40,6 +40,7 @@ struct alignas(128) EcCtrl {
   unsigned long long snap_from[EC_MAX_P];    // snapshot word of source rank
   unsigned long long rsdone_from[EC_MAX_P];  // gen+1: source's reduced shard ready
   unsigned long long arrive_from[EC_MAX_P];  // gen+1: source boarded (all-arrive)
+  unsigned long long done_from[EC_MAX_P];    // gen+1: source's data for gen is in our slot
 };
 
 struct alignas(128) EcLocal {
@@ -66,8 +67,11 @@ struct alignas(128) EcLocal {
   int arrive_pending;              // all-arrive: activate once everyone boarded
   int arrive_activate;
   int initialized;
+  unsigned long long t_snap;       // globaltimer at this generation's snapshot
+  unsigned long long t_rs;         // globaltimer when the last worker finished its shard
   unsigned int poison;             // fold's non-finite flag (device word)
   int pad4;
+  unsigned long long posted;       // doorbell: highest stream-posted request seq + 1
 };
 
 struct alignas(64) EcReq {
@@ -79,11 +83,14 @@ struct alignas(64) EcReq {
   unsigned long long pad[4];
 };
 
-struct alignas(32) EcLog {
+struct alignas(64) EcLog {
   unsigned long long gen1;
   unsigned long long mask;
   unsigned long long has;
   unsigned long long nap;
+  // %globaltimer (ns) of this rank's engine: snapshot taken, round command
+  // issued (all snapshots in), own shard reduced, round published
+  unsigned long long t_snap, t_cmd, t_rs, t_done;
 };
 
 struct alignas(128) EcHostCtl {
@@ -105,6 +112,9 @@ struct alignas(128) EcHostCtl {
 struct EcDesc {
   int rank, P, flavor, dtype;
   int R, W, replay, vec;              // ring slots, worker CTAs, replay flag, elems / 16 B
+  int mode;                           // data phase: 0 = fused TMA, 1 = two-phase ld.cg pull
+  int chv, stages;                    // TMA chunk (16-B vectors) and pipeline depth
+  int smem_bytes;
   long long n, nvec;                  // elements, whole 16-B vectors
   long long slot_bytes;
   long long n_forced;

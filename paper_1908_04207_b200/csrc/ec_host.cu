@@ -19,7 +19,7 @@
 
 // launchers (ec_kernels.cu)
 cudaError_t launch_engine(int dtype, const EcDesc* d_descs, int n_local, int blocks_per_rank,
-                          unsigned long long epoch, cudaStream_t s);
+                          unsigned long long epoch, int smem_bytes, cudaStream_t s);
 cudaError_t launch_fold(int dtype, void* stash, const void* grad, long long n, int mode,
                         unsigned int* nonfinite, cudaStream_t s);
 cudaError_t launch_update(int dtype, void* w, const void* u, double lr, long long n, cudaStream_t s);
@@ -28,7 +28,8 @@ cudaError_t launch_momentum(int dtype, void* w, void* buf, const void* u, double
 cudaError_t launch_reduce(int dtype, const void* const* srcs, int p, unsigned long long has,
                           void* dst, long long n, int div, cudaStream_t s);
 cudaError_t launch_post(EcReq* rec, unsigned long long seq1, unsigned int type, unsigned int flags,
-                        long long t, long long arg, unsigned int* poison, cudaStream_t s);
+                        long long t, long long arg, unsigned int* poison,
+                        unsigned long long* doorbell, cudaStream_t s);
 cudaError_t launch_write_u64(unsigned long long* p, unsigned long long v, cudaStream_t s);
 cudaError_t launch_direct(int dtype, const EcDesc* d_desc, long long nvec, unsigned long long seq,
                           unsigned int type, unsigned int flags, long long t, long long arg,
@@ -128,6 +129,7 @@ struct ec_comm {
   bool direct = false;          // world of one rank: no persistent kernel (see ec_kernels.cu)
   void* last_stream = nullptr;  // direct mode orders host-posted requests on it
   unsigned long long epoch = 0;
+  int mode = 0, chv = 256, stages = 4, smem_bytes = 0;  // data phase (see EcDesc)
 };
 
 static int check_li(ec_comm_t* c, int li) {
@@ -181,8 +183,9 @@ int ec_comm_create(int world_size, int rank_lo, int n_local, int device, int64_t
     workers_per_rank = env ? atoi(env) : 0;
   }
   if (workers_per_rank <= 0) {
+    const bool ldg = getenv("EC_DATA") && strcmp(getenv("EC_DATA"), "ldg") == 0;
     if (n_local == 1) {
-      workers_per_rank = 64;
+      workers_per_rank = ldg ? 128 : 32;
     } else {  // emulated world: all ranks' CTA groups share one GPU
       workers_per_rank = (144 / n_local) - 1;
       if (workers_per_rank > 16) workers_per_rank = 16;
@@ -191,6 +194,22 @@ int ec_comm_create(int world_size, int rank_lo, int n_local, int device, int64_t
   }
   c->W = workers_per_rank;
   c->direct = world_size == 1 && !getenv("EC_FORCE_ENGINE");
+  // Data phase: fused TMA (default) or two-phase ld.cg pull (EC_DATA=ldg).
+  // TMA geometry: P source slices + 1 output slice per stage, `stages` deep,
+  // within ~150 KB of shared memory.
+  c->mode = (getenv("EC_DATA") && strcmp(getenv("EC_DATA"), "ldg") == 0) ? 1 : 0;
+  {
+    int chb = world_size <= 12 ? 4096 : 1024;
+    if (const char* e = getenv("EC_CHUNK")) chb = atoi(e);
+    int st = (150 * 1024) / ((world_size + 1) * chb);
+    if (st > 4) st = 4;
+    if (const char* e = getenv("EC_STAGES")) st = atoi(e);
+    if (st < 2) st = 2;
+    if (st > 8) st = 8;
+    c->chv = chb / 16;
+    c->stages = st;
+    c->smem_bytes = c->mode == 0 ? st * (world_size + 1) * chb : 0;
+  }
   if (const char* env = getenv("EC_TIMEOUT_S")) c->timeout_ns = (unsigned long long)(atof(env) * 1e9);
   c->ctrl.assign(world_size, nullptr);
   c->send.assign(world_size, nullptr);
@@ -333,6 +352,10 @@ static int upload_descs(ec_comm_t* c) {
     x.slot_bytes = c->slot_bytes;
     x.n_forced = r->n_forced;
     x.timeout_ns = c->timeout_ns;
+    x.mode = c->mode;
+    x.chv = c->chv;
+    x.stages = c->stages;
+    x.smem_bytes = c->smem_bytes;
     for (int q = 0; q < c->P; ++q) {
       x.ctrl[q] = c->ctrl[q];
       x.send[q] = c->send[q];
@@ -357,7 +380,7 @@ int ec_comm_start(ec_comm_t* c) {
     return EC_OK;
   }
   c->epoch += 1;
-  CK(launch_engine(c->dtype, c->d_descs, c->n_local, 1 + c->W, c->epoch, c->es));
+  CK(launch_engine(c->dtype, c->d_descs, c->n_local, 1 + c->W, c->epoch, c->smem_bytes, c->es));
   c->running = true;
   return EC_OK;
 }
@@ -509,7 +532,8 @@ int ec_post_contribute(ec_comm_t* c, int li, int64_t t, uint32_t flags, void* st
     return EC_OK;
   }
   EcReq* dq = &r->hd->req[seq % EC_REQ_RING];
-  CK(launch_post(dq, seq + 1, EC_REQ_CONTRIB, flags & 7u, t, 0, &r->local->poison, (cudaStream_t)stream));
+  CK(launch_post(dq, seq + 1, EC_REQ_CONTRIB, flags & 7u, t, 0, &r->local->poison,
+                 &r->local->posted, (cudaStream_t)stream));
   if (seq_out) *seq_out = seq;
   return EC_OK;
 }
@@ -567,6 +591,24 @@ int ec_gen_info(ec_comm_t* c, int li, int64_t gen, uint64_t* mask, uint64_t* has
   if (mask) *mask = m;
   if (has) *has = hm;
   if (nap) *nap = (int)np;
+  return EC_OK;
+}
+
+int ec_gen_times(ec_comm_t* c, int li, int64_t gen, uint64_t* t4) {
+  int rc = check_li(c, li);
+  if (rc) return rc;
+  EcRankHost* r = c->L[li];
+  if (gen < 0 || (long long)aload(&r->h->done_gen1) <= gen)
+    return fail(EC_E_STATE, "generation %lld has not completed", (long long)gen);
+  EcLog* lg = &r->h->log[gen % EC_LOG_RING];
+  unsigned long long g1 = aload(&lg->gen1);
+  t4[0] = aload(&lg->t_snap);
+  t4[1] = aload(&lg->t_cmd);
+  t4[2] = aload(&lg->t_rs);
+  t4[3] = aload(&lg->t_done);
+  __atomic_thread_fence(__ATOMIC_ACQUIRE);
+  if (aload(&lg->gen1) != g1 || g1 != (unsigned long long)gen + 1)
+    return fail(EC_E_STATE, "generation %lld fell out of the log", (long long)gen);
   return EC_OK;
 }
 

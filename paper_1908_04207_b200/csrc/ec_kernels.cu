@@ -119,22 +119,292 @@ __device__ __forceinline__ long long shard_lo(long long nvec, int q, int P) {
   return (long long)(((unsigned long long)nvec * (unsigned long long)q) / (unsigned long long)P);
 }
 
+// ---------------------------------------------------------------------------
+// TMA helpers (1-D bulk copies; peer addresses work through the UVA window)
+
+__device__ __forceinline__ unsigned smem_u32(const void* p) {
+  return (unsigned)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ void mbar_init(unsigned long long* b, unsigned count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" :: "r"(smem_u32(b)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(unsigned long long* b, unsigned bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;"
+               :: "r"(smem_u32(b)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ bool mbar_try_wait(unsigned long long* b, unsigned parity) {
+  unsigned ok;
+  asm volatile("{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n"
+               " selp.u32 %0, 1, 0, p;\n}" : "=r"(ok) : "r"(smem_u32(b)), "r"(parity) : "memory");
+  return ok != 0;
+}
+__device__ __forceinline__ void tma_load(void* sdst, const void* gsrc, unsigned bytes,
+                                         unsigned long long* bar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+               :: "r"(smem_u32(sdst)), "l"(gsrc), "r"(bytes), "r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void tma_store(void* gdst, const void* ssrc, unsigned bytes) {
+  asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;"
+               :: "l"(gdst), "r"(smem_u32(ssrc)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void tma_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void tma_wait_read() {
+  asm volatile("cp.async.bulk.wait_group.read %0;" :: "n"(N) : "memory");
+}
+// allow the n most recent store groups to still be reading shared memory
+__device__ __forceinline__ void tma_wait_read_n(int n) {
+  switch (n) {
+    case 0: tma_wait_read<0>(); break;
+    case 1: tma_wait_read<1>(); break;
+    case 2: tma_wait_read<2>(); break;
+    case 3: tma_wait_read<3>(); break;
+    case 4: tma_wait_read<4>(); break;
+    case 5: tma_wait_read<5>(); break;
+    case 6: tma_wait_read<6>(); break;
+    default: tma_wait_read<7>(); break;
+  }
+}
+__device__ __forceinline__ void tma_wait_all() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
+__device__ __forceinline__ void fence_proxy_async_smem() {
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+__device__ __forceinline__ void fence_proxy_async_global() {
+  asm volatile("fence.proxy.async.global;" ::: "memory");
+}
+
+// TMA data phase geometry (host and device agree): chunks of `chv` 16-byte
+// vectors, `stages` deep, P source slices + 1 output slice per stage.
+__device__ __forceinline__ long long chunk_lo(long long nch, int q, int P) {
+  return (long long)(((unsigned long long)nch * (unsigned long long)q) / (unsigned long long)P);
+}
+
+template <typename T, int P>
+__device__ __forceinline__ void reduce_chunk_smem(const char* src, char* out, int nvv, int chb,
+                                                  unsigned long long has, int p, T inv, bool pow2) {
+  constexpr int V = Ops<T>::V;
+  for (int i = threadIdx.x; i < nvv; i += blockDim.x) {
+    Vec16<T> x[P];
+#pragma unroll
+    for (int q = 0; q < P; ++q)
+      x[q].raw = ((has >> q) & 1ull) ? *reinterpret_cast<const uint4*>(src + (size_t)q * chb + i * 16)
+                                     : make_uint4(0, 0, 0, 0);
+    Vec16<T> o;
+#pragma unroll
+    for (int l = 0; l < V; ++l) {
+      T c[P];
+#pragma unroll
+      for (int q = 0; q < P; ++q) c[q] = Ops<T>::canon(x[q].e[l]);
+      o.e[l] = Ops<T>::divp(tree_sum<T, P>(c), p, inv, pow2);
+    }
+    *reinterpret_cast<uint4*>(out + i * 16) = o.raw;
+  }
+}
+
+template <typename T>
+__device__ void reduce_chunk_smem_dyn(const char* src, char* out, int nvv, int chb,
+                                      unsigned long long has, int p, T inv, bool pow2) {
+  constexpr int V = Ops<T>::V;
+  for (int i = threadIdx.x; i < nvv; i += blockDim.x) {
+    Vec16<T> o;
+#pragma unroll
+    for (int l = 0; l < V; ++l) {
+      auto leaf = [&](int q) -> T {
+        if (!((has >> q) & 1ull)) return Ops<T>::zero();
+        Vec16<T> x;
+        x.raw = *reinterpret_cast<const uint4*>(src + (size_t)q * chb + i * 16);
+        return Ops<T>::canon(x.e[l]);
+      };
+      o.e[l] = Ops<T>::divp(tree_sum_dyn<T>(p, leaf), p, inv, pow2);
+    }
+    *reinterpret_cast<uint4*>(out + i * 16) = o.raw;
+  }
+}
+
+template <typename T>
+__device__ __forceinline__ void reduce_chunk(const char* src, char* out, int nvv, int chb,
+                                             unsigned long long has, int p) {
+  const bool pow2 = (p & (p - 1)) == 0;
+  const T inv = (T)1 / (T)p;
+  switch (p) {
+    case 1: reduce_chunk_smem<T, 1>(src, out, nvv, chb, has, p, inv, pow2); break;
+    case 2: reduce_chunk_smem<T, 2>(src, out, nvv, chb, has, p, inv, pow2); break;
+    case 3: reduce_chunk_smem<T, 3>(src, out, nvv, chb, has, p, inv, pow2); break;
+    case 4: reduce_chunk_smem<T, 4>(src, out, nvv, chb, has, p, inv, pow2); break;
+    case 5: reduce_chunk_smem<T, 5>(src, out, nvv, chb, has, p, inv, pow2); break;
+    case 6: reduce_chunk_smem<T, 6>(src, out, nvv, chb, has, p, inv, pow2); break;
+    case 7: reduce_chunk_smem<T, 7>(src, out, nvv, chb, has, p, inv, pow2); break;
+    case 8: reduce_chunk_smem<T, 8>(src, out, nvv, chb, has, p, inv, pow2); break;
+    default: reduce_chunk_smem_dyn<T>(src, out, nvv, chb, has, p, inv, pow2); break;
+  }
+}
+
+// One round of the fused TMA data phase for CTA w of this rank:
+//   for each chunk of MY shard: bulk-load the chunk from every contributing
+//   rank's send buffer (peer memory, NVLink) into shared memory, reduce it in
+//   tree order, then bulk-store the result into EVERY rank's result slot
+//   (reduce-scatter pull and all-gather push, pipelined per chunk).
+template <typename T>
+__device__ void round_tma(const EcDesc& d, int w, long long g, unsigned long long has,
+                          char* smem, unsigned long long* full, unsigned long long& it) {
+  const int P = d.P, r = d.rank, S = d.stages;
+  const int chv = d.chv, chb = d.chv * 16;
+  const long long nch = (d.nvec + chv - 1) / chv;
+  const long long c0 = chunk_lo(nch, r, P), c1 = chunk_lo(nch, r + 1, P);
+  const long long mine = (c1 - c0 > w) ? (c1 - c0 - w + d.W - 1) / d.W : 0;
+  const long long off = (g % d.R) * d.slot_bytes;
+  const size_t stage_bytes = (size_t)(P + 1) * chb;
+  const unsigned npop = (unsigned)__popcll(has);
+  auto issue = [&](long long k) {  // thread 0: loads of my k-th chunk
+    const int s = (int)((it + k) % S);
+    const long long c = c0 + w + k * d.W;
+    const long long v0 = c * chv;
+    const unsigned bytes = (unsigned)(min((long long)chv, d.nvec - v0) * 16);
+    char* st = smem + s * stage_bytes;
+    mbar_expect_tx(&full[s], npop * bytes);
+    for (int q = 0; q < P; ++q)
+      if ((has >> q) & 1ull) tma_load(st + (size_t)q * chb, d.send[q] + v0 * 16, bytes, &full[s]);
+  };
+  if (threadIdx.x == 0) {
+    fence_proxy_async_global();  // peers' generic writes (acquired via flags) -> async-proxy reads
+    for (long long k = 0; k < mine && k < S; ++k) issue(k);
+  }
+  for (long long k = 0; k < mine; ++k) {
+    const int s = (int)((it + k) % S);
+    const unsigned parity = (unsigned)(((it + k) / S) & 1ull);
+    const long long c = c0 + w + k * d.W;
+    const long long v0 = c * chv;
+    const int nvv = (int)min((long long)chv, d.nvec - v0);
+    char* st = smem + s * stage_bytes;
+    char* out = st + (size_t)P * chb;
+    // the out slice of stage s was last stored from S chunks ago; the S-1 newer
+    // store groups may still be in flight
+    if (threadIdx.x == 0) tma_wait_read_n(S - 1);
+    while (!mbar_try_wait(&full[s], parity)) {
+    }
+    __syncthreads();
+    reduce_chunk<T>(st, out, nvv, chb, has, P);
+    fence_proxy_async_smem();
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      for (int j = 0; j < P; ++j) {
+        const int q = (r + j) % P;  // own slot first, then peers round-robin
+        tma_store(d.ring[q] + off + v0 * 16, out, (unsigned)nvv * 16);
+      }
+      tma_commit();
+      if (k + S < mine) issue(k + S);
+    }
+  }
+  it += (unsigned long long)mine;
+  if (threadIdx.x == 0) {
+    tma_wait_all();
+    fence_proxy_async_global();
+  }
+}
+
+// scalar tail (n % V elements): reduced by the last owner, pushed to every slot
+template <typename T>
+__device__ void tail_push(const EcDesc& d, unsigned long long has, long long g) {
+  const long long e = d.nvec * Ops<T>::V + threadIdx.x;
+  if (threadIdx.x >= Ops<T>::V || e >= d.n) return;
+  const bool pow2 = (d.P & (d.P - 1)) == 0;
+  const T inv = (T)1 / (T)d.P;
+  auto leaf = [&](int q) -> T {
+    if (!((has >> q) & 1ull)) return Ops<T>::zero();
+    const volatile T* s = reinterpret_cast<const volatile T*>(d.send[q]);
+    return Ops<T>::canon(s[e]);
+  };
+  const T u = Ops<T>::divp(tree_sum_dyn<T>(d.P, leaf), d.P, inv, pow2);
+  const long long off = (g % d.R) * d.slot_bytes;
+  for (int q = 0; q < d.P; ++q) reinterpret_cast<volatile T*>(d.ring[q] + off)[e] = u;
+}
+
+// Two-phase pull data path (ld.global.cg): reduce-scatter, then all-gather.
+template <typename T>
+__device__ void round_ldg(const EcDesc& d, int w, long long g, unsigned long long has,
+                          unsigned long long seen) {
+  EcLocal* L = d.local;
+  EcCtrl* C = d.ctrl[d.rank];
+  const int tid = threadIdx.x;
+  const long long bt = blockDim.x;
+  char* my_slot = d.ring[d.rank] + (g % d.R) * d.slot_bytes;
+  const long long off = (g % d.R) * d.slot_bytes;
+  {
+    const long long v0 = shard_lo(d.nvec, d.rank, d.P), v1 = shard_lo(d.nvec, d.rank + 1, d.P);
+    rs_shard<T>(d, has, v0, v1, my_slot, (long long)w * bt + tid, (long long)d.W * bt);
+    if (d.rank == d.P - 1 && w == 0 && tid < Ops<T>::V) rs_tail<T>(d, has, my_slot, tid);
+  }
+  __syncthreads();
+  if (tid == 0) {
+    __threadfence();
+    unsigned long long old = atomicAdd(&L->rs_count, 1ull);
+    if (old + 1 == (unsigned long long)d.W * seen) {
+      fence_acq_rel_sys();
+      for (int q = 0; q < d.P; ++q) st_release_sys(&d.ctrl[q]->rsdone_from[d.rank], (unsigned long long)g + 1);
+      L->t_rs = globaltimer_ns();
+    }
+    const unsigned long long t0 = globaltimer_ns();
+    for (int q = 0; q < d.P; ++q) {
+      while (ld_acquire_sys(&C->rsdone_from[q]) < (unsigned long long)g + 1) {
+        if (globaltimer_ns() - t0 > d.timeout_ns) {
+          st_release_sys(&d.hctl->error_info, 0x100 + q);
+          st_release_sys(&d.hctl->error, EC_DERR_TIMEOUT);
+          break;
+        }
+      }
+    }
+  }
+  __syncthreads();
+  constexpr int U = 4;
+  const long long start = (long long)w * bt + tid, stride = (long long)d.W * bt;
+  for (int k = 1; k < d.P; ++k) {
+    const int q = (d.rank + k) % d.P;
+    const char* src = d.ring[q] + off;
+    const long long v0 = shard_lo(d.nvec, q, d.P), v1 = shard_lo(d.nvec, q + 1, d.P);
+    for (long long base = v0 + start; base < v1; base += stride * U) {
+      uint4 x[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        long long v = base + (long long)u * stride;
+        if (v < v1) x[u] = ld_cg_v4(src + v * 16);
+      }
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        long long v = base + (long long)u * stride;
+        if (v < v1) st_v4(my_slot + v * 16, x[u]);
+      }
+    }
+  }
+  if (d.rank != d.P - 1 && w == 0 && tid < Ops<T>::V) {
+    const long long e = d.nvec * Ops<T>::V + tid;
+    if (e < d.n) {
+      const volatile T* s = reinterpret_cast<const volatile T*>(d.ring[d.P - 1] + off);
+      reinterpret_cast<T*>(my_slot)[e] = s[e];
+    }
+  }
+}
+
 template <typename T>
 __device__ void engine_worker(const EcDesc& d, int w, unsigned long long epoch) {
   EcLocal* L = d.local;
-  EcCtrl* C = d.ctrl[d.rank];
+  extern __shared__ __align__(128) char smem[];
+  __shared__ __align__(8) unsigned long long full[8];
   __shared__ unsigned long long s_seq, s_has;
   __shared__ long long s_gen;
   __shared__ int s_exit;
   const int tid = threadIdx.x;
-  const long long bt = blockDim.x;
-  if (tid == 0) s_seq = ld_acquire_gpu(&L->cmd_seq);
+  if (tid == 0) {
+    s_seq = ld_acquire_gpu(&L->cmd_seq);
+    for (int s = 0; s < d.stages; ++s) mbar_init(&full[s], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
   __syncthreads();
   unsigned long long seen = s_seq;
+  unsigned long long it = 0;  // chunks this CTA has pipelined (stage / parity)
   __syncthreads();
   while (true) {
     if (tid == 0) {
-      unsigned ns = 64;
+      unsigned ns = 32;
       while (true) {
         unsigned long long s = ld_acquire_gpu(&L->cmd_seq);
         if (s != seen) {
@@ -149,7 +419,7 @@ __device__ void engine_worker(const EcDesc& d, int w, unsigned long long epoch) 
           break;
         }
         __nanosleep(ns);
-        if (ns < 2048) ns <<= 1;
+        if (ns < 256) ns <<= 1;
       }
     }
     __syncthreads();
@@ -157,73 +427,27 @@ __device__ void engine_worker(const EcDesc& d, int w, unsigned long long epoch) 
     seen = s_seq;
     const long long g = s_gen;
     const unsigned long long has = s_has;
-    char* my_slot = d.ring[d.rank] + (g % d.R) * d.slot_bytes;
-    const long long off = (g % d.R) * d.slot_bytes;
-
-    // ---- reduce-scatter: my shard, read from every rank's send buffer
-    {
-      const long long v0 = shard_lo(d.nvec, d.rank, d.P), v1 = shard_lo(d.nvec, d.rank + 1, d.P);
-      rs_shard<T>(d, has, v0, v1, my_slot, (long long)w * bt + tid, (long long)d.W * bt);
-      if (d.rank == d.P - 1 && w == 0 && tid < Ops<T>::V) rs_tail<T>(d, has, my_slot, tid);
+    if (d.mode == 0) {
+      round_tma<T>(d, w, g, has, smem, full, it);
+      if (w == 0 && d.rank == d.P - 1) tail_push<T>(d, has, g);
+    } else {
+      round_ldg<T>(d, w, g, has, seen);
     }
     __syncthreads();
     if (tid == 0) {
       fence_acq_rel_sys();
-      unsigned long long old = atomicAdd(&L->rs_count, 1ull);
+      const unsigned long long old = atomicAdd(&L->ag_count, 1ull);
       if (old + 1 == (unsigned long long)d.W * seen) {
+        // every CTA of this rank is done: tell the world (TMA mode: our pushes
+        // into every slot have landed) / ourselves (pull mode)
         fence_acq_rel_sys();
-        for (int q = 0; q < d.P; ++q) st_release_sys(&d.ctrl[q]->rsdone_from[d.rank], (unsigned long long)g + 1);
-      }
-      // ---- all-gather: wait for every owner's shard
-      const unsigned long long t0 = globaltimer_ns();
-      unsigned ns = 32;
-      for (int q = 0; q < d.P; ++q) {
-        while (ld_acquire_sys(&C->rsdone_from[q]) < (unsigned long long)g + 1) {
-          if (globaltimer_ns() - t0 > d.timeout_ns) {
-            st_release_sys(&d.hctl->error, EC_DERR_TIMEOUT);
-            st_release_sys(&d.hctl->error_info, 0x100 + q);
-            break;
-          }
-          __nanosleep(ns);
-          if (ns < 1024) ns <<= 1;
+        if (d.mode == 0) {
+          L->t_rs = globaltimer_ns();
+          for (int q = 0; q < d.P; ++q) st_release_sys(&d.ctrl[q]->done_from[d.rank], (unsigned long long)g + 1);
+        } else {
+          st_release_sys(&d.ctrl[d.rank]->done_from[d.rank], (unsigned long long)g + 1);
         }
       }
-    }
-    __syncthreads();
-    {
-      constexpr int U = 4;
-      const long long start = (long long)w * bt + tid, stride = (long long)d.W * bt;
-      for (int k = 1; k < d.P; ++k) {
-        const int q = (d.rank + k) % d.P;
-        const char* src = d.ring[q] + off;
-        const long long v0 = shard_lo(d.nvec, q, d.P), v1 = shard_lo(d.nvec, q + 1, d.P);
-        for (long long base = v0 + start; base < v1; base += stride * U) {
-          uint4 x[U];
-#pragma unroll
-          for (int u = 0; u < U; ++u) {
-            long long v = base + (long long)u * stride;
-            if (v < v1) x[u] = ld_cg_v4(src + v * 16);
-          }
-#pragma unroll
-          for (int u = 0; u < U; ++u) {
-            long long v = base + (long long)u * stride;
-            if (v < v1) st_v4(my_slot + v * 16, x[u]);
-          }
-        }
-      }
-      if (d.rank != d.P - 1 && w == 0 && tid < Ops<T>::V) {
-        const long long e = d.nvec * Ops<T>::V + tid;
-        if (e < d.n) {
-          const volatile T* s = reinterpret_cast<const volatile T*>(d.ring[d.P - 1] + off);
-          reinterpret_cast<T*>(my_slot)[e] = s[e];
-        }
-      }
-    }
-    __syncthreads();
-    if (tid == 0) {
-      __threadfence();
-      unsigned long long old = atomicAdd(&L->ag_count, 1ull);
-      if (old + 1 == (unsigned long long)d.W * seen) st_release_gpu(&L->round_done, seen);
     }
   }
 }
@@ -249,6 +473,7 @@ __device__ void engine_controller(const EcDesc& d, unsigned long long epoch) {
   unsigned long long seq = L->cmd_seq;
   bool stopping = false;
   unsigned long long stop_t0 = 0;
+  unsigned long long t_snap = L->t_snap;
   unsigned ns = 32;
 
   // write this rank's word into every rank's control block (peer stores over NVLink)
@@ -270,14 +495,20 @@ __device__ void engine_controller(const EcDesc& d, unsigned long long epoch) {
     return (int)((d.forced[gen] >> r) & 1ull);
   };
 
+  unsigned iter = 0;
   while (true) {
     bool progress = false;
-    if (!stopping && ld_relaxed_sys(&H->stop)) {
+    // Host-mapped words cost a PCIe round trip: poll them when the device
+    // doorbell (bumped by every stream-posted request) says so, and otherwise
+    // only every 16th pass (host-posted requests, stop).
+    ++iter;
+    const bool poll_host = (iter & 15u) == 0 || ld_acquire_gpu(&L->posted) > next_req;
+    if (poll_host && !stopping && ld_relaxed_sys(&H->stop)) {
       stopping = true;
       stop_t0 = globaltimer_ns();
     }
     // ---- requests, strictly in sequence order
-    while (true) {
+    while (poll_host) {
       EcReq* q = &H->req[next_req % EC_REQ_RING];
       if (ld_acquire_sys(&q->seq1) != next_req + 1) break;
       const unsigned type = ld_relaxed_sys_u32(&q->type);
@@ -346,8 +577,16 @@ __device__ void engine_controller(const EcDesc& d, unsigned long long epoch) {
           go = !held;
         }
       }
+      if (go && g >= d.R) {
+        // Result-slot reuse guard: peers write our slot g % R once the round
+        // starts, so never snapshot g while the host still reads generation
+        // g - R (pin_lo <= g - R).  SC fence pairs with ec_wait's pin store.
+        fence_sc_sys();
+        if (ld_acquire_sys(&H->pin_lo) <= (unsigned long long)(g - d.R)) go = false;
+      }
       if (go) {
         push_all(1, (((unsigned long long)g + 1) << 2) | (unsigned long long)contrib);
+        t_snap = globaltimer_ns();
         st_release_sys(&H->snap_gen1, (unsigned long long)g + 1);
         if (contrib & (int)EC_SNAP_FRESH) hold_from = EC_INF_GEN;  // stash delivered (eagersgd.py:117-124)
         snapped = 1;
@@ -365,43 +604,36 @@ __device__ void engine_controller(const EcDesc& d, unsigned long long epoch) {
         has |= ((w >> 1) & 1ull) << q;
       }
       if (all) {
-        // result-slot reuse guard: never overwrite generation h = g - R while h >= pin_lo
         bool timed_out = false;
-        if (g >= d.R) {
-          fence_sc_sys();
-          const unsigned long long tp = globaltimer_ns();
-          unsigned ns2 = 32;
-          while (ld_acquire_sys(&H->pin_lo) <= (unsigned long long)(g - d.R)) {
-            if (globaltimer_ns() - tp > d.timeout_ns) { timed_out = true; break; }
-            __nanosleep(ns2);
-            if (ns2 < 1024) ns2 <<= 1;
-          }
-        }
-        if (timed_out) {
-          st_release_sys(&H->error_info, (unsigned long long)g | (1ull << 62));
-          st_release_sys(&H->error, EC_DERR_TIMEOUT);
-          break;
-        }
         L->cmd_gen = g;
         L->cmd_has = has;
         ++seq;
-        st_release_gpu(&L->cmd_seq, seq);
         const unsigned long long t0 = globaltimer_ns();
+        st_release_gpu(&L->cmd_seq, seq);
         unsigned ns3 = 32;
-        while (ld_acquire_gpu(&L->round_done) != seq) {
-          if (globaltimer_ns() - t0 > d.timeout_ns) { timed_out = true; break; }
-          __nanosleep(ns3);
-          if (ns3 < 256) ns3 <<= 1;
+        // round complete at this rank: TMA mode needs every owner's pushes into
+        // our slot, pull mode only our own all-gather
+        for (int q = (d.mode == 0 ? 0 : r); q < (d.mode == 0 ? P : r + 1) && !timed_out; ++q) {
+          while (ld_acquire_sys(&C->done_from[q]) < (unsigned long long)g + 1) {
+            if (globaltimer_ns() - t0 > d.timeout_ns) { timed_out = true; break; }
+            __nanosleep(ns3);
+            if (ns3 < 128) ns3 <<= 1;
+          }
         }
         if (timed_out) {
           st_release_sys(&H->error_info, (unsigned long long)g);
           st_release_sys(&H->error, EC_DERR_TIMEOUT);
           break;
         }
+        const unsigned long long t_done = globaltimer_ns();
         EcLog* lg = &H->log[g % EC_LOG_RING];
         st_relaxed_sys(&lg->mask, fresh);
         st_relaxed_sys(&lg->has, has);
         st_relaxed_sys(&lg->nap, (unsigned long long)__popcll(fresh));
+        st_relaxed_sys(&lg->t_snap, t_snap);
+        st_relaxed_sys(&lg->t_cmd, t0);
+        st_relaxed_sys(&lg->t_rs, *(volatile unsigned long long*)&L->t_rs);
+        st_relaxed_sys(&lg->t_done, t_done);
         st_release_sys(&lg->gen1, (unsigned long long)g + 1);
         st_release_sys(&H->done_gen1, (unsigned long long)g + 1);
         ++g;
@@ -435,6 +667,7 @@ __device__ void engine_controller(const EcDesc& d, unsigned long long epoch) {
   L->internal_act = internal_act;
   L->arrive_pending = arrive_pending;
   L->arrive_activate = arrive_activate;
+  L->t_snap = t_snap;
   __threadfence();
   st_release_gpu(&L->exit_epoch, epoch);
   st_release_sys(&H->exited, epoch);
@@ -526,6 +759,11 @@ ec_direct_round(const EcDesc* __restrict__ dp) {
       st_relaxed_sys(&lg->mask, fresh);
       st_relaxed_sys(&lg->has, has);
       st_relaxed_sys(&lg->nap, fresh);
+      const unsigned long long tn = globaltimer_ns();
+      st_relaxed_sys(&lg->t_snap, tn);
+      st_relaxed_sys(&lg->t_cmd, tn);
+      st_relaxed_sys(&lg->t_rs, tn);
+      st_relaxed_sys(&lg->t_done, tn);
       st_release_sys(&lg->gen1, (unsigned long long)g + 1);
       if (fresh) L->hold_from = EC_INF_GEN;
       L->g = g + 1;
@@ -730,7 +968,7 @@ ec_reduce_kernel(EcSrcs s, int p, unsigned long long has, T* __restrict__ dst, l
 
 __global__ void ec_post_kernel(EcReq* rec, unsigned long long seq1, unsigned int type,
                                unsigned int flags, long long t, long long arg,
-                               unsigned int* poison) {
+                               unsigned int* poison, unsigned long long* doorbell) {
   if (threadIdx.x != 0) return;
   if (poison) {
     if (*(volatile unsigned int*)poison) flags |= EC_CF_POISON;
@@ -743,6 +981,7 @@ __global__ void ec_post_kernel(EcReq* rec, unsigned long long seq1, unsigned int
   v->arg = arg;
   fence_acq_rel_sys();
   st_release_sys(&rec->seq1, seq1);
+  if (doorbell) atomicMax(doorbell, seq1);
 }
 
 __global__ void ec_write_u64_kernel(unsigned long long* p, unsigned long long v) {
@@ -800,15 +1039,17 @@ cudaError_t preload_kernels() {
 }
 
 cudaError_t launch_engine(int dtype, const EcDesc* d_descs, int n_local, int blocks_per_rank,
-                          unsigned long long epoch, cudaStream_t s) {
+                          unsigned long long epoch, int smem_bytes, cudaStream_t s) {
   void* args[] = {(void*)&d_descs, (void*)&blocks_per_rank, (void*)&epoch};
   dim3 grid(n_local * blocks_per_rank), block(256);
   const void* fn = dtype == 0 ? (const void*)ec_engine<float>
                   : dtype == 1 ? (const void*)ec_engine<double>
                                : (const void*)ec_engine<long long>;
+  cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_bytes);
+  if (e != cudaSuccess) return e;
   counted();
-  if (getenv("EC_NONCOOP")) return cudaLaunchKernel(fn, grid, block, args, 0, s);
-  return cudaLaunchCooperativeKernel(fn, grid, block, args, 0, s);
+  if (getenv("EC_NONCOOP")) return cudaLaunchKernel(fn, grid, block, args, smem_bytes, s);
+  return cudaLaunchCooperativeKernel(fn, grid, block, args, smem_bytes, s);
 }
 
 cudaError_t launch_fold(int dtype, void* stash, const void* grad, long long n, int mode,
@@ -872,9 +1113,10 @@ cudaError_t launch_reduce(int dtype, const void* const* srcs, int p, unsigned lo
 }
 
 cudaError_t launch_post(EcReq* rec, unsigned long long seq1, unsigned int type, unsigned int flags,
-                        long long t, long long arg, unsigned int* poison, cudaStream_t s) {
+                        long long t, long long arg, unsigned int* poison,
+                        unsigned long long* doorbell, cudaStream_t s) {
   counted();
-  ec_post_kernel<<<1, 32, 0, s>>>(rec, seq1, type, flags, t, arg, poison);
+  ec_post_kernel<<<1, 32, 0, s>>>(rec, seq1, type, flags, t, arg, poison, doorbell);
   return cudaGetLastError();
 }
 

@@ -1,0 +1,225 @@
+"""Benchmark drivers on real GPUs (harness.py of the reference, re-done for B200).
+
+* `allreduce_sweep` -- BASELINE config 5: partial-allreduce bus bandwidth over
+  payload sizes 1 KB .. 1 GB in all-arrive mode (nap = P, so nothing can be
+  skipped), with the device's own phase timestamps (snapshot -> reduction ->
+  publish) beside the host-observed round time.
+* `bench_flavor` -- the reference's latency / NAP microbenchmark
+  (harness.py:206-241): each rank idles its injected delay from a common round
+  origin, then calls the collective; records `BenchRecord(flavor, round, rank,
+  latency_us, nap, initiator)` in the reference's CSV schema.
+
+Run under torchrun (one rank per GPU):
+
+    torchrun --nproc-per-node 8 -m paper_1908_04207_b200.harness sweep --out sweep.json
+    torchrun --nproc-per-node 8 -m paper_1908_04207_b200.harness latency --p 8
+"""
+
+from __future__ import annotations
+
+import argparse
+import ctypes as C
+import json
+import math
+import os
+import sys
+import time
+from dataclasses import dataclass
+
+os.environ.setdefault("CUDA_MODULE_LOADING", "EAGER")
+
+BENCH_SCHEMA = "eagercoll-bench-v1"
+_BENCH_FIELDS = ("flavor", "round", "rank", "latency_us", "nap", "initiator")
+
+
+@dataclass
+class BenchRecord:
+    """harness.py:180-196 of the reference."""
+    flavor: str
+    round: int
+    rank: int
+    latency_us: int
+    nap: int
+    initiator: int = -1
+
+
+def _gen_times(h, g):
+    from ._lib import call
+    t4 = (C.c_uint64 * 4)()
+    call("ec_gen_times", h.comm.ptr, h.li, g, t4)
+    return list(t4)
+
+
+def _round(h, t, all_arrive=True):
+    from . import _lib
+    flags = _lib.EC_CF_FRESH | (_lib.EC_CF_ALL_ARRIVE if all_arrive else 0) | \
+        (_lib.EC_CF_ACTIVATE if h._may_activate(t) else 0)
+    seq = h._post_contribute(t, flags)
+    h._reply(seq)
+    h._wait(t, 60.0, pin=False)
+
+
+def allreduce_sweep(world, rank, p, sizes_bytes, flavor="solo", rounds_cap=50, workers=None,
+                    max_over_ranks=lambda x: x, barrier=lambda: None):
+    """Bus bandwidth of the partial allreduce per payload size (fp32)."""
+    import torch
+
+    from .collectives import AllreduceHandle, CollectiveConfig
+    out = []
+    cid = 1000
+    for nbytes in sizes_bytes:
+        n = max(1, nbytes // 4)
+        cid += 1
+        if workers is not None:
+            world.workers = workers
+        cfg = CollectiveConfig(p=p, flavor=flavor, vector_len=n, element="f4", seed=1234)
+        h = AllreduceHandle(cfg, rank, world, cid=cid)
+        h.send_buffer().normal_()
+        rounds = int(max(5, min(rounds_cap, (2 << 30) // max(1, 4 * n))))
+        for t in range(3):
+            _round(h, t)
+        barrier()
+        t0 = time.perf_counter()
+        for t in range(3, 3 + rounds):
+            _round(h, t)
+        dt = time.perf_counter() - t0
+        phases = [_gen_times(h, g) for g in range(3, 3 + rounds)]
+        data_us = sum((x[3] - x[1]) for x in phases) / rounds / 1e3
+        rs_us = sum((x[2] - x[1]) for x in phases) / rounds / 1e3
+        round_us = max_over_ranks(dt / rounds * 1e6)
+        data_us = max_over_ranks(data_us)
+        bus = 2 * (p - 1) / p * 4 * n if p > 1 else 0
+        out.append({"bytes": 4 * n, "rounds": rounds, "us_per_round": round_us,
+                    "busbw_gbs": bus / (round_us * 1e-6) / 1e9,
+                    "device_data_us": data_us, "device_rs_us": max_over_ranks(rs_us),
+                    "busbw_device_gbs": bus / (data_us * 1e-6) / 1e9 if data_us > 0 else None,
+                    "workers": h.comm.world.workers if workers is None else workers})
+        h.close()
+    return out
+
+
+def bench_flavor(world, rank, p, flavor, model, rounds=64, vector_len=64, link_slack_us=1000,
+                 seed=1234):
+    """harness.py:206-241 on hardware: rank r sleeps to t*period + delay[r, t],
+    then call_round; returns its BenchRecords."""
+    import numpy as np
+
+    from .collectives import AllreduceHandle, CollectiveConfig, drive, initiator_for_round
+    from .transport import delay_table
+    delays = delay_table(model, p, rounds)
+    period = int(delays.max()) + link_slack_us + 1000
+    cfg = CollectiveConfig(p=p, flavor=flavor, vector_len=vector_len, element="f8", seed=seed)
+    h = AllreduceHandle(cfg, rank, world, cid=2000 + hash(flavor) % 100)
+    vec = np.full(vector_len, float(rank + 1))
+    recs = []
+    world._barrier()
+    origin = time.perf_counter()
+    for t in range(rounds):
+        target = origin + (t * period + int(delays[rank, t])) * 1e-6
+        d = target - time.perf_counter()
+        if d > 0:
+            time.sleep(d)
+        t0 = time.perf_counter()
+        res = drive(h.call_round(t, vec))
+        lat = int((time.perf_counter() - t0) * 1e6)
+        init = initiator_for_round(seed, res.rnd, p) if flavor == "majority" else -1
+        recs.append(BenchRecord(flavor, t, rank, lat, res.nap, init))
+    h.close()
+    return recs
+
+
+def summarize(records):
+    """harness.py:347-370"""
+    import numpy as np
+    out = {"flavors": {}, "speedup_vs_sync": {}}
+    by = {}
+    for b in records:
+        by.setdefault(b.flavor, []).append(b)
+    for f, recs in sorted(by.items()):
+        lat = np.array([b.latency_us for b in recs], dtype=np.float64)
+        nap = np.array([b.nap for b in recs], dtype=np.float64)
+        out["flavors"][f] = {"n": len(recs), "mean_latency_us": float(lat.mean()),
+                             "std_latency_us": float(lat.std()), "mean_nap": float(nap.mean())}
+    if "sync" in by:
+        base = out["flavors"]["sync"]["mean_latency_us"]
+        for f in by:
+            own = out["flavors"][f]["mean_latency_us"]
+            out["speedup_vs_sync"][f] = base / own if own else float("inf")
+    return out
+
+
+def write_bench_csv(records, path: str) -> None:
+    """harness.py:373-378 (same schema line and columns)."""
+    with open(path, "w") as f:
+        f.write(f"# {BENCH_SCHEMA}\n")
+        f.write(",".join(_BENCH_FIELDS) + "\n")
+        for b in records:
+            f.write(",".join(str(getattr(b, k)) for k in _BENCH_FIELDS) + "\n")
+
+
+def _main(argv=None):
+    import torch
+    import torch.distributed as dist
+
+    from .transport import DelayModel
+    from .world import ProcessWorld
+    ap = argparse.ArgumentParser()
+    ap.add_argument("mode", choices=("sweep", "latency"))
+    ap.add_argument("--flavors", default="solo,majority")
+    ap.add_argument("--sizes", default="1K,4K,16K,64K,256K,1M,4M,16M,64M,100M,256M,1G")
+    ap.add_argument("--workers", default="")
+    ap.add_argument("--out", default="")
+    ap.add_argument("--rounds", type=int, default=64)
+    ap.add_argument("--delay", default="linear_skew:1.0")
+    args = ap.parse_args(argv)
+    rank = int(os.environ.get("RANK", 0))
+    p = int(os.environ.get("WORLD_SIZE", 1))
+    local = int(os.environ.get("LOCAL_RANK", 0))
+    torch.cuda.set_device(local)
+    if p > 1:
+        dist.init_process_group("gloo")
+    world = ProcessWorld(rank=rank, p=p, device=local)
+
+    def max_over(x):
+        if p == 1:
+            return x
+        t = torch.tensor([float(x)], dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    result = {"p": p}
+    if args.mode == "sweep":
+        mult = {"K": 1 << 10, "M": 1_000_000, "G": 1 << 30}
+        sizes = [int(s[:-1]) * mult[s[-1]] if s[-1] in mult else int(s) for s in args.sizes.split(",")]
+        sizes = [s if not (s == 100_000_000) else 100_000_000 for s in sizes]
+        workers = [int(w) for w in args.workers.split(",")] if args.workers else [None]
+        for f in args.flavors.split(","):
+            for w in workers:
+                result[f"{f}_w{w}"] = allreduce_sweep(world, rank, p, sizes, f, workers=w,
+                                                      max_over_ranks=max_over,
+                                                      barrier=world.barrier)
+    else:
+        kind, unit = args.delay.split(":")
+        model = DelayModel(kind, unit_ms=float(unit), k=1, seed=11)
+        recs = []
+        for f in ("sync", "solo", "majority"):
+            recs += bench_flavor(world, rank, p, f, model, rounds=args.rounds)
+        allr = [None] * p
+        dist.all_gather_object(allr, recs) if p > 1 else allr.__setitem__(0, recs)
+        flat = sorted((r for rr in allr for r in rr), key=lambda b: (b.flavor, b.round, b.rank))
+        result["summary"] = summarize(flat)
+        if rank == 0 and args.out:
+            write_bench_csv(flat, args.out + ".csv")
+    if rank == 0:
+        s = json.dumps(result)
+        print(s, flush=True)
+        if args.out and args.mode == "sweep":
+            with open(args.out, "w") as f:
+                f.write(s + "\n")
+    world.close()
+    if p > 1:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    sys.exit(_main())
