@@ -221,29 +221,30 @@ def main():
         step(t)
         t += 1
     quiesce()
-    timers: dict = {}
+    _lib.lib.ec_profile_enable(1)
     launches0 = _lib.lib.ec_launch_count()
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     naps = []
     with ClockSampler(local_rank) as clk:
         ev0.record()
         for _ in range(args.steps):
-            _, res, _g = step(t, timers)
+            _, res, _g = step(t)
             naps.append(res.nap)
             t += 1
         ev1.record()
         ev1.synchronize()
     launches = _lib.lib.ec_launch_count() - launches0
+    _lib.lib.ec_profile_enable(0)
+    import ctypes as C
+    prof_ms, prof_n = (C.c_double * 2)(), (C.c_int64 * 2)()
+    _lib.lib.ec_profile_read(prof_ms, prof_n)
     ms = ev0.elapsed_time(ev1)
     quiesce()
     ms_max = max_over_ranks(ms)
     value = world * args.steps / (ms_max / 1e3)
 
-    def kernel_ms(name):
-        evs = timers.get(name, [])
-        return sum(a.elapsed_time(b) for a, b in evs) / max(1, len(evs))
-
-    upd_ms, fold_ms = kernel_ms("update"), kernel_ms("fold")
+    fold_ms = prof_ms[0] / max(1, prof_n[0])      # CUDA events around each launch, timed region
+    upd_ms = prof_ms[1] / max(1, prof_n[1])
     peak, peak_kind = _peaks()
     upd_gbs = 12 * n / (upd_ms / 1e3) / 1e9
     fold_bytes = 8 * n            # every round is fresh: the fold writes 0 + g into a null stash
@@ -336,20 +337,15 @@ def bench_allreduce(args, pw, rank, world, dev, barrier, max_over_ranks, quiesce
         h.send_buffer().normal_()
         rounds = max(10, args.steps)
 
-        def rnd(t):
-            flags = _lib.EC_CF_FRESH | _lib.EC_CF_ALL_ARRIVE | \
-                (_lib.EC_CF_ACTIVATE if h._may_activate(t) else 0)
-            seq = h._post_contribute(t, flags)
-            h._reply(seq)
-            h._wait(t, 60.0, pin=False)
+        from paper_1908_04207_b200.harness import _round as rnd
 
         for t in range(3):
-            rnd(t)
+            rnd(h, t)
         quiesce()
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record()
         for t in range(3, 3 + rounds):
-            rnd(t)
+            rnd(h, t)
         e1.record()
         e1.synchronize()
         ms = max_over_ranks(e0.elapsed_time(e1)) / rounds

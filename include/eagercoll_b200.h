@@ -117,6 +117,23 @@ int ec_done_gen(ec_comm_t* c, int local_idx, int64_t* gen);
  * its result slot against reuse until ec_set_pin releases it. */
 int ec_wait(ec_comm_t* c, int local_idx, int64_t t, int timeout_ms, int pin,
             int64_t* gen, uint64_t* mask, int* nap);
+/* call_round in one call (collectives.py:334-345): ec_post_contribute(t, flags)
+ * + ec_reply + ec_wait(t, unpinned).  *status is the offer's reply. */
+int ec_round(ec_comm_t* c, int local_idx, int64_t t, uint32_t flags, void* stream,
+             int timeout_ms, int* status, int64_t* gen, uint64_t* mask, int* nap);
+/* One eager-SGD step of the hot path in one call (eagersgd.py:129-167):
+ * fold grad into the stash (fold_mode, skipped if grad is NULL), offer it
+ * (flags), wait for the latest generation >= t (pinned), w = w - lr*u (or the
+ * momentum form when mom != NULL and mu != 0), release the pin in stream order.
+ * *status = the offer's reply; on EC_R_POISONED nothing else happens. */
+int ec_step(ec_comm_t* c, int local_idx, int64_t t, const void* grad, int fold_mode,
+            uint32_t flags, void* w, void* mom, double lr, double mu, void* stream,
+            int timeout_ms, int* status, int64_t* gen, uint64_t* mask, int* nap);
+/* Instrumentation: with profiling on, ec_step brackets its fold and update
+ * launches with CUDA events; ec_profile_read sums the durations
+ * (ms_sum[0]/counts[0] = fold, [1] = update) and clears the record. */
+int ec_profile_enable(int on);
+int ec_profile_read(double* ms_sum2, int64_t* counts2);
 /* Mask / nap of an earlier generation from the device log (RoundRecord source). */
 int ec_gen_info(ec_comm_t* c, int local_idx, int64_t gen, uint64_t* mask,
                 uint64_t* has_data, int* nap);

@@ -649,6 +649,110 @@ int ec_wait(ec_comm_t* c, int li, int64_t t, int timeout_ms, int pin, int64_t* g
   return EC_OK;
 }
 
+// ---- kernel-duration instrumentation for ec_step (bench.py roofline) --------
+struct EcTimedLaunch {
+  int kind;  // 0 fold, 1 update
+  cudaEvent_t a, b;
+};
+static std::mutex g_prof_mu;
+static int g_prof_on = 0;
+static std::vector<EcTimedLaunch> g_prof;
+static std::vector<cudaEvent_t> g_ev_pool;
+
+static cudaEvent_t prof_event() {
+  if (!g_ev_pool.empty()) {
+    cudaEvent_t e = g_ev_pool.back();
+    g_ev_pool.pop_back();
+    return e;
+  }
+  cudaEvent_t e = nullptr;
+  cudaEventCreate(&e);
+  return e;
+}
+
+struct ProfScope {
+  int kind;
+  cudaStream_t s;
+  cudaEvent_t a = nullptr;
+  ProfScope(int k, void* stream) : kind(k), s((cudaStream_t)stream) {
+    if (!__atomic_load_n(&g_prof_on, __ATOMIC_RELAXED)) return;
+    std::lock_guard<std::mutex> g(g_prof_mu);
+    a = prof_event();
+    cudaEventRecord(a, s);
+  }
+  ~ProfScope() {
+    if (!a) return;
+    std::lock_guard<std::mutex> g(g_prof_mu);
+    cudaEvent_t b = prof_event();
+    cudaEventRecord(b, s);
+    g_prof.push_back({kind, a, b});
+  }
+};
+
+int ec_profile_enable(int on) {
+  __atomic_store_n(&g_prof_on, on ? 1 : 0, __ATOMIC_RELAXED);
+  return EC_OK;
+}
+
+int ec_profile_read(double* ms_sum, int64_t* counts) {
+  std::lock_guard<std::mutex> g(g_prof_mu);
+  ms_sum[0] = ms_sum[1] = 0.0;
+  counts[0] = counts[1] = 0;
+  for (auto& x : g_prof) {
+    float ms = 0.f;
+    cudaEventSynchronize(x.b);
+    if (cudaEventElapsedTime(&ms, x.a, x.b) == cudaSuccess) {
+      ms_sum[x.kind] += ms;
+      counts[x.kind] += 1;
+    }
+    g_ev_pool.push_back(x.a);
+    g_ev_pool.push_back(x.b);
+  }
+  g_prof.clear();
+  return EC_OK;
+}
+
+int ec_round(ec_comm_t* c, int li, int64_t t, uint32_t flags, void* stream, int timeout_ms,
+             int* status, int64_t* gen, uint64_t* mask, int* nap) {
+  uint64_t seq;
+  int rc = ec_post_contribute(c, li, t, flags, stream, &seq);
+  if (rc) return rc;
+  int st = 0;
+  if ((rc = ec_reply(c, li, seq, timeout_ms, &st))) return rc;
+  if (status) *status = st;
+  if (st == EC_R_POISONED || st == EC_R_ERROR) return EC_OK;
+  return ec_wait(c, li, t, timeout_ms, 0, gen, mask, nap);
+}
+
+int ec_step(ec_comm_t* c, int li, int64_t t, const void* grad, int fold_mode, uint32_t flags,
+            void* w, void* mom, double lr, double mu, void* stream, int timeout_ms,
+            int* status, int64_t* gen, uint64_t* mask, int* nap) {
+  int rc = check_li(c, li);
+  if (rc) return rc;
+  if (!w) return fail(EC_E_ARG, "null weights");
+  if (grad) {
+    ProfScope ps(0, stream);
+    if ((rc = ec_fold(c, li, grad, fold_mode, stream))) return rc;
+  }
+  uint64_t seq;
+  if ((rc = ec_post_contribute(c, li, t, flags, stream, &seq))) return rc;
+  int st = 0;
+  if ((rc = ec_reply(c, li, seq, timeout_ms, &st))) return rc;
+  if (status) *status = st;
+  if (st == EC_R_POISONED || st == EC_R_ERROR) return EC_OK;
+  int64_t G;
+  if ((rc = ec_wait(c, li, t, timeout_ms, 1, &G, mask, nap))) return rc;
+  if (gen) *gen = G;
+  const void* u = ec_slot_ptr(c, li, G);
+  {
+    ProfScope ps(1, stream);
+    if (mom && mu != 0.0) rc = ec_momentum_update(w, mom, u, lr, mu, c->n, c->dtype, stream);
+    else rc = ec_sgd_update(w, u, lr, c->n, c->dtype, stream);
+  }
+  if (rc) return rc;
+  return ec_set_pin(c, li, ~0ull, 1, stream);
+}
+
 int ec_set_pin(ec_comm_t* c, int li, uint64_t pin_lo, int ordered, void* stream) {
   int rc = check_li(c, li);
   if (rc) return rc;

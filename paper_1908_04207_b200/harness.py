@@ -51,12 +51,16 @@ def _gen_times(h, g):
 
 
 def _round(h, t, all_arrive=True):
+    """One all-arrive round through ec_round (post + reply + wait in one C call)."""
     from . import _lib
+    from ._lib import call
     flags = _lib.EC_CF_FRESH | (_lib.EC_CF_ALL_ARRIVE if all_arrive else 0) | \
         (_lib.EC_CF_ACTIVATE if h._may_activate(t) else 0)
-    seq = h._post_contribute(t, flags)
-    h._reply(seq)
-    h._wait(t, 60.0, pin=False)
+    h._ensure_started()
+    st, gen, mask, nap = C.c_int(), C.c_int64(), C.c_uint64(), C.c_int()
+    call("ec_round", h.comm.ptr, h.li, t, flags, h._stream(), 60000, C.byref(st), C.byref(gen),
+         C.byref(mask), C.byref(nap))
+    return gen.value
 
 
 def allreduce_sweep(world, rank, p, sizes_bytes, flavor="solo", rounds_cap=50, workers=None,
@@ -83,9 +87,13 @@ def allreduce_sweep(world, rank, p, sizes_bytes, flavor="solo", rounds_cap=50, w
         for t in range(3, 3 + rounds):
             _round(h, t)
         dt = time.perf_counter() - t0
-        phases = [_gen_times(h, g) for g in range(3, 3 + rounds)]
+        phases = [_gen_times(h, g) for g in range(2, 3 + rounds)]
+        prev, phases = phases[0], phases[1:]
         data_us = sum((x[3] - x[1]) for x in phases) / rounds / 1e3
         rs_us = sum((x[2] - x[1]) for x in phases) / rounds / 1e3
+        snap_wait_us = sum((x[1] - x[0]) for x in phases) / rounds / 1e3
+        gaps = [phases[0][0] - prev[3]] + [phases[i][0] - phases[i - 1][3] for i in range(1, rounds)]
+        turnaround_us = sum(gaps) / rounds / 1e3
         round_us = max_over_ranks(dt / rounds * 1e6)
         data_us = max_over_ranks(data_us)
         bus = 2 * (p - 1) / p * 4 * n if p > 1 else 0
@@ -93,6 +101,8 @@ def allreduce_sweep(world, rank, p, sizes_bytes, flavor="solo", rounds_cap=50, w
                     "busbw_gbs": bus / (round_us * 1e-6) / 1e9,
                     "device_data_us": data_us, "device_rs_us": max_over_ranks(rs_us),
                     "busbw_device_gbs": bus / (data_us * 1e-6) / 1e9 if data_us > 0 else None,
+                    "snap_to_start_us": max_over_ranks(snap_wait_us),
+                    "done_to_next_snap_us": max_over_ranks(turnaround_us),
                     "workers": h.comm.world.workers if workers is None else workers})
         h.close()
     return out
