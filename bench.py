@@ -163,6 +163,7 @@ def main():
     ap.add_argument("--cpu-budget", type=float, default=12.0)
     ap.add_argument("--imb-unit-ms", type=float, default=1.0)
     ap.add_argument("--imb-steps", type=int, default=32)
+    ap.add_argument("--lag", type=int, default=2, help="async steps in flight before reconciling")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
     rank, local_rank, world = _env_world()
@@ -178,7 +179,8 @@ def main():
     if world > 1:
         dist.init_process_group("gloo", rank=rank, world_size=world)
     from paper_1908_04207_b200 import (AllreduceHandle, CollectiveConfig, ProcessWorld,
-                                       TrainState, _lib, drive, train_step)
+                                       TrainState, _lib, attach_delivery_tracking, drive,
+                                       finish_step, train_step, train_step_async)
     from paper_1908_04207_b200.transport import DelayModel, device_delay, inject_delay
 
     pw = ProcessWorld(rank=rank, p=world, device=local_rank)
@@ -211,15 +213,30 @@ def main():
     st = TrainState.fresh(w0, LR, rank=rank, tau=None)
     all_arrive = world > 1
 
-    def step(t, timers=None, g=None):
-        return drive(train_step(st, None, h, grad=grads[t % 2] if g is None else g,
-                                all_arrive=all_arrive, timers=timers))
+    attach_delivery_tracking(h, st)
+
+    def run_steps(k, grad_fn, pre=None, ev_end=None, naps=None):
+        """Issue k async steps (ec_step_async: no host round trip), reconciling
+        each LAG steps behind; ev_end is recorded right after the last issue."""
+        from collections import deque
+        pend = deque()
+        for i in range(k):
+            if pre is not None:
+                pre(i)
+            pend.append(train_step_async(st, h, grad_fn(st.t), all_arrive=all_arrive))
+            if len(pend) > args.lag:
+                _, res, _g = finish_step(st, h, pend.popleft())
+                if naps is not None:
+                    naps.append(res.nap)
+        if ev_end is not None:
+            ev_end.record()
+        while pend:
+            _, res, _g = finish_step(st, h, pend.popleft())
+            if naps is not None:
+                naps.append(res.nap)
 
     # ---- main timed loop: inputs resident in HBM (working set >> 126 MB L2)
-    t = 0
-    for _ in range(args.warmup):
-        step(t)
-        t += 1
+    run_steps(args.warmup, lambda t: grads[t % 2])
     quiesce()
     _lib.lib.ec_profile_enable(1)
     launches0 = _lib.lib.ec_launch_count()
@@ -227,11 +244,7 @@ def main():
     naps = []
     with ClockSampler(local_rank) as clk:
         ev0.record()
-        for _ in range(args.steps):
-            _, res, _g = step(t)
-            naps.append(res.nap)
-            t += 1
-        ev1.record()
+        run_steps(args.steps, lambda t: grads[t % 2], ev_end=ev1, naps=naps)
         ev1.synchronize()
     launches = _lib.lib.ec_launch_count() - launches0
     _lib.lib.ec_profile_enable(0)
@@ -253,19 +266,15 @@ def main():
     # ---- e2e: gradient from pinned host memory every step, result read back
     host_grad = torch.randn(n, generator=torch.Generator().manual_seed(7 + rank)).pin_memory()
     dgrad = torch.empty(n, device=dev)
-    for _ in range(2):
-        dgrad.copy_(host_grad, non_blocking=True)
-        step(t, g=dgrad)
-        t += 1
+    h2d = lambda i: dgrad.copy_(host_grad, non_blocking=True)  # noqa: E731
+    run_steps(2, lambda t: dgrad, pre=h2d)
     quiesce()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e2e_steps = max(5, args.steps // 2)
     e0.record()
-    for _ in range(e2e_steps):
-        dgrad.copy_(host_grad, non_blocking=True)
-        _, res, _g = step(t, g=dgrad)           # res.included / res.nap: read back over PCIe
-        t += 1
-    e1.record()
+    # each step: H2D of the gradient from pinned memory, the step, and the
+    # step's result (generation, mask, nap) read back by finish_step
+    run_steps(e2e_steps, lambda t: dgrad, pre=h2d, ev_end=e1)
     e1.synchronize()
     quiesce()
     e2e_ms = max_over_ranks(e0.elapsed_time(e1))

@@ -129,6 +129,15 @@ int ec_round(ec_comm_t* c, int local_idx, int64_t t, uint32_t flags, void* strea
 int ec_step(ec_comm_t* c, int local_idx, int64_t t, const void* grad, int fold_mode,
             uint32_t flags, void* w, void* mom, double lr, double mu, void* stream,
             int timeout_ms, int* status, int64_t* gen, uint64_t* mask, int* nap);
+/* The same step with no host round trip (stream-ordered, returns at once):
+ * fold with the mode the device's stash state dictates (null stash: 0 + g),
+ * post the offer, wait ON THE DEVICE for a generation >= t and pin it, update
+ * from that slot, unpin.  The host reads the outcome later with
+ * ec_step_result(seq, t); steps must be issued in order. */
+int ec_step_async(ec_comm_t* c, int local_idx, int64_t t, const void* grad, uint32_t flags,
+                  void* w, void* mom, double lr, double mu, void* stream, uint64_t* seq);
+int ec_step_result(ec_comm_t* c, int local_idx, uint64_t seq, int64_t t, int timeout_ms,
+                   int* status, int64_t* gen, uint64_t* mask, int* nap);
 /* Instrumentation: with profiling on, ec_step brackets its fold and update
  * launches with CUDA events; ec_profile_read sums the durations
  * (ms_sum[0]/counts[0] = fold, [1] = update) and clears the record. */

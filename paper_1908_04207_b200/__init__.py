@@ -29,8 +29,8 @@ from .collectives import (  # noqa: E402,F401
     ceil_log2, drive, floor_pow2, initiator_for_round, run_allreduce, tree_order_sum,
 )
 from .eagersgd import (  # noqa: E402,F401
-    DivergenceError, GradientBuffer, TrainState, attach_delivery_tracking, resync_models,
-    resync_step, staleness_guard, train_step, training_process,
+    DivergenceError, GradientBuffer, TrainState, attach_delivery_tracking, finish_step,
+    resync_models, resync_step, staleness_guard, train_step, train_step_async, training_process,
 )
 from .trace import TraceRecorder  # noqa: E402,F401
 from .transport import DelayModel, Sleep, delayed_ranks, inject_delay  # noqa: E402,F401

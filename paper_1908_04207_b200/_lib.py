@@ -56,6 +56,9 @@ _SIGS = {
     "ec_gen_info": (_i32, [_vp, _i32, _i64, _P(_u64), _P(_u64), _P(_i32)]),
     "ec_set_pin": (_i32, [_vp, _i32, _u64, _i32, _vp]),
     "ec_gen_times": (_i32, [_vp, _i32, _i64, _P(_u64)]),
+    "ec_step_async": (_i32, [_vp, _i32, _i64, _vp, _u32, _vp, _vp, C.c_double, C.c_double, _vp,
+                             _P(_u64)]),
+    "ec_step_result": (_i32, [_vp, _i32, _u64, _i64, _i32, _P(_i32), _P(_i64), _P(_u64), _P(_i32)]),
     "ec_profile_enable": (_i32, [_i32]),
     "ec_profile_read": (_i32, [_P(C.c_double), _P(_i64)]),
     "ec_round": (_i32, [_vp, _i32, _i64, _u32, _vp, _i32, _P(_i32), _P(_i64), _P(_u64), _P(_i32)]),

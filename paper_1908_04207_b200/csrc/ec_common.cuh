@@ -43,6 +43,15 @@ struct alignas(128) EcCtrl {
   unsigned long long done_from[EC_MAX_P];    // gen+1: source's data for gen is in our slot
 };
 
+struct alignas(64) EcReq {
+  unsigned long long seq1;   // request sequence + 1; written last (release)
+  unsigned int type;
+  unsigned int flags;
+  long long t;
+  long long arg;
+  unsigned long long pad[4];
+};
+
 struct alignas(128) EcLocal {
   // round command: controller -> workers
   unsigned long long cmd_seq;      // incremented per round; ~0ull = exit
@@ -72,16 +81,15 @@ struct alignas(128) EcLocal {
   unsigned int poison;             // fold's non-finite flag (device word)
   int pad4;
   unsigned long long posted;       // doorbell: highest stream-posted request seq + 1
+  unsigned long long done_gen1_dev;  // device mirror of EcHostCtl::done_gen1 (async steps)
+  long long step_gen;              // generation the current async step's update reads
+  int stash_null;                  // 1: the stash holds no pending gradient (fold writes 0+g)
+  int pad5;
+  unsigned long long pad6[4];
+  EcReq dreq[EC_REQ_RING];         // stream-posted requests (device copy of the ring)
 };
 
-struct alignas(64) EcReq {
-  unsigned long long seq1;   // request sequence + 1; written last (release)
-  unsigned int type;
-  unsigned int flags;
-  long long t;
-  long long arg;
-  unsigned long long pad[4];
-};
+
 
 struct alignas(64) EcLog {
   unsigned long long gen1;
@@ -106,6 +114,8 @@ struct alignas(128) EcHostCtl {
   unsigned long long pad1[10];
   EcReq req[EC_REQ_RING];
   unsigned long long reply[EC_REQ_RING];   // ((seq+1) << 8) | status
+  unsigned long long stepgen[EC_REQ_RING]; // async step t: generation its update read, + 1
+  unsigned long long steptag[EC_REQ_RING]; // t + 1 once stepgen[t % RING] is valid
   EcLog log[EC_LOG_RING];
 };
 

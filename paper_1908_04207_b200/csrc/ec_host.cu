@@ -27,9 +27,15 @@ cudaError_t launch_momentum(int dtype, void* w, void* buf, const void* u, double
                             long long n, cudaStream_t s);
 cudaError_t launch_reduce(int dtype, const void* const* srcs, int p, unsigned long long has,
                           void* dst, long long n, int div, cudaStream_t s);
-cudaError_t launch_post(EcReq* rec, unsigned long long seq1, unsigned int type, unsigned int flags,
-                        long long t, long long arg, unsigned int* poison,
-                        unsigned long long* doorbell, cudaStream_t s);
+cudaError_t launch_post(EcLocal* L, unsigned long long seq1, unsigned int type, unsigned int flags,
+                        long long t, long long arg, cudaStream_t s);
+cudaError_t launch_fold_auto(int dtype, void* stash, const void* grad, long long n, EcLocal* L,
+                             cudaStream_t s);
+cudaError_t launch_wait_gen(EcLocal* L, EcHostCtl* H, long long t, int R, unsigned long long timeout_ns,
+                            cudaStream_t s);
+cudaError_t launch_update_gen(int dtype, void* w, void* mom, const char* ring, long long slot_bytes,
+                              int R, const EcLocal* L, double lr, double mu, long long n,
+                              cudaStream_t s);
 cudaError_t launch_write_u64(unsigned long long* p, unsigned long long v, cudaStream_t s);
 cudaError_t launch_direct(int dtype, const EcDesc* d_desc, long long nvec, unsigned long long seq,
                           unsigned int type, unsigned int flags, long long t, long long arg,
@@ -241,6 +247,7 @@ int ec_comm_create(int world_size, int rank_lo, int n_local, int device, int64_t
     memset(&init, 0, sizeof(init));
     init.hold_from = EC_INF_GEN;
     init.contributed_round = -1;
+    init.stash_null = 1;
     if ((e = cudaMemcpy(r->local, &init, sizeof(init), cudaMemcpyHostToDevice)) != cudaSuccess) {
       ec_comm_destroy(c);
       return fail(EC_E_CUDA, "init local: %s", cudaGetErrorString(e));
@@ -531,9 +538,7 @@ int ec_post_contribute(ec_comm_t* c, int li, int64_t t, uint32_t flags, void* st
     if (seq_out) *seq_out = seq;
     return EC_OK;
   }
-  EcReq* dq = &r->hd->req[seq % EC_REQ_RING];
-  CK(launch_post(dq, seq + 1, EC_REQ_CONTRIB, flags & 7u, t, 0, &r->local->poison,
-                 &r->local->posted, (cudaStream_t)stream));
+  CK(launch_post(r->local, seq + 1, EC_REQ_CONTRIB, flags & 7u, t, 0, (cudaStream_t)stream));
   if (seq_out) *seq_out = seq;
   return EC_OK;
 }
@@ -751,6 +756,57 @@ int ec_step(ec_comm_t* c, int li, int64_t t, const void* grad, int fold_mode, ui
   }
   if (rc) return rc;
   return ec_set_pin(c, li, ~0ull, 1, stream);
+}
+
+int ec_step_async(ec_comm_t* c, int li, int64_t t, const void* grad, uint32_t flags, void* w,
+                  void* mom, double lr, double mu, void* stream, uint64_t* seq_out) {
+  int rc = check_li(c, li);
+  if (rc) return rc;
+  if (!w || !grad) return fail(EC_E_ARG, "null weights or gradient");
+  if (c->dtype == EC_I64) return fail(EC_E_ARG, "eager-SGD step needs a float dtype");
+  EcRankHost* r = c->L[li];
+  cudaStream_t s = (cudaStream_t)stream;
+  {
+    ProfScope ps(0, stream);
+    CK(launch_fold_auto(c->dtype, r->send, grad, c->n, r->local, s));
+  }
+  uint64_t seq;
+  if ((rc = ec_post_contribute(c, li, t, flags, stream, &seq))) return rc;
+  CK(launch_wait_gen(r->local, r->hd, t, c->R, c->timeout_ns, s));
+  {
+    ProfScope ps(1, stream);
+    CK(launch_update_gen(c->dtype, w, (mom && mu != 0.0) ? mom : nullptr, r->ring, c->slot_bytes, c->R,
+                         r->local, lr, mu, c->n, s));
+  }
+  CK(launch_write_u64(&r->hd->pin_lo, ~0ull, s));
+  if (seq_out) *seq_out = seq;
+  return EC_OK;
+}
+
+int ec_step_result(ec_comm_t* c, int li, uint64_t seq, int64_t t, int timeout_ms, int* status,
+                   int64_t* gen, uint64_t* mask, int* nap) {
+  int rc = check_li(c, li);
+  if (rc) return rc;
+  EcRankHost* r = c->L[li];
+  if ((rc = ec_reply(c, li, seq, timeout_ms, status))) return rc;
+  if (status && (*status == EC_R_POISONED || *status == EC_R_ERROR)) return EC_OK;
+  Backoff bo;
+  while (aload(&r->h->steptag[t % EC_REQ_RING]) != (unsigned long long)t + 1) {
+    if ((rc = device_error(r))) return rc;
+    if (bo.expired(timeout_ms))
+      return fail(EC_E_TIMEOUT, "rank %d step %lld did not complete", r->rank, (long long)t);
+    bo.pause();
+  }
+  const int64_t G = (int64_t)aload(&r->h->stepgen[t % EC_REQ_RING]) - 1;
+  if (gen) *gen = G;
+  if (mask || nap) {
+    uint64_t m = 0;
+    int np = 0;
+    if ((rc = ec_gen_info(c, li, G, &m, nullptr, &np))) return rc;
+    if (mask) *mask = m;
+    if (nap) *nap = np;
+  }
+  return EC_OK;
 }
 
 int ec_set_pin(ec_comm_t* c, int li, uint64_t pin_lo, int ordered, void* stream) {

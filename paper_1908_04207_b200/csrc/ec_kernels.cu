@@ -507,14 +507,26 @@ __device__ void engine_controller(const EcDesc& d, unsigned long long epoch) {
       stopping = true;
       stop_t0 = globaltimer_ns();
     }
-    // ---- requests, strictly in sequence order
-    while (poll_host) {
-      EcReq* q = &H->req[next_req % EC_REQ_RING];
-      if (ld_acquire_sys(&q->seq1) != next_req + 1) break;
-      const unsigned type = ld_relaxed_sys_u32(&q->type);
-      const unsigned fl = ld_relaxed_sys_u32(&q->flags);
-      const long long t = (long long)ld_relaxed_sys((const unsigned long long*)&q->t);
-      const long long arg = (long long)ld_relaxed_sys((const unsigned long long*)&q->arg);
+    // ---- requests, strictly in sequence order: stream-posted ones sit in the
+    // device ring (cheap), host-posted ones only in the host-mapped ring
+    while (true) {
+      EcReq* dq = &L->dreq[next_req % EC_REQ_RING];
+      unsigned type, fl;
+      long long t, arg;
+      if (ld_acquire_gpu(&dq->seq1) == next_req + 1) {
+        type = *(volatile unsigned*)&dq->type;
+        fl = *(volatile unsigned*)&dq->flags;
+        t = *(volatile long long*)&dq->t;
+        arg = *(volatile long long*)&dq->arg;
+      } else {
+        if (!poll_host) break;
+        EcReq* q = &H->req[next_req % EC_REQ_RING];
+        if (ld_acquire_sys(&q->seq1) != next_req + 1) break;
+        type = ld_relaxed_sys_u32(&q->type);
+        fl = ld_relaxed_sys_u32(&q->flags);
+        t = (long long)ld_relaxed_sys((const unsigned long long*)&q->t);
+        arg = (long long)ld_relaxed_sys((const unsigned long long*)&q->arg);
+      }
       unsigned long long status = 3;  // OK
       if (type == EC_REQ_CONTRIB) {
         if (fl & EC_CF_POISON) {
@@ -588,7 +600,10 @@ __device__ void engine_controller(const EcDesc& d, unsigned long long epoch) {
         push_all(1, (((unsigned long long)g + 1) << 2) | (unsigned long long)contrib);
         t_snap = globaltimer_ns();
         st_release_sys(&H->snap_gen1, (unsigned long long)g + 1);
-        if (contrib & (int)EC_SNAP_FRESH) hold_from = EC_INF_GEN;  // stash delivered (eagersgd.py:117-124)
+        if (contrib & (int)EC_SNAP_FRESH) {
+          hold_from = EC_INF_GEN;  // stash delivered (eagersgd.py:117-124)
+          *(volatile int*)&L->stash_null = 1;
+        }
         snapped = 1;
         progress = true;
       }
@@ -636,6 +651,7 @@ __device__ void engine_controller(const EcDesc& d, unsigned long long epoch) {
         st_relaxed_sys(&lg->t_done, t_done);
         st_release_sys(&lg->gen1, (unsigned long long)g + 1);
         st_release_sys(&H->done_gen1, (unsigned long long)g + 1);
+        st_release_gpu(&L->done_gen1_dev, (unsigned long long)g + 1);
         ++g;
         snapped = 0;
         contrib = 0;
@@ -709,6 +725,7 @@ __global__ void ec_direct_decide(const EcDesc* __restrict__ dp, unsigned long lo
   if (type == EC_REQ_CONTRIB) {
     const unsigned int poison = *(volatile unsigned int*)&L->poison;
     *(volatile unsigned int*)&L->poison = 0u;
+    *(volatile int*)&L->stash_null = 0;  // the stash now holds an offer
     if (poison) {
       status = 4;
     } else if (t < g || (t == g && L->snapped)) {
@@ -765,13 +782,17 @@ ec_direct_round(const EcDesc* __restrict__ dp) {
       st_relaxed_sys(&lg->t_rs, tn);
       st_relaxed_sys(&lg->t_done, tn);
       st_release_sys(&lg->gen1, (unsigned long long)g + 1);
-      if (fresh) L->hold_from = EC_INF_GEN;
+      if (fresh) {
+        L->hold_from = EC_INF_GEN;
+        L->stash_null = 1;
+      }
       L->g = g + 1;
       L->snapped = 0;
       L->contrib = 0;
       __threadfence();
       st_release_sys(&H->snap_gen1, (unsigned long long)g + 1);
       st_release_sys(&H->done_gen1, (unsigned long long)g + 1);
+      st_release_gpu(&L->done_gen1_dev, (unsigned long long)g + 1);
     }
   }
 }
@@ -966,22 +987,23 @@ ec_reduce_kernel(EcSrcs s, int p, unsigned long long has, T* __restrict__ dst, l
   }
 }
 
-__global__ void ec_post_kernel(EcReq* rec, unsigned long long seq1, unsigned int type,
-                               unsigned int flags, long long t, long long arg,
-                               unsigned int* poison, unsigned long long* doorbell) {
+__global__ void ec_post_kernel(EcLocal* L, unsigned long long seq1, unsigned int type,
+                               unsigned int flags, long long t, long long arg) {
   if (threadIdx.x != 0) return;
-  if (poison) {
-    if (*(volatile unsigned int*)poison) flags |= EC_CF_POISON;
-    *(volatile unsigned int*)poison = 0u;
+  if (type == EC_REQ_CONTRIB) {
+    if (*(volatile unsigned int*)&L->poison) flags |= EC_CF_POISON;
+    *(volatile unsigned int*)&L->poison = 0u;
+    *(volatile int*)&L->stash_null = 0;  // the stash / send buffer now holds an offer
   }
+  EcReq* rec = &L->dreq[(seq1 - 1) % EC_REQ_RING];
   volatile EcReq* v = rec;
   v->type = type;
   v->flags = flags;
   v->t = t;
   v->arg = arg;
-  fence_acq_rel_sys();
-  st_release_sys(&rec->seq1, seq1);
-  if (doorbell) atomicMax(doorbell, seq1);
+  __threadfence();
+  st_release_gpu(&rec->seq1, seq1);
+  atomicMax(&L->posted, seq1);
 }
 
 __global__ void ec_write_u64_kernel(unsigned long long* p, unsigned long long v) {
@@ -995,6 +1017,118 @@ __global__ void ec_spin_kernel(unsigned long long ns) {
   if (threadIdx.x != 0) return;
   const unsigned long long t0 = globaltimer_ns();
   while (globaltimer_ns() - t0 < ns) __nanosleep(1000);
+}
+
+// ---------------------------------------------------------------------------
+// asynchronous eager-SGD step: every decision the host used to wait for is
+// taken on the device, in stream order, so a step is five launches and no
+// host round trip: fold (mode from the device's stash state) -> post ->
+// wait for a generation >= t (pin it) -> update from that slot -> unpin.
+
+template <typename T>
+__global__ void __launch_bounds__(256)
+ec_fold_auto_kernel(T* __restrict__ stash, const T* __restrict__ grad, long long n,
+                    EcLocal* __restrict__ L, int vec_ok) {
+  const int add = *(volatile int*)&L->stash_null ? 0 : 1;
+  constexpr int V = Ops<T>::V;
+  bool bad = false;
+  const long long tid = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  const long long nth = (long long)gridDim.x * blockDim.x;
+  long long done = 0;
+  if (vec_ok) {
+    const long long nv = n / V;
+    for (long long v = tid; v < nv; v += nth) {
+      Vec16<T> gv, sv, o;
+      gv.raw = ld_stream_v4(grad + v * V);
+      if (add) sv.raw = ld_stream_v4(stash + v * V);
+#pragma unroll
+      for (int l = 0; l < V; ++l) {
+        bad |= !Ops<T>::finite(gv.e[l]);
+        o.e[l] = add ? Ops<T>::add(sv.e[l], gv.e[l]) : Ops<T>::canon(gv.e[l]);
+      }
+      st_v4(stash + v * V, o.raw);
+    }
+    done = nv * V;
+  }
+  for (long long e = done + tid; e < n; e += nth) {
+    T gv = grad[e];
+    bad |= !Ops<T>::finite(gv);
+    stash[e] = add ? Ops<T>::add(stash[e], gv) : Ops<T>::canon(gv);
+  }
+  if (__any_sync(0xffffffffu, bad) && (threadIdx.x & 31) == 0) atomicOr(&L->poison, 1u);
+}
+
+__global__ void ec_wait_gen_kernel(EcLocal* L, EcHostCtl* H, long long t, int R,
+                                   unsigned long long timeout_ns) {
+  if (threadIdx.x != 0) return;
+  const unsigned long long t0 = globaltimer_ns();
+  unsigned long long d1;
+  while ((d1 = ld_acquire_gpu(&L->done_gen1_dev)) < (unsigned long long)t + 1) {
+    if (ld_relaxed_sys(&H->error) || globaltimer_ns() - t0 > timeout_ns) {
+      st_release_sys(&H->error_info, 0x200);
+      st_release_sys(&H->error, EC_DERR_TIMEOUT);
+      d1 = ld_acquire_gpu(&L->done_gen1_dev);
+      break;
+    }
+    __nanosleep(64);
+  }
+  long long G = (long long)d1 - 1;
+  // pin G (Dekker with the controller's check before snapshotting G + R)
+  while (true) {
+    st_relaxed_sys(&H->pin_lo, (unsigned long long)G);
+    fence_sc_sys();
+    const long long D = (long long)ld_acquire_gpu(&L->done_gen1_dev) - 1;
+    if (D < G + R - 1) break;
+    G = D;
+  }
+  L->step_gen = G;
+  st_relaxed_sys(&H->stepgen[t % EC_REQ_RING], (unsigned long long)G + 1);
+  st_release_sys(&H->steptag[t % EC_REQ_RING], (unsigned long long)t + 1);
+}
+
+template <typename T>
+__global__ void __launch_bounds__(256)
+ec_update_gen_kernel(T* __restrict__ w, T* __restrict__ mom, const char* __restrict__ ring,
+                     long long slot_bytes, int R, const EcLocal* __restrict__ L, T lr, T mu,
+                     long long n, int vec_ok) {
+  const long long G = *(volatile const long long*)&L->step_gen;
+  const T* __restrict__ u = reinterpret_cast<const T*>(ring + (G % R) * slot_bytes);
+  constexpr int V = Ops<T>::V;
+  const long long tid = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  const long long nth = (long long)gridDim.x * blockDim.x;
+  long long done = 0;
+  if (vec_ok) {
+    const long long nv = n / V;
+    for (long long v = tid; v < nv; v += nth) {
+      Vec16<T> wv, uv;
+      wv.raw = ld_stream_v4(w + v * V);
+      uv.raw = ld_cg_v4(u + v * V);
+      if (mom) {
+        Vec16<T> bv;
+        bv.raw = ld_stream_v4(mom + v * V);
+#pragma unroll
+        for (int l = 0; l < V; ++l) {
+          bv.e[l] = Ops<T>::mom(mu, bv.e[l], uv.e[l]);
+          wv.e[l] = Ops<T>::sgd(wv.e[l], lr, bv.e[l]);
+        }
+        st_v4(mom + v * V, bv.raw);
+      } else {
+#pragma unroll
+        for (int l = 0; l < V; ++l) wv.e[l] = Ops<T>::sgd(wv.e[l], lr, uv.e[l]);
+      }
+      st_v4(w + v * V, wv.raw);
+    }
+    done = nv * V;
+  }
+  for (long long e = done + tid; e < n; e += nth) {
+    T uu = u[e];
+    if (mom) {
+      T b = Ops<T>::mom(mu, mom[e], uu);
+      mom[e] = b;
+      uu = b;
+    }
+    w[e] = Ops<T>::sgd(w[e], lr, uu);
+  }
 }
 
 // ---------------------------------------------------------------------------
@@ -1029,6 +1163,9 @@ cudaError_t preload_kernels() {
       (const void*)ec_direct_decide, (const void*)ec_direct_round<float>,
       (const void*)ec_direct_round<double>, (const void*)ec_direct_round<long long>,
       (const void*)ec_post_kernel, (const void*)ec_write_u64_kernel, (const void*)ec_spin_kernel,
+      (const void*)ec_fold_auto_kernel<float>, (const void*)ec_fold_auto_kernel<double>,
+      (const void*)ec_fold_auto_kernel<long long>, (const void*)ec_wait_gen_kernel,
+      (const void*)ec_update_gen_kernel<float>, (const void*)ec_update_gen_kernel<double>,
   };
   for (const void* f : fns) {
     cudaFuncAttributes a;
@@ -1112,11 +1249,10 @@ cudaError_t launch_reduce(int dtype, const void* const* srcs, int p, unsigned lo
   return cudaGetLastError();
 }
 
-cudaError_t launch_post(EcReq* rec, unsigned long long seq1, unsigned int type, unsigned int flags,
-                        long long t, long long arg, unsigned int* poison,
-                        unsigned long long* doorbell, cudaStream_t s) {
+cudaError_t launch_post(EcLocal* L, unsigned long long seq1, unsigned int type, unsigned int flags,
+                        long long t, long long arg, cudaStream_t s) {
   counted();
-  ec_post_kernel<<<1, 32, 0, s>>>(rec, seq1, type, flags, t, arg, poison, doorbell);
+  ec_post_kernel<<<1, 32, 0, s>>>(L, seq1, type, flags, t, arg);
   return cudaGetLastError();
 }
 
@@ -1130,6 +1266,43 @@ cudaError_t launch_direct(int dtype, const EcDesc* d_desc, long long nvec, unsig
   if (dtype == 0) ec_direct_round<float><<<grid, 256, 0, s>>>(d_desc);
   else if (dtype == 1) ec_direct_round<double><<<grid, 256, 0, s>>>(d_desc);
   else ec_direct_round<long long><<<grid, 256, 0, s>>>(d_desc);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_fold_auto(int dtype, void* stash, const void* grad, long long n, EcLocal* L,
+                             cudaStream_t s) {
+  counted();
+  const int vec_ok = ((((uintptr_t)stash) | ((uintptr_t)grad)) & 15) == 0;
+  const int V = dtype == 0 ? 4 : 2;
+  const int grid = grid_for(n / V + 1, 256);
+  if (dtype == 0) ec_fold_auto_kernel<float><<<grid, 256, 0, s>>>((float*)stash, (const float*)grad, n, L, vec_ok);
+  else if (dtype == 1) ec_fold_auto_kernel<double><<<grid, 256, 0, s>>>((double*)stash, (const double*)grad, n, L, vec_ok);
+  else ec_fold_auto_kernel<long long><<<grid, 256, 0, s>>>((long long*)stash, (const long long*)grad, n, L, vec_ok);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_wait_gen(EcLocal* L, EcHostCtl* H, long long t, int R, unsigned long long timeout_ns,
+                            cudaStream_t s) {
+  counted();
+  ec_wait_gen_kernel<<<1, 32, 0, s>>>(L, H, t, R, timeout_ns);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_update_gen(int dtype, void* w, void* mom, const char* ring, long long slot_bytes,
+                              int R, const EcLocal* L, double lr, double mu, long long n,
+                              cudaStream_t s) {
+  counted();
+  const int vec_ok = ((((uintptr_t)w) | ((uintptr_t)mom) | ((uintptr_t)ring) | slot_bytes) & 15) == 0;
+  const int V = dtype == 0 ? 4 : 2;
+  const int grid = grid_for(n / V + 1, 256);
+  if (dtype == 0)
+    ec_update_gen_kernel<float><<<grid, 256, 0, s>>>((float*)w, (float*)mom, ring, slot_bytes, R, L,
+                                                     (float)lr, (float)mu, n, vec_ok);
+  else if (dtype == 1)
+    ec_update_gen_kernel<double><<<grid, 256, 0, s>>>((double*)w, (double*)mom, ring, slot_bytes, R, L,
+                                                      lr, mu, n, vec_ok);
+  else
+    return cudaErrorInvalidValue;
   return cudaGetLastError();
 }
 

@@ -331,3 +331,50 @@ def test_staleness_guard_holds_external_activation():
     g, r1 = hs[0].wait_blocking(1)
     assert r1.included == 0b11 and _np(r1.u).tolist() == [1.5] * 4
     world.close()
+
+
+@pytest.mark.parametrize("p", [1, 3, 4])
+def test_async_steps_match_oracle(p):
+    """train_step_async (device-side fold mode, wait and update) gives the same
+    bits as the oracle, with steps issued two ahead of reconciliation."""
+    from collections import deque
+
+    from paper_1908_04207_b200 import finish_step, train_step_async
+    n, lr, steps = 100_003, 0.05, 5
+    rng = np.random.default_rng(p)
+    grads = rng.standard_normal((steps, p, n), dtype=np.float32)
+    w0 = rng.standard_normal(n, dtype=np.float32)
+    world = EmulatedWorld(p)
+    cfg = CollectiveConfig(p=p, flavor="solo", vector_len=n, element="f4")
+    hs = [AllreduceHandle(cfg, r, world) for r in range(p)]
+    states = [TrainState.fresh(w0, lr, rank=r, tau=None) for r in range(p)]
+    gd = torch.as_tensor(grads, device="cuda")
+    out = {}
+
+    def body(r):
+        torch.cuda.set_device(0)
+        attach_delivery_tracking(hs[r], states[r])
+        pend, res = deque(), []
+        for t in range(steps):
+            pend.append(train_step_async(states[r], hs[r], gd[t, r], all_arrive=True))
+            if len(pend) > 2:
+                res.append(finish_step(states[r], hs[r], pend.popleft()))
+        while pend:
+            res.append(finish_step(states[r], hs[r], pend.popleft()))
+        torch.cuda.current_stream().synchronize()
+        out[r] = res
+
+    th = [threading.Thread(target=body, args=(r,)) for r in range(p)]
+    [x.start() for x in th]
+    [x.join() for x in th]
+    w = w0.copy()
+    for t in range(steps):
+        u, inc, _ = R.allreduce_round(list(grads[t]), [True] * p, np.float32)
+        w = R.sgd_update(w, u, lr)
+        for r in range(p):
+            _, res, gen = out[r][t]
+            assert gen == t and res.included == inc
+    for r in range(p):
+        assert states[r].w.cpu().numpy().tobytes() == w.tobytes()
+        assert states[r].send_buf.is_null
+    world.close()
