@@ -133,7 +133,8 @@ int ec_step(ec_comm_t* c, int local_idx, int64_t t, const void* grad, int fold_m
  * fold with the mode the device's stash state dictates (null stash: 0 + g),
  * post the offer, wait ON THE DEVICE for a generation >= t and pin it, update
  * from that slot, unpin.  The host reads the outcome later with
- * ec_step_result(seq, t); steps must be issued in order. */
+ * ec_step_result(seq, t); steps must be issued in order.  The device-side
+ * wait occupies `stream`: ranks sharing one GPU need distinct streams. */
 int ec_step_async(ec_comm_t* c, int local_idx, int64_t t, const void* grad, uint32_t flags,
                   void* w, void* mom, double lr, double mu, void* stream, uint64_t* seq);
 int ec_step_result(ec_comm_t* c, int local_idx, uint64_t seq, int64_t t, int timeout_ms,

@@ -336,7 +336,9 @@ def test_staleness_guard_holds_external_activation():
 @pytest.mark.parametrize("p", [1, 3, 4])
 def test_async_steps_match_oracle(p):
     """train_step_async (device-side fold mode, wait and update) gives the same
-    bits as the oracle, with steps issued two ahead of reconciliation."""
+    bits as the oracle, with steps issued two ahead of reconciliation.  Each
+    emulated rank needs its own stream: a device-side wait would otherwise sit
+    in front of the peers' offers on a shared stream."""
     from collections import deque
 
     from paper_1908_04207_b200 import finish_step, train_step_async
@@ -349,10 +351,13 @@ def test_async_steps_match_oracle(p):
     hs = [AllreduceHandle(cfg, r, world) for r in range(p)]
     states = [TrainState.fresh(w0, lr, rank=r, tau=None) for r in range(p)]
     gd = torch.as_tensor(grads, device="cuda")
+    streams = [torch.cuda.Stream() for _ in range(p)]
+    torch.cuda.synchronize()
     out = {}
 
     def body(r):
         torch.cuda.set_device(0)
+        torch.cuda.set_stream(streams[r])
         attach_delivery_tracking(hs[r], states[r])
         pend, res = deque(), []
         for t in range(steps):
