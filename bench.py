@@ -252,6 +252,7 @@ def main():
     prof_ms, prof_n = (C.c_double * 2)(), (C.c_int64 * 2)()
     _lib.lib.ec_profile_read(prof_ms, prof_n)
     ms = ev0.elapsed_time(ev1)
+    timeline = device_timeline(h, st.t, args.steps, max_over_ranks) if world > 1 else None
     quiesce()
     ms_max = max_over_ranks(ms)
     value = world * args.steps / (ms_max / 1e3)
@@ -320,6 +321,7 @@ def main():
                 "update": {"bytes_per_launch": 12 * n, "avg_launch_ms": upd_ms, "gbs": upd_gbs,
                            "frac": upd_gbs / peak},
             },
+            "timeline_us": timeline,
             "cpu_baseline": cpu,
             "clocks": clk.summary(),
             "gpu_launches": int(launches),
@@ -330,6 +332,23 @@ def main():
     if world > 1:
         dist.destroy_process_group()
     return 0
+
+
+def device_timeline(h, t_end, k, max_over_ranks):
+    """Mean per-round phases from the engine's %globaltimer stamps over the
+    last k generations (max over ranks): done(g-1) -> snapshot(g) (host
+    turnaround incl. fold + offer + all-arrive), snapshot -> all snapshots in,
+    data phase (reduce-scatter pull + all-gather push), plus the whole period."""
+    from paper_1908_04207_b200.harness import _gen_times
+    gens = list(range(max(1, t_end - k), t_end))
+    ts = [_gen_times(h, g) for g in [gens[0] - 1] + gens]
+    turn = [ts[i][0] - ts[i - 1][3] for i in range(1, len(ts))]
+    snap = [ts[i][1] - ts[i][0] for i in range(1, len(ts))]
+    data = [ts[i][3] - ts[i][1] for i in range(1, len(ts))]
+    period = (ts[-1][3] - ts[0][3]) / (len(ts) - 1)
+    m = lambda xs: max_over_ranks(sum(xs) / len(xs) / 1e3)  # noqa: E731
+    return {"done_to_snapshot": m(turn), "snapshot_to_start": m(snap), "data_phase": m(data),
+            "period": max_over_ranks(period / 1e3)}
 
 
 def bench_allreduce(args, pw, rank, world, dev, barrier, max_over_ranks, quiesce):

@@ -191,7 +191,7 @@ int ec_comm_create(int world_size, int rank_lo, int n_local, int device, int64_t
   if (workers_per_rank <= 0) {
     const bool ldg = getenv("EC_DATA") && strcmp(getenv("EC_DATA"), "ldg") == 0;
     if (n_local == 1) {
-      workers_per_rank = ldg ? 128 : 32;
+      workers_per_rank = ldg ? 128 : 64;
     } else {  // emulated world: all ranks' CTA groups share one GPU
       workers_per_rank = (144 / n_local) - 1;
       if (workers_per_rank > 16) workers_per_rank = 16;
@@ -205,13 +205,16 @@ int ec_comm_create(int world_size, int rank_lo, int n_local, int device, int64_t
   // within ~150 KB of shared memory.
   c->mode = (getenv("EC_DATA") && strcmp(getenv("EC_DATA"), "ldg") == 0) ? 1 : 0;
   {
-    int chb = world_size <= 12 ? 4096 : 1024;
+    int chb = world_size <= 12 ? 16384 : 1024;
     if (const char* e = getenv("EC_CHUNK")) chb = atoi(e);
     int st = (150 * 1024) / ((world_size + 1) * chb);
     if (st > 4) st = 4;
     if (const char* e = getenv("EC_STAGES")) st = atoi(e);
     if (st < 2) st = 2;
     if (st > 8) st = 8;
+    // stay inside the opt-in shared-memory limit (227 KB per CTA, minus static)
+    while (st > 2 && (long long)st * (world_size + 1) * chb > 200 * 1024) --st;
+    while (chb > 1024 && (long long)st * (world_size + 1) * chb > 200 * 1024) chb /= 2;
     c->chv = chb / 16;
     c->stages = st;
     c->smem_bytes = c->mode == 0 ? st * (world_size + 1) * chb : 0;

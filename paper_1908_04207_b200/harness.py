@@ -178,6 +178,8 @@ def _main(argv=None):
     ap.add_argument("--flavors", default="solo,majority")
     ap.add_argument("--sizes", default="1K,4K,16K,64K,256K,1M,4M,16M,64M,100M,256M,1G")
     ap.add_argument("--workers", default="")
+    ap.add_argument("--chunks", default="", help="TMA chunk bytes to sweep (EC_CHUNK)")
+    ap.add_argument("--stages", default="", help="TMA pipeline depths to sweep (EC_STAGES)")
     ap.add_argument("--out", default="")
     ap.add_argument("--rounds", type=int, default=64)
     ap.add_argument("--delay", default="linear_skew:1.0")
@@ -203,11 +205,29 @@ def _main(argv=None):
         sizes = [int(s[:-1]) * mult[s[-1]] if s[-1] in mult else int(s) for s in args.sizes.split(",")]
         sizes = [s if not (s == 100_000_000) else 100_000_000 for s in sizes]
         workers = [int(w) for w in args.workers.split(",")] if args.workers else [None]
+        chunks = args.chunks.split(",") if args.chunks else [None]
+        stages = args.stages.split(",") if args.stages else [None]
         for f in args.flavors.split(","):
             for w in workers:
-                result[f"{f}_w{w}"] = allreduce_sweep(world, rank, p, sizes, f, workers=w,
-                                                      max_over_ranks=max_over,
-                                                      barrier=world.barrier)
+                for ch in chunks:
+                    for stg in stages:
+                        for key, val in (("EC_CHUNK", ch), ("EC_STAGES", stg)):
+                            if val is None:
+                                os.environ.pop(key, None)
+                            else:
+                                os.environ[key] = val
+                        key = f"{f}_w{w}_c{ch}_s{stg}"
+                        try:
+                            result[key] = allreduce_sweep(
+                                world, rank, p, sizes, f, workers=w, max_over_ranks=max_over,
+                                barrier=world.barrier)
+                        except Exception as e:  # a geometry that cannot launch
+                            result[key] = {"error": str(e)[:200]}
+                            for cid in [c for c in world.comms if c >= 1000]:
+                                try:
+                                    world.release(cid)
+                                except Exception:
+                                    pass
     else:
         kind, unit = args.delay.split(":")
         model = DelayModel(kind, unit_ms=float(unit), k=1, seed=11)
