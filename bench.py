@@ -243,8 +243,10 @@ def main():
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     naps = []
     with ClockSampler(local_rank) as clk:
+        h0 = time.perf_counter()
         ev0.record()
         run_steps(args.steps, lambda t: grads[t % 2], ev_end=ev1, naps=naps)
+        host_ms = (time.perf_counter() - h0) * 1e3
         ev1.synchronize()
     launches = _lib.lib.ec_launch_count() - launches0
     _lib.lib.ec_profile_enable(0)
@@ -322,6 +324,7 @@ def main():
                            "frac": upd_gbs / peak},
             },
             "timeline_us": timeline,
+            "host_ms_per_step": host_ms / args.steps,
             "cpu_baseline": cpu,
             "clocks": clk.summary(),
             "gpu_launches": int(launches),
@@ -340,14 +343,16 @@ def device_timeline(h, t_end, k, max_over_ranks):
     turnaround incl. fold + offer + all-arrive), snapshot -> all snapshots in,
     data phase (reduce-scatter pull + all-gather push), plus the whole period."""
     from paper_1908_04207_b200.harness import _gen_times
-    gens = list(range(max(1, t_end - k), t_end))
+    gens = list(range(max(1, t_end - k + 1), t_end))   # skip the round after the quiesce
     ts = [_gen_times(h, g) for g in [gens[0] - 1] + gens]
-    turn = [ts[i][0] - ts[i - 1][3] for i in range(1, len(ts))]
+    local = [ts[i][4] - ts[i - 1][3] for i in range(1, len(ts))]     # update+fold+offer
+    arrive = [ts[i][0] - ts[i][4] for i in range(1, len(ts))]        # all-arrive + activation
     snap = [ts[i][1] - ts[i][0] for i in range(1, len(ts))]
     data = [ts[i][3] - ts[i][1] for i in range(1, len(ts))]
     period = (ts[-1][3] - ts[0][3]) / (len(ts) - 1)
     m = lambda xs: max_over_ranks(sum(xs) / len(xs) / 1e3)  # noqa: E731
-    return {"done_to_snapshot": m(turn), "snapshot_to_start": m(snap), "data_phase": m(data),
+    return {"done_to_offer": m(local), "offer_to_snapshot": m(arrive),
+            "snapshot_to_start": m(snap), "data_phase": m(data),
             "period": max_over_ranks(period / 1e3)}
 
 

@@ -148,9 +148,9 @@ int ec_profile_read(double* ms_sum2, int64_t* counts2);
 int ec_gen_info(ec_comm_t* c, int local_idx, int64_t gen, uint64_t* mask,
                 uint64_t* has_data, int* nap);
 /* Device timestamps (%globaltimer ns) of a completed generation at this rank:
- * t4 = {snapshot taken, reduction issued (all snapshots in), own shard reduced,
- * published}. */
-int ec_gen_times(ec_comm_t* c, int local_idx, int64_t gen, uint64_t* t4);
+ * t5 = {snapshot taken, reduction issued (all snapshots in), own data phase
+ * done, published, own offer processed (0 if none)}. */
+int ec_gen_times(ec_comm_t* c, int local_idx, int64_t gen, uint64_t* t5);
 /* Lowest generation the host may still read: the engine never overwrites the
  * slot of generation h unless h < pin_lo.  ordered != 0 performs the store in
  * `stream` order (release after the update kernel read the slot); ordered == 0

@@ -99,6 +99,8 @@ struct alignas(64) EcLog {
   // %globaltimer (ns) of this rank's engine: snapshot taken, round command
   // issued (all snapshots in), own shard reduced, round published
   unsigned long long t_snap, t_cmd, t_rs, t_done;
+  unsigned long long t_req;        // this rank's offer for the generation was processed
+  unsigned long long pad[3];
 };
 
 struct alignas(128) EcHostCtl {

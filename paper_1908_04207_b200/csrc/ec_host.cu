@@ -602,7 +602,7 @@ int ec_gen_info(ec_comm_t* c, int li, int64_t gen, uint64_t* mask, uint64_t* has
   return EC_OK;
 }
 
-int ec_gen_times(ec_comm_t* c, int li, int64_t gen, uint64_t* t4) {
+int ec_gen_times(ec_comm_t* c, int li, int64_t gen, uint64_t* t5) {
   int rc = check_li(c, li);
   if (rc) return rc;
   EcRankHost* r = c->L[li];
@@ -610,10 +610,11 @@ int ec_gen_times(ec_comm_t* c, int li, int64_t gen, uint64_t* t4) {
     return fail(EC_E_STATE, "generation %lld has not completed", (long long)gen);
   EcLog* lg = &r->h->log[gen % EC_LOG_RING];
   unsigned long long g1 = aload(&lg->gen1);
-  t4[0] = aload(&lg->t_snap);
-  t4[1] = aload(&lg->t_cmd);
-  t4[2] = aload(&lg->t_rs);
-  t4[3] = aload(&lg->t_done);
+  t5[0] = aload(&lg->t_snap);
+  t5[1] = aload(&lg->t_cmd);
+  t5[2] = aload(&lg->t_rs);
+  t5[3] = aload(&lg->t_done);
+  t5[4] = aload(&lg->t_req);
   __atomic_thread_fence(__ATOMIC_ACQUIRE);
   if (aload(&lg->gen1) != g1 || g1 != (unsigned long long)gen + 1)
     return fail(EC_E_STATE, "generation %lld fell out of the log", (long long)gen);

@@ -474,6 +474,7 @@ __device__ void engine_controller(const EcDesc& d, unsigned long long epoch) {
   bool stopping = false;
   unsigned long long stop_t0 = 0;
   unsigned long long t_snap = L->t_snap;
+  unsigned long long t_req = 0;
   unsigned ns = 32;
 
   // write this rank's word into every rank's control block (peer stores over NVLink)
@@ -543,6 +544,7 @@ __device__ void engine_controller(const EcDesc& d, unsigned long long epoch) {
           contrib = (int)(EC_SNAP_DATA | ((fl & 1u) ? EC_SNAP_FRESH : 0ull));
           contributed_round = t;
           status = 1;
+          t_req = globaltimer_ns();
           if (fl & 4u) {  // all-arrive
             push_all(2, (unsigned long long)g + 1);
             arrive_pending = 1;
@@ -649,6 +651,8 @@ __device__ void engine_controller(const EcDesc& d, unsigned long long epoch) {
         st_relaxed_sys(&lg->t_cmd, t0);
         st_relaxed_sys(&lg->t_rs, *(volatile unsigned long long*)&L->t_rs);
         st_relaxed_sys(&lg->t_done, t_done);
+        st_relaxed_sys(&lg->t_req, t_req);
+        t_req = 0;
         st_release_sys(&lg->gen1, (unsigned long long)g + 1);
         st_release_sys(&H->done_gen1, (unsigned long long)g + 1);
         st_release_gpu(&L->done_gen1_dev, (unsigned long long)g + 1);

@@ -45,9 +45,9 @@ class BenchRecord:
 
 def _gen_times(h, g):
     from ._lib import call
-    t4 = (C.c_uint64 * 4)()
-    call("ec_gen_times", h.comm.ptr, h.li, g, t4)
-    return list(t4)
+    t5 = (C.c_uint64 * 5)()
+    call("ec_gen_times", h.comm.ptr, h.li, g, t5)
+    return list(t5)
 
 
 def _round(h, t, all_arrive=True):
