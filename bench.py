@@ -312,7 +312,7 @@ def main():
                        "mean_nap": float(np.mean(naps))},
             "e2e": {"value": e2e_value, "unit": "steps/s", "h2d_bytes_per_step": 4 * n,
                     "d2h_bytes_per_step": 16},
-            "roofline": {"bound": "hbm", "kernel": "ec_update_kernel<float>",
+            "roofline": {"bound": "hbm", "kernel": "ec_update_gen_kernel<float>",
                          "achieved": upd_gbs, "peak": peak, "unit": "GB/s",
                          "frac": upd_gbs / peak, "traffic": _traffic("update"),
                          "bytes_per_launch": 12 * n, "avg_launch_ms": upd_ms,
