@@ -85,7 +85,10 @@ struct alignas(128) EcLocal {
   long long step_gen;              // generation the current async step's update reads
   int stash_null;                  // 1: the stash holds no pending gradient (fold writes 0+g)
   int pad5;
-  unsigned long long pad6[4];
+  unsigned long long fold_count;   // CTAs of the fused fold+post kernel done (last one posts)
+  unsigned long long upd_count;    // CTAs of the fused wait+update kernel done (last one unpins)
+  unsigned long long step_tag;     // t + 1 once step_gen holds step t's generation
+  unsigned long long pad6;
   EcReq dreq[EC_REQ_RING];         // stream-posted requests (device copy of the ring)
 };
 

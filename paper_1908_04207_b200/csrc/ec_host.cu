@@ -30,12 +30,12 @@ cudaError_t launch_reduce(int dtype, const void* const* srcs, int p, unsigned lo
 cudaError_t launch_post(EcLocal* L, unsigned long long seq1, unsigned int type, unsigned int flags,
                         long long t, long long arg, cudaStream_t s);
 cudaError_t launch_fold_auto(int dtype, void* stash, const void* grad, long long n, EcLocal* L,
-                             cudaStream_t s);
+                             unsigned long long seq1, unsigned flags, long long t, cudaStream_t s);
 cudaError_t launch_wait_gen(EcLocal* L, EcHostCtl* H, long long t, int R, unsigned long long timeout_ns,
                             cudaStream_t s);
 cudaError_t launch_update_gen(int dtype, void* w, void* mom, const char* ring, long long slot_bytes,
-                              int R, const EcLocal* L, double lr, double mu, long long n,
-                              cudaStream_t s);
+                              int R, EcLocal* L, double lr, double mu, long long n, EcHostCtl* H,
+                              long long t, unsigned long long timeout_ns, cudaStream_t s);
 cudaError_t launch_write_u64(unsigned long long* p, unsigned long long v, cudaStream_t s);
 cudaError_t launch_direct(int dtype, const EcDesc* d_desc, long long nvec, unsigned long long seq,
                           unsigned int type, unsigned int flags, long long t, long long arg,
@@ -770,19 +770,29 @@ int ec_step_async(ec_comm_t* c, int li, int64_t t, const void* grad, uint32_t fl
   if (c->dtype == EC_I64) return fail(EC_E_ARG, "eager-SGD step needs a float dtype");
   EcRankHost* r = c->L[li];
   cudaStream_t s = (cudaStream_t)stream;
+  if (!c->running && (rc = ec_comm_start(c))) return rc;
+  unsigned long long seq;
   {
-    ProfScope ps(0, stream);
-    CK(launch_fold_auto(c->dtype, r->send, grad, c->n, r->local, s));
+    std::lock_guard<std::mutex> g(r->mu);
+    if ((rc = reserve_seq(c, r, &seq))) return rc;
   }
-  uint64_t seq;
-  if ((rc = ec_post_contribute(c, li, t, flags, stream, &seq))) return rc;
-  CK(launch_wait_gen(r->local, r->hd, t, c->R, c->timeout_ns, s));
   {
+    // fold (+ the offer's post, fused into the fold's last CTA, engine mode)
+    ProfScope ps(0, stream);
+    CK(launch_fold_auto(c->dtype, r->send, grad, c->n, r->local, c->direct ? 0 : seq + 1,
+                        flags & 7u, t, s));
+  }
+  if (c->direct) {
+    c->last_stream = stream;
+    CK(launch_direct(c->dtype, c->d_descs + li, c->n / (16 / c->elem), seq, EC_REQ_CONTRIB,
+                     flags & 7u, t, 0, s));
+  }
+  {
+    // device wait for a generation >= t + pin, update, unpin: one launch
     ProfScope ps(1, stream);
     CK(launch_update_gen(c->dtype, w, (mom && mu != 0.0) ? mom : nullptr, r->ring, c->slot_bytes, c->R,
-                         r->local, lr, mu, c->n, s));
+                         r->local, lr, mu, c->n, r->hd, t, c->timeout_ns, s));
   }
-  CK(launch_write_u64(&r->hd->pin_lo, ~0ull, s));
   if (seq_out) *seq_out = seq;
   return EC_OK;
 }

@@ -991,25 +991,6 @@ ec_reduce_kernel(EcSrcs s, int p, unsigned long long has, T* __restrict__ dst, l
   }
 }
 
-__global__ void ec_post_kernel(EcLocal* L, unsigned long long seq1, unsigned int type,
-                               unsigned int flags, long long t, long long arg) {
-  if (threadIdx.x != 0) return;
-  if (type == EC_REQ_CONTRIB) {
-    if (*(volatile unsigned int*)&L->poison) flags |= EC_CF_POISON;
-    *(volatile unsigned int*)&L->poison = 0u;
-    *(volatile int*)&L->stash_null = 0;  // the stash / send buffer now holds an offer
-  }
-  EcReq* rec = &L->dreq[(seq1 - 1) % EC_REQ_RING];
-  volatile EcReq* v = rec;
-  v->type = type;
-  v->flags = flags;
-  v->t = t;
-  v->arg = arg;
-  __threadfence();
-  st_release_gpu(&rec->seq1, seq1);
-  atomicMax(&L->posted, seq1);
-}
-
 __global__ void ec_write_u64_kernel(unsigned long long* p, unsigned long long v) {
   if (threadIdx.x == 0) {
     fence_acq_rel_sys();
@@ -1029,10 +1010,32 @@ __global__ void ec_spin_kernel(unsigned long long ns) {
 // host round trip: fold (mode from the device's stash state) -> post ->
 // wait for a generation >= t (pin it) -> update from that slot -> unpin.
 
+// post a request into the device ring (one thread)
+__device__ __forceinline__ void post_request(EcLocal* L, unsigned long long seq1, unsigned type,
+                                             unsigned flags, long long t, long long arg) {
+  if (type == EC_REQ_CONTRIB) {
+    if (*(volatile unsigned int*)&L->poison) flags |= EC_CF_POISON;
+    *(volatile unsigned int*)&L->poison = 0u;
+    *(volatile int*)&L->stash_null = 0;  // the stash / send buffer now holds an offer
+  }
+  EcReq* rec = &L->dreq[(seq1 - 1) % EC_REQ_RING];
+  volatile EcReq* v = rec;
+  v->type = type;
+  v->flags = flags;
+  v->t = t;
+  v->arg = arg;
+  __threadfence();
+  st_release_gpu(&rec->seq1, seq1);
+  atomicMax(&L->posted, seq1);
+}
+
+// fold with the device-decided mode; with seq1 != 0 the last CTA also posts the
+// offer (fused fold + post: one launch, the offer leaves as the stash is ready)
 template <typename T>
 __global__ void __launch_bounds__(256)
 ec_fold_auto_kernel(T* __restrict__ stash, const T* __restrict__ grad, long long n,
-                    EcLocal* __restrict__ L, int vec_ok) {
+                    EcLocal* __restrict__ L, int vec_ok, unsigned long long seq1, unsigned flags,
+                    long long t) {
   const int add = *(volatile int*)&L->stash_null ? 0 : 1;
   constexpr int V = Ops<T>::V;
   bool bad = false;
@@ -1040,17 +1043,31 @@ ec_fold_auto_kernel(T* __restrict__ stash, const T* __restrict__ grad, long long
   const long long nth = (long long)gridDim.x * blockDim.x;
   long long done = 0;
   if (vec_ok) {
+    constexpr int U = 2;
     const long long nv = n / V;
-    for (long long v = tid; v < nv; v += nth) {
-      Vec16<T> gv, sv, o;
-      gv.raw = ld_stream_v4(grad + v * V);
-      if (add) sv.raw = ld_stream_v4(stash + v * V);
+    for (long long base = tid; base < nv; base += nth * U) {
+      Vec16<T> gv[U], sv[U];
 #pragma unroll
-      for (int l = 0; l < V; ++l) {
-        bad |= !Ops<T>::finite(gv.e[l]);
-        o.e[l] = add ? Ops<T>::add(sv.e[l], gv.e[l]) : Ops<T>::canon(gv.e[l]);
+      for (int u = 0; u < U; ++u) {
+        const long long v = base + u * nth;
+        if (v < nv) {
+          gv[u].raw = ld_stream_v4(grad + v * V);
+          if (add) sv[u].raw = ld_stream_v4(stash + v * V);
+        }
       }
-      st_v4(stash + v * V, o.raw);
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const long long v = base + u * nth;
+        if (v < nv) {
+          Vec16<T> o;
+#pragma unroll
+          for (int l = 0; l < V; ++l) {
+            bad |= !Ops<T>::finite(gv[u].e[l]);
+            o.e[l] = add ? Ops<T>::add(sv[u].e[l], gv[u].e[l]) : Ops<T>::canon(gv[u].e[l]);
+          }
+          st_v4(stash + v * V, o.raw);
+        }
+      }
     }
     done = nv * V;
   }
@@ -1060,11 +1077,21 @@ ec_fold_auto_kernel(T* __restrict__ stash, const T* __restrict__ grad, long long
     stash[e] = add ? Ops<T>::add(stash[e], gv) : Ops<T>::canon(gv);
   }
   if (__any_sync(0xffffffffu, bad) && (threadIdx.x & 31) == 0) atomicOr(&L->poison, 1u);
+  if (seq1 == 0) return;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence();
+    if (atomicAdd(&L->fold_count, 1ull) == gridDim.x - 1) {
+      __threadfence();
+      L->fold_count = 0;
+      post_request(L, seq1, EC_REQ_CONTRIB, flags, t, 0);
+    }
+  }
 }
 
-__global__ void ec_wait_gen_kernel(EcLocal* L, EcHostCtl* H, long long t, int R,
-                                   unsigned long long timeout_ns) {
-  if (threadIdx.x != 0) return;
+// wait for a generation >= t, pin it, publish it for the update (one thread)
+__device__ void wait_and_pin(EcLocal* L, EcHostCtl* H, long long t, int R,
+                             unsigned long long timeout_ns) {
   const unsigned long long t0 = globaltimer_ns();
   unsigned long long d1;
   while ((d1 = ld_acquire_gpu(&L->done_gen1_dev)) < (unsigned long long)t + 1) {
@@ -1088,39 +1115,70 @@ __global__ void ec_wait_gen_kernel(EcLocal* L, EcHostCtl* H, long long t, int R,
   L->step_gen = G;
   st_relaxed_sys(&H->stepgen[t % EC_REQ_RING], (unsigned long long)G + 1);
   st_release_sys(&H->steptag[t % EC_REQ_RING], (unsigned long long)t + 1);
+  st_release_gpu(&L->step_tag, (unsigned long long)t + 1);
 }
 
+__global__ void ec_wait_gen_kernel(EcLocal* L, EcHostCtl* H, long long t, int R,
+                                   unsigned long long timeout_ns) {
+  if (threadIdx.x == 0) wait_and_pin(L, H, t, R, timeout_ns);
+}
+
+// update from the slot of the step's generation; with H != nullptr the kernel
+// also performs the wait (block 0) and the last CTA releases the pin
+// (fused wait + update + unpin: one launch)
 template <typename T>
 __global__ void __launch_bounds__(256)
 ec_update_gen_kernel(T* __restrict__ w, T* __restrict__ mom, const char* __restrict__ ring,
-                     long long slot_bytes, int R, const EcLocal* __restrict__ L, T lr, T mu,
-                     long long n, int vec_ok) {
-  const long long G = *(volatile const long long*)&L->step_gen;
+                     long long slot_bytes, int R, EcLocal* __restrict__ L, T lr, T mu,
+                     long long n, int vec_ok, EcHostCtl* H, long long t,
+                     unsigned long long timeout_ns) {
+  __shared__ long long s_gen;
+  if (threadIdx.x == 0) {
+    if (H != nullptr) {
+      if (blockIdx.x == 0) wait_and_pin(L, H, t, R, timeout_ns);
+      while (ld_acquire_gpu(&L->step_tag) != (unsigned long long)t + 1) __nanosleep(256);
+    }
+    s_gen = *(volatile const long long*)&L->step_gen;
+  }
+  __syncthreads();
+  const long long G = s_gen;
   const T* __restrict__ u = reinterpret_cast<const T*>(ring + (G % R) * slot_bytes);
   constexpr int V = Ops<T>::V;
   const long long tid = (long long)blockIdx.x * blockDim.x + threadIdx.x;
   const long long nth = (long long)gridDim.x * blockDim.x;
   long long done = 0;
   if (vec_ok) {
+    constexpr int U = 2;
     const long long nv = n / V;
-    for (long long v = tid; v < nv; v += nth) {
-      Vec16<T> wv, uv;
-      wv.raw = ld_stream_v4(w + v * V);
-      uv.raw = ld_cg_v4(u + v * V);
-      if (mom) {
-        Vec16<T> bv;
-        bv.raw = ld_stream_v4(mom + v * V);
+    for (long long base = tid; base < nv; base += nth * U) {
+      Vec16<T> wv[U], uv[U], bv[U];
 #pragma unroll
-        for (int l = 0; l < V; ++l) {
-          bv.e[l] = Ops<T>::mom(mu, bv.e[l], uv.e[l]);
-          wv.e[l] = Ops<T>::sgd(wv.e[l], lr, bv.e[l]);
+      for (int k = 0; k < U; ++k) {
+        const long long v = base + k * nth;
+        if (v < nv) {
+          wv[k].raw = ld_stream_v4(w + v * V);
+          uv[k].raw = ld_cg_v4(u + v * V);
+          if (mom) bv[k].raw = ld_stream_v4(mom + v * V);
         }
-        st_v4(mom + v * V, bv.raw);
-      } else {
-#pragma unroll
-        for (int l = 0; l < V; ++l) wv.e[l] = Ops<T>::sgd(wv.e[l], lr, uv.e[l]);
       }
-      st_v4(w + v * V, wv.raw);
+#pragma unroll
+      for (int k = 0; k < U; ++k) {
+        const long long v = base + k * nth;
+        if (v < nv) {
+          if (mom) {
+#pragma unroll
+            for (int l = 0; l < V; ++l) {
+              bv[k].e[l] = Ops<T>::mom(mu, bv[k].e[l], uv[k].e[l]);
+              wv[k].e[l] = Ops<T>::sgd(wv[k].e[l], lr, bv[k].e[l]);
+            }
+            st_v4(mom + v * V, bv[k].raw);
+          } else {
+#pragma unroll
+            for (int l = 0; l < V; ++l) wv[k].e[l] = Ops<T>::sgd(wv[k].e[l], lr, uv[k].e[l]);
+          }
+          st_v4(w + v * V, wv[k].raw);
+        }
+      }
     }
     done = nv * V;
   }
@@ -1133,6 +1191,21 @@ ec_update_gen_kernel(T* __restrict__ w, T* __restrict__ mom, const char* __restr
     }
     w[e] = Ops<T>::sgd(w[e], lr, uu);
   }
+  if (H == nullptr) return;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence();
+    if (atomicAdd(&L->upd_count, 1ull) == gridDim.x - 1) {
+      L->upd_count = 0;
+      fence_acq_rel_sys();
+      st_release_sys(&H->pin_lo, ~0ull);  // every CTA has read the slot: unpin
+    }
+  }
+}
+
+__global__ void ec_post_kernel(EcLocal* L, unsigned long long seq1, unsigned int type,
+                               unsigned int flags, long long t, long long arg) {
+  if (threadIdx.x == 0) post_request(L, seq1, type, flags, t, arg);
 }
 
 // ---------------------------------------------------------------------------
@@ -1274,14 +1347,17 @@ cudaError_t launch_direct(int dtype, const EcDesc* d_desc, long long nvec, unsig
 }
 
 cudaError_t launch_fold_auto(int dtype, void* stash, const void* grad, long long n, EcLocal* L,
-                             cudaStream_t s) {
+                             unsigned long long seq1, unsigned flags, long long t, cudaStream_t s) {
   counted();
   const int vec_ok = ((((uintptr_t)stash) | ((uintptr_t)grad)) & 15) == 0;
   const int V = dtype == 0 ? 4 : 2;
-  const int grid = grid_for(n / V + 1, 256);
-  if (dtype == 0) ec_fold_auto_kernel<float><<<grid, 256, 0, s>>>((float*)stash, (const float*)grad, n, L, vec_ok);
-  else if (dtype == 1) ec_fold_auto_kernel<double><<<grid, 256, 0, s>>>((double*)stash, (const double*)grad, n, L, vec_ok);
-  else ec_fold_auto_kernel<long long><<<grid, 256, 0, s>>>((long long*)stash, (const long long*)grad, n, L, vec_ok);
+  const int grid = grid_for((n / V + 1) / 2 + 1, 256);
+  if (dtype == 0)
+    ec_fold_auto_kernel<float><<<grid, 256, 0, s>>>((float*)stash, (const float*)grad, n, L, vec_ok, seq1, flags, t);
+  else if (dtype == 1)
+    ec_fold_auto_kernel<double><<<grid, 256, 0, s>>>((double*)stash, (const double*)grad, n, L, vec_ok, seq1, flags, t);
+  else
+    ec_fold_auto_kernel<long long><<<grid, 256, 0, s>>>((long long*)stash, (const long long*)grad, n, L, vec_ok, seq1, flags, t);
   return cudaGetLastError();
 }
 
@@ -1293,18 +1369,18 @@ cudaError_t launch_wait_gen(EcLocal* L, EcHostCtl* H, long long t, int R, unsign
 }
 
 cudaError_t launch_update_gen(int dtype, void* w, void* mom, const char* ring, long long slot_bytes,
-                              int R, const EcLocal* L, double lr, double mu, long long n,
-                              cudaStream_t s) {
+                              int R, EcLocal* L, double lr, double mu, long long n, EcHostCtl* H,
+                              long long t, unsigned long long timeout_ns, cudaStream_t s) {
   counted();
   const int vec_ok = ((((uintptr_t)w) | ((uintptr_t)mom) | ((uintptr_t)ring) | slot_bytes) & 15) == 0;
   const int V = dtype == 0 ? 4 : 2;
-  const int grid = grid_for(n / V + 1, 256);
+  const int grid = grid_for((n / V + 1) / 2 + 1, 256);
   if (dtype == 0)
     ec_update_gen_kernel<float><<<grid, 256, 0, s>>>((float*)w, (float*)mom, ring, slot_bytes, R, L,
-                                                     (float)lr, (float)mu, n, vec_ok);
+                                                     (float)lr, (float)mu, n, vec_ok, H, t, timeout_ns);
   else if (dtype == 1)
     ec_update_gen_kernel<double><<<grid, 256, 0, s>>>((double*)w, (double*)mom, ring, slot_bytes, R, L,
-                                                      lr, mu, n, vec_ok);
+                                                      lr, mu, n, vec_ok, H, t, timeout_ns);
   else
     return cudaErrorInvalidValue;
   return cudaGetLastError();

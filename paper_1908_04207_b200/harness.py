@@ -138,6 +138,45 @@ def bench_flavor(world, rank, p, flavor, model, rounds=64, vector_len=64, link_s
     return recs
 
 
+def run_training_rank(world, rank, p, flavor, *, epochs=48, steps_per_epoch=4, dim=64,
+                      n_samples=4096, batch_per_rank=128, lr=0.05, tau=8, resync_period=8,
+                      delay=None, seed=1234, data_seed=99, device_delay=False, cid_base=3000,
+                      time_scale=1.0):
+    """One rank of the reference's run_training (harness.py:275-340) on a device
+    world: hyperplane regression (BASELINE config 1), real injected delays,
+    the flavor's partial allreduce + a sync resync handle.  Returns this rank's
+    metrics rows, per-epoch validation MSE, wall time and ledger entries."""
+    import torch
+
+    from .collectives import AllreduceHandle, CollectiveConfig, drive
+    from .eagersgd import TrainState, training_process
+    from .models import gen_dataset, init_weights
+    from .trace import DeliveryLedger
+    from .transport import inject_delay
+    ds = gen_dataset(dim, n_samples, seed=data_seed, device=torch.device("cuda", world.device))
+    w0 = init_weights(dim, seed=seed)
+    h = AllreduceHandle(CollectiveConfig(p=p, flavor=flavor, vector_len=dim, element="f4",
+                                         seed=seed), rank, world, cid=cid_base)
+    hr = AllreduceHandle(CollectiveConfig(p=p, flavor="sync", vector_len=dim, element="f4"),
+                         rank, world, cid=cid_base + 1)
+    st = TrainState.fresh(w0, lr, rank=rank, resync_period=resync_period, tau=tau)
+    ledger = DeliveryLedger()
+    metrics, val = [], {}
+    delay_fn = None
+    if delay is not None and delay.kind != "none":
+        delay_fn = lambda r, t: int(inject_delay(r, t, delay, p) * time_scale)  # noqa: E731
+    t0 = time.perf_counter()
+    drive(training_process(rank, st, h, hr, ds, epochs=epochs, steps_per_epoch=steps_per_epoch,
+                           batch_per_rank=batch_per_rank, data_seed=data_seed,
+                           delay_fn=delay_fn, metrics=metrics, transport=None,
+                           guard=tau is not None, ledger=ledger, val_out=val,
+                           device_delay=device_delay))
+    torch.cuda.current_stream().synchronize()
+    wall = time.perf_counter() - t0
+    return {"rows": metrics, "val": val, "wall_s": wall, "ledger": ledger.entries(),
+            "w": st.w.detach().cpu().numpy(), "handles": (h, hr)}
+
+
 def summarize(records):
     """harness.py:347-370"""
     import numpy as np
@@ -174,7 +213,7 @@ def _main(argv=None):
     from .transport import DelayModel
     from .world import ProcessWorld
     ap = argparse.ArgumentParser()
-    ap.add_argument("mode", choices=("sweep", "latency"))
+    ap.add_argument("mode", choices=("sweep", "latency", "train"))
     ap.add_argument("--flavors", default="solo,majority")
     ap.add_argument("--sizes", default="1K,4K,16K,64K,256K,1M,4M,16M,64M,100M,256M,1G")
     ap.add_argument("--workers", default="")
@@ -228,6 +267,34 @@ def _main(argv=None):
                                     world.release(cid)
                                 except Exception:
                                     pass
+    elif args.mode == "train":
+        # BASELINE config 1 on GPUs: hyperplane, random_subset 0.2 ms k=1 seed 11
+        import numpy as np
+        model = DelayModel("random_subset", unit_ms=0.2, k=1, seed=11)
+        if args.delay != "linear_skew:1.0":
+            kind, unit = args.delay.split(":")
+            model = DelayModel(kind, unit_ms=float(unit), k=1, seed=11)
+        out = {}
+        for i, f in enumerate(("sync", "solo", "majority")):
+            world._barrier()
+            r = run_training_rank(world, rank, p, f, delay=model, cid_base=3000 + 10 * i)
+            for hh in r["handles"]:
+                hh.close()
+            allr = [None] * p
+            if p > 1:
+                dist.all_gather_object(allr, {k: r[k] for k in ("rows", "val", "wall_s")})
+            else:
+                allr[0] = {k: r[k] for k in ("rows", "val", "wall_s")}
+            wall = max(x["wall_s"] for x in allr)
+            steps = sum(len(x["rows"]) for x in allr)
+            last = max(e for x in allr for (_, e) in x["val"])
+            vals = [v for x in allr for (rr, e), v in x["val"].items() if e == last]
+            naps = [row["nap"] for x in allr for row in x["rows"]]
+            out[f] = {"wall_s": wall, "steps_per_s": steps / wall, "final_val_mse": float(np.mean(vals)),
+                      "mean_nap": float(np.mean(naps))}
+        for f in out:
+            out[f]["speedup_vs_sync"] = out[f]["steps_per_s"] / out["sync"]["steps_per_s"]
+        result["train"] = out
     else:
         kind, unit = args.delay.split(":")
         model = DelayModel(kind, unit_ms=float(unit), k=1, seed=11)
