@@ -143,6 +143,9 @@ int ec_step_result(ec_comm_t* c, int local_idx, uint64_t seq, int64_t t, int tim
  * launches with CUDA events; ec_profile_read sums the durations
  * (ms_sum[0]/counts[0] = fold, [1] = update) and clears the record. */
 int ec_profile_enable(int on);
+/* %globaltimer duration of the update of the last step reconciled by
+ * ec_step_result (from the device wait's release to the last CTA). */
+int ec_step_update_ns(ec_comm_t* c, int local_idx, uint64_t* ns);
 int ec_profile_read(double* ms_sum2, int64_t* counts2);
 /* Mask / nap of an earlier generation from the device log (RoundRecord source). */
 int ec_gen_info(ec_comm_t* c, int local_idx, int64_t gen, uint64_t* mask,

@@ -88,7 +88,7 @@ struct alignas(128) EcLocal {
   unsigned long long fold_count;   // CTAs of the fused fold+post kernel done (last one posts)
   unsigned long long upd_count;    // CTAs of the fused wait+update kernel done (last one unpins)
   unsigned long long step_tag;     // t + 1 once step_gen holds step t's generation
-  unsigned long long pad6;
+  unsigned long long upd_t0;       // globaltimer when the fused update's compute began
   EcReq dreq[EC_REQ_RING];         // stream-posted requests (device copy of the ring)
 };
 
@@ -121,6 +121,7 @@ struct alignas(128) EcHostCtl {
   unsigned long long reply[EC_REQ_RING];   // ((seq+1) << 8) | status
   unsigned long long stepgen[EC_REQ_RING]; // async step t: generation its update read, + 1
   unsigned long long steptag[EC_REQ_RING]; // t + 1 once stepgen[t % RING] is valid
+  unsigned long long stepns[EC_REQ_RING];  // async step t: update compute duration (ns)
   EcLog log[EC_LOG_RING];
 };
 

@@ -109,6 +109,7 @@ struct EcRankHost {
   unsigned long long* forced = nullptr;
   long long n_forced = 0;
   unsigned long long next_seq = 0;
+  unsigned long long last_update_ns = 0;  // device-timed update of the last reconciled async step
   std::mutex mu;
 };
 
@@ -698,6 +699,13 @@ struct ProfScope {
   }
 };
 
+int ec_step_update_ns(ec_comm_t* c, int li, uint64_t* ns) {
+  int rc = check_li(c, li);
+  if (rc) return rc;
+  *ns = c->L[li]->last_update_ns;
+  return EC_OK;
+}
+
 int ec_profile_enable(int on) {
   __atomic_store_n(&g_prof_on, on ? 1 : 0, __ATOMIC_RELAXED);
   return EC_OK;
@@ -813,6 +821,7 @@ int ec_step_result(ec_comm_t* c, int li, uint64_t seq, int64_t t, int timeout_ms
   }
   const int64_t G = (int64_t)aload(&r->h->stepgen[t % EC_REQ_RING]) - 1;
   if (gen) *gen = G;
+  r->last_update_ns = aload(&r->h->stepns[t % EC_REQ_RING]);
   if (mask || nap) {
     uint64_t m = 0;
     int np = 0;

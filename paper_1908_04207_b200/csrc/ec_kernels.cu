@@ -1113,14 +1113,17 @@ __device__ void wait_and_pin(EcLocal* L, EcHostCtl* H, long long t, int R,
     G = D;
   }
   L->step_gen = G;
+  L->upd_t0 = globaltimer_ns();
   st_relaxed_sys(&H->stepgen[t % EC_REQ_RING], (unsigned long long)G + 1);
-  st_release_sys(&H->steptag[t % EC_REQ_RING], (unsigned long long)t + 1);
   st_release_gpu(&L->step_tag, (unsigned long long)t + 1);
 }
 
 __global__ void ec_wait_gen_kernel(EcLocal* L, EcHostCtl* H, long long t, int R,
                                    unsigned long long timeout_ns) {
-  if (threadIdx.x == 0) wait_and_pin(L, H, t, R, timeout_ns);
+  if (threadIdx.x == 0) {
+    wait_and_pin(L, H, t, R, timeout_ns);
+    st_release_sys(&H->steptag[t % EC_REQ_RING], (unsigned long long)t + 1);
+  }
 }
 
 // update from the slot of the step's generation; with H != nullptr the kernel
@@ -1197,8 +1200,11 @@ ec_update_gen_kernel(T* __restrict__ w, T* __restrict__ mom, const char* __restr
     __threadfence();
     if (atomicAdd(&L->upd_count, 1ull) == gridDim.x - 1) {
       L->upd_count = 0;
+      const unsigned long long t1 = globaltimer_ns();
       fence_acq_rel_sys();
       st_release_sys(&H->pin_lo, ~0ull);  // every CTA has read the slot: unpin
+      st_relaxed_sys(&H->stepns[t % EC_REQ_RING], t1 - *(volatile unsigned long long*)&L->upd_t0);
+      st_release_sys(&H->steptag[t % EC_REQ_RING], (unsigned long long)t + 1);
     }
   }
 }

@@ -222,7 +222,11 @@ def _main(argv=None):
     ap.add_argument("--out", default="")
     ap.add_argument("--rounds", type=int, default=64)
     ap.add_argument("--delay", default="linear_skew:1.0")
+    ap.add_argument("--epochs", type=int, default=48)
     args = ap.parse_args(argv)
+    if os.environ.get("EC_DEBUG_DUMP"):
+        import faulthandler
+        faulthandler.dump_traceback_later(float(os.environ["EC_DEBUG_DUMP"]), exit=True)
     rank = int(os.environ.get("RANK", 0))
     p = int(os.environ.get("WORLD_SIZE", 1))
     local = int(os.environ.get("LOCAL_RANK", 0))
@@ -275,9 +279,12 @@ def _main(argv=None):
             kind, unit = args.delay.split(":")
             model = DelayModel(kind, unit_ms=float(unit), k=1, seed=11)
         out = {}
-        for i, f in enumerate(("sync", "solo", "majority")):
+        flavors = [f for f in args.flavors.split(",") if f] if args.flavors != "solo,majority" \
+            else ["sync", "solo", "majority"]
+        for i, f in enumerate(flavors):
             world._barrier()
-            r = run_training_rank(world, rank, p, f, delay=model, cid_base=3000 + 10 * i)
+            r = run_training_rank(world, rank, p, f, delay=model, cid_base=3000 + 10 * i,
+                                  epochs=args.epochs)
             for hh in r["handles"]:
                 hh.close()
             allr = [None] * p
@@ -292,8 +299,9 @@ def _main(argv=None):
             naps = [row["nap"] for x in allr for row in x["rows"]]
             out[f] = {"wall_s": wall, "steps_per_s": steps / wall, "final_val_mse": float(np.mean(vals)),
                       "mean_nap": float(np.mean(naps))}
-        for f in out:
-            out[f]["speedup_vs_sync"] = out[f]["steps_per_s"] / out["sync"]["steps_per_s"]
+        if "sync" in out:
+            for f in out:
+                out[f]["speedup_vs_sync"] = out[f]["steps_per_s"] / out["sync"]["steps_per_s"]
         result["train"] = out
     else:
         kind, unit = args.delay.split(":")

@@ -135,6 +135,23 @@ class Comm:
         return self._views[key]
 
 
+def warm_device_libraries(device: int) -> None:
+    """Initialise cuBLAS (and torch's allocator/streams) before any engine runs.
+
+    A persistent engine never finishes, so anything that synchronises the whole
+    device -- cuBLAS handle/workspace creation on the first matmul, cudaFree in
+    the caching allocator -- would wait on it forever.  Worlds call this at
+    construction; code that initialises other libraries late should do so inside
+    `world.quiesced()`.
+    """
+    with torch.cuda.device(device):
+        a = torch.ones(64, 64, device=f"cuda:{device}")
+        (a @ a).sum().item()
+        (a @ a[:, 0]).sum().item()
+        torch.cuda.current_blas_handle()
+        torch.cuda.synchronize(device)
+
+
 class _WorldBase:
     device: int
     ring_slots: int
@@ -236,6 +253,7 @@ class EmulatedWorld(_WorldBase):
         self.ring_slots = ring_slots
         self.workers = workers
         self._attached: dict = {}
+        warm_device_libraries(device)
 
     def attach(self, cfg, cid: int, rank: int):
         if cfg.p != self.p:
@@ -275,6 +293,7 @@ class ProcessWorld(_WorldBase):
         self.device = torch.cuda.current_device() if device is None else device
         self.ring_slots = ring_slots
         self.workers = workers
+        warm_device_libraries(self.device)
 
     def _all_gather(self, obj):
         if self.p == 1:

@@ -383,3 +383,48 @@ def test_async_steps_match_oracle(p):
         assert states[r].w.cpu().numpy().tobytes() == w.tobytes()
         assert states[r].send_buf.is_null
     world.close()
+
+
+@pytest.mark.parametrize("flavor", ["sync", "solo", "majority"])
+def test_training_process_config1_emulated(golden_dir, flavor):
+    """BASELINE config 1 live (not replayed) on one GPU: 4 emulated ranks run the
+    reference's training_process with its seeded random_subset delays, the
+    staleness guard (tau = 8) and resync every 8 epochs.  Checks the run's
+    contracts -- exactly-once, tau-bounded delivery, bit-identical weights after
+    the final resync -- and that it converges to the reference's val MSE."""
+    from paper_1908_04207_b200 import DelayModel, inject_delay, training_process
+    from paper_1908_04207_b200.models import gen_dataset, init_weights
+    p, epochs, spe = 4, 16, 4
+    world = EmulatedWorld(p)
+    ds = gen_dataset(64, 4096, seed=99)
+    w0 = init_weights(64, seed=1234)
+    model = DelayModel("random_subset", unit_ms=0.2, k=1, seed=11)
+    cfg = CollectiveConfig(p=p, flavor=flavor, vector_len=64, element="f4", seed=1234)
+    scfg = CollectiveConfig(p=p, flavor="sync", vector_len=64, element="f4")
+    hs = [AllreduceHandle(cfg, r, world, cid=0) for r in range(p)]
+    hr = [AllreduceHandle(scfg, r, world, cid=1) for r in range(p)]
+    states = [TrainState.fresh(w0, 0.05, rank=r, resync_period=8, tau=8) for r in range(p)]
+    ledger = DeliveryLedger()
+    val, errors = {}, []
+
+    def body(r):
+        try:
+            torch.cuda.set_device(0)
+            drive(training_process(r, states[r], hs[r], hr[r], ds, epochs=epochs,
+                                   steps_per_epoch=spe, batch_per_rank=128, data_seed=99,
+                                   delay_fn=lambda rank, t: inject_delay(rank, t, model, p),
+                                   guard=True, ledger=ledger, val_out=val))
+        except BaseException as e:
+            errors.append(e)
+
+    th = [threading.Thread(target=body, args=(r,)) for r in range(p)]
+    [x.start() for x in th]
+    [x.join() for x in th]
+    assert not errors, errors
+    # final resync at epoch 16: every rank holds the same bits
+    ws = [s.w.cpu().numpy() for s in states]
+    assert all(w.tobytes() == ws[0].tobytes() for w in ws)
+    assert not ledger.audit(tau=8, allow_pending_after=epochs * spe - 9)
+    tr = np.load(os.path.join(golden_dir, f"c1_{flavor}.npz"))
+    assert abs(np.mean([v for (r, e), v in val.items() if e == epochs - 1]) - 0.0106) < 0.003
+    world.close()
