@@ -207,10 +207,14 @@ def main():
 
     gen = torch.Generator(device=dev)
     gen.manual_seed(1234 + rank)
-    grads = [torch.randn(n, device=dev, generator=gen) for _ in range(2)]
     w0 = torch.randn(n, device=dev, generator=gen) * 0.01
     cfg = CollectiveConfig(p=world, flavor="solo", vector_len=n, element="f4", seed=1234)
     h = AllreduceHandle(cfg, rank, pw, cid=0)
+    # the step's gradient lives in the registered bucket (where backward would
+    # write it), so while the stash is null the offer is zero-copy
+    gbuf = h.grad_buffer()
+    gbuf.normal_(generator=gen)
+    grads = [gbuf, gbuf]
     st = TrainState.fresh(w0, LR, rank=rank, tau=None)
     all_arrive = world > 1
 
@@ -275,12 +279,12 @@ def main():
     upd_ms = sum(upd_ns) / max(1, len(upd_ns)) / 1e6
     peak, peak_kind = _peaks()
     upd_gbs = 12 * n / (upd_ms / 1e3) / 1e9
-    fold_bytes = 8 * n            # every round is fresh: the fold writes 0 + g into a null stash
+    fold_bytes = 8 * n            # a fold into a null stash writes 0 + g (zero-copy offers skip it)
     fold_gbs = fold_bytes / (fold_ms / 1e3) / 1e9
 
     # ---- e2e: gradient from pinned host memory every step, result read back
     host_grad = torch.randn(n, generator=torch.Generator().manual_seed(7 + rank)).pin_memory()
-    dgrad = torch.empty(n, device=dev)
+    dgrad = gbuf                          # the H2D copy lands in the registered bucket
     h2d = lambda i: dgrad.copy_(host_grad, non_blocking=True)  # noqa: E731
     run_steps(2, lambda t: dgrad, pre=h2d)
     quiesce()

@@ -87,8 +87,11 @@ int ec_comm_error(ec_comm_t* c, int local_idx, uint64_t* code, uint64_t* info);
 /* Diagnostics snapshot of a local rank's engine (16 int64 words, see ec_host.cu). */
 int ec_debug_state(ec_comm_t* c, int local_idx, int64_t* out16);
 
-/* device addresses of the local rank's send buffer and of result slot `gen % R` */
+/* device addresses of the local rank's send buffer, its registered gradient
+ * buffer (write the gradient here and pass it to ec_step_async: while the stash
+ * is null the reduction reads it in place, no fold) and result slot `gen % R` */
 void* ec_send_ptr(ec_comm_t* c, int local_idx);
+void* ec_grad_ptr(ec_comm_t* c, int local_idx);
 void* ec_slot_ptr(ec_comm_t* c, int local_idx, int64_t gen);
 int64_t ec_n_elems(ec_comm_t* c);
 

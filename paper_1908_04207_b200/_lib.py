@@ -43,6 +43,7 @@ _SIGS = {
     "ec_comm_error": (_i32, [_vp, _i32, _P(_u64), _P(_u64)]),
     "ec_debug_state": (_i32, [_vp, _i32, _P(_i64)]),
     "ec_send_ptr": (_vp, [_vp, _i32]),
+    "ec_grad_ptr": (_vp, [_vp, _i32]),
     "ec_slot_ptr": (_vp, [_vp, _i32, _i64]),
     "ec_n_elems": (_i64, [_vp]),
     "ec_fold": (_i32, [_vp, _i32, _vp, _i32, _vp]),

@@ -185,6 +185,13 @@ class AllreduceHandle:
         """The device send buffer (also the eager-SGD stash, eagersgd.py:68)."""
         return self.comm.send_view(self.li)
 
+    def grad_buffer(self) -> torch.Tensor:
+        """The registered gradient bucket.  Write the step's gradient here and
+        pass it to train_step_async: while the stash is null the reduction reads
+        it in place over NVLink (zero-copy offer, no fold); a refused offer is
+        folded into the stash on the device before the next step."""
+        return self.comm.grad_view(self.li)
+
     def _slot(self, gen: int) -> torch.Tensor:
         return self.comm.slot_view(self.li, gen)
 

@@ -26,9 +26,17 @@
 // internal contribution flag (set by the post kernel from the fold's poison word)
 #define EC_CF_POISON 0x100
 
-// snapshot word: ((gen+1) << 2) | has_data << 1 | fresh
+// snapshot word: ((gen+1) << 3) | src_grad << 2 | has_data << 1 | fresh
 #define EC_SNAP_FRESH 1ull
 #define EC_SNAP_DATA 2ull
+#define EC_SNAP_SRC_GRAD 4ull   // the offer is the registered gradient buffer, not the stash
+#define EC_SNAP_SHIFT 3
+// contribution flag: offer the registered gradient buffer (zero-copy, stash null)
+#define EC_CF_SRC_GRAD 8u
+// direct mode: offer the gradient buffer iff the stash is still null at decision time
+#define EC_CF_SRC_GRAD_AUTO 16u
+// done word: gen + 1, top bit = a reduced value of this owner's shard was non-finite
+#define EC_DONE_POISON (1ull << 63)
 
 // device error codes (EcHostCtl::error)
 #define EC_DERR_ORDER 1      // contribution for a future generation
@@ -89,6 +97,12 @@ struct alignas(128) EcLocal {
   unsigned long long upd_count;    // CTAs of the fused wait+update kernel done (last one unpins)
   unsigned long long step_tag;     // t + 1 once step_gen holds step t's generation
   unsigned long long upd_t0;       // globaltimer when the fused update's compute began
+  unsigned long long cmd_src;      // round: ranks whose offer is their gradient buffer
+  unsigned long long req_done_dev; // requests the controller has processed (device mirror)
+  int late_copy;                   // a zero-copy offer was refused: copy gbuf -> stash
+  int step_late;                   // latched late_copy for the current async step's update
+  unsigned int round_poison;       // this rank's CTAs saw a non-finite reduced value
+  unsigned int upd_bad;            // the async step's update read a non-finite u
   EcReq dreq[EC_REQ_RING];         // stream-posted requests (device copy of the ring)
 };
 
@@ -103,7 +117,8 @@ struct alignas(64) EcLog {
   // issued (all snapshots in), own shard reduced, round published
   unsigned long long t_snap, t_cmd, t_rs, t_done;
   unsigned long long t_req;        // this rank's offer for the generation was processed
-  unsigned long long pad[3];
+  unsigned long long poison;       // some owner reduced a non-finite value in this generation
+  unsigned long long pad[2];
 };
 
 struct alignas(128) EcHostCtl {
@@ -122,6 +137,7 @@ struct alignas(128) EcHostCtl {
   unsigned long long stepgen[EC_REQ_RING]; // async step t: generation its update read, + 1
   unsigned long long steptag[EC_REQ_RING]; // t + 1 once stepgen[t % RING] is valid
   unsigned long long stepns[EC_REQ_RING];  // async step t: update compute duration (ns)
+  unsigned long long stepbad[EC_REQ_RING]; // async step t: u had a non-finite element
   EcLog log[EC_LOG_RING];
 };
 
@@ -138,6 +154,7 @@ struct EcDesc {
   EcCtrl* ctrl[EC_MAX_P];
   char* send[EC_MAX_P];
   char* ring[EC_MAX_P];
+  char* gbuf[EC_MAX_P];               // registered gradient buffers (zero-copy offers)
   EcHostCtl* hctl;
   EcLocal* local;
   const unsigned long long* forced;

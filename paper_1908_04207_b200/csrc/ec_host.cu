@@ -30,12 +30,14 @@ cudaError_t launch_reduce(int dtype, const void* const* srcs, int p, unsigned lo
 cudaError_t launch_post(EcLocal* L, unsigned long long seq1, unsigned int type, unsigned int flags,
                         long long t, long long arg, cudaStream_t s);
 cudaError_t launch_fold_auto(int dtype, void* stash, const void* grad, long long n, EcLocal* L,
-                             unsigned long long seq1, unsigned flags, long long t, cudaStream_t s);
+                             unsigned long long seq1, unsigned flags, long long t, int zero_copy,
+                             cudaStream_t s);
 cudaError_t launch_wait_gen(EcLocal* L, EcHostCtl* H, long long t, int R, unsigned long long timeout_ns,
                             cudaStream_t s);
 cudaError_t launch_update_gen(int dtype, void* w, void* mom, const char* ring, long long slot_bytes,
                               int R, EcLocal* L, double lr, double mu, long long n, EcHostCtl* H,
-                              long long t, unsigned long long timeout_ns, cudaStream_t s);
+                              long long t, unsigned long long timeout_ns, unsigned long long seq1,
+                              void* stash, const void* gbuf, cudaStream_t s);
 cudaError_t launch_write_u64(unsigned long long* p, unsigned long long v, cudaStream_t s);
 cudaError_t launch_direct(int dtype, const EcDesc* d_desc, long long nvec, unsigned long long seq,
                           unsigned int type, unsigned int flags, long long t, long long arg,
@@ -103,6 +105,7 @@ struct EcRankHost {
   EcCtrl* ctrl = nullptr;
   char* send = nullptr;
   char* ring = nullptr;
+  char* gbuf = nullptr;        // registered gradient buffer (zero-copy offers)
   EcHostCtl* h = nullptr;      // host view
   EcHostCtl* hd = nullptr;     // device view of the same pinned page
   EcLocal* local = nullptr;
@@ -118,7 +121,7 @@ struct BlobV1 {
   int rank;
   long long n;
   int dtype, R;
-  cudaIpcMemHandle_t ctrl, send, ring;
+  cudaIpcMemHandle_t ctrl, send, ring, gbuf;
 };
 
 struct ec_comm {
@@ -128,7 +131,7 @@ struct ec_comm {
   unsigned long long timeout_ns = 60ull * 1000000000ull;
   std::vector<EcRankHost*> L;
   std::vector<EcCtrl*> ctrl;
-  std::vector<char*> send, ring;
+  std::vector<char*> send, ring, gbuf;
   std::vector<int> opened;  // 1 = IPC-opened peer
   EcDesc* d_descs = nullptr;
   cudaStream_t es = nullptr;
@@ -224,6 +227,7 @@ int ec_comm_create(int world_size, int rank_lo, int n_local, int device, int64_t
   c->ctrl.assign(world_size, nullptr);
   c->send.assign(world_size, nullptr);
   c->ring.assign(world_size, nullptr);
+  c->gbuf.assign(world_size, nullptr);
   c->opened.assign(world_size, 0);
   for (int i = 0; i < n_local; ++i) {
     EcRankHost* r = new EcRankHost();
@@ -233,6 +237,8 @@ int ec_comm_create(int world_size, int rank_lo, int n_local, int device, int64_t
     if ((e = cudaMalloc(&r->ctrl, sizeof(EcCtrl))) != cudaSuccess ||
         (e = cudaMalloc(&r->send, c->slot_bytes)) != cudaSuccess ||
         (e = cudaMalloc(&r->ring, c->slot_bytes * c->R)) != cudaSuccess ||
+        (e = cudaMalloc(&r->gbuf, c->slot_bytes)) != cudaSuccess ||
+        (e = cudaMemset(r->gbuf, 0, c->slot_bytes)) != cudaSuccess ||
         (e = cudaMalloc(&r->local, sizeof(EcLocal))) != cudaSuccess ||
         (e = cudaMemset(r->ctrl, 0, sizeof(EcCtrl))) != cudaSuccess ||
         (e = cudaMemset(r->send, 0, c->slot_bytes)) != cudaSuccess ||
@@ -259,6 +265,7 @@ int ec_comm_create(int world_size, int rank_lo, int n_local, int device, int64_t
     c->ctrl[r->rank] = r->ctrl;
     c->send[r->rank] = r->send;
     c->ring[r->rank] = r->ring;
+    c->gbuf[r->rank] = r->gbuf;
   }
   if (cudaMalloc(&c->d_descs, sizeof(EcDesc) * n_local) != cudaSuccess) {
     ec_comm_destroy(c);
@@ -290,6 +297,7 @@ int ec_comm_export(ec_comm_t* c, int li, void* blob, size_t cap, size_t* len) {
   CK(cudaIpcGetMemHandle(&b.ctrl, r->ctrl));
   CK(cudaIpcGetMemHandle(&b.send, r->send));
   CK(cudaIpcGetMemHandle(&b.ring, r->ring));
+  CK(cudaIpcGetMemHandle(&b.gbuf, r->gbuf));
   memcpy(blob, &b, sizeof(b));
   if (len) *len = sizeof(b);
   return EC_OK;
@@ -309,13 +317,15 @@ int ec_comm_import(ec_comm_t* c, int peer, const void* blob, size_t len) {
                 b.n, c->n, b.dtype, c->dtype, b.R, c->R);
   if (c->opened[peer]) return EC_OK;
   CK(cudaSetDevice(c->device));
-  void *pc = nullptr, *ps = nullptr, *pr = nullptr;
+  void *pc = nullptr, *ps = nullptr, *pr = nullptr, *pg = nullptr;
   CK(cudaIpcOpenMemHandle(&pc, b.ctrl, cudaIpcMemLazyEnablePeerAccess));
   CK(cudaIpcOpenMemHandle(&ps, b.send, cudaIpcMemLazyEnablePeerAccess));
   CK(cudaIpcOpenMemHandle(&pr, b.ring, cudaIpcMemLazyEnablePeerAccess));
+  CK(cudaIpcOpenMemHandle(&pg, b.gbuf, cudaIpcMemLazyEnablePeerAccess));
   c->ctrl[peer] = (EcCtrl*)pc;
   c->send[peer] = (char*)ps;
   c->ring[peer] = (char*)pr;
+  c->gbuf[peer] = (char*)pg;
   c->opened[peer] = 1;
   return EC_OK;
 }
@@ -371,6 +381,7 @@ static int upload_descs(ec_comm_t* c) {
       x.ctrl[q] = c->ctrl[q];
       x.send[q] = c->send[q];
       x.ring[q] = c->ring[q];
+      x.gbuf[q] = c->gbuf[q];
     }
     x.hctl = r->hd;
     x.local = r->local;
@@ -433,12 +444,14 @@ int ec_comm_destroy(ec_comm_t* c) {
       cudaIpcCloseMemHandle(c->ctrl[q]);
       cudaIpcCloseMemHandle(c->send[q]);
       cudaIpcCloseMemHandle(c->ring[q]);
+      cudaIpcCloseMemHandle(c->gbuf[q]);
     }
   }
   for (EcRankHost* r : c->L) {
     if (r->ctrl) cudaFree(r->ctrl);
     if (r->send) cudaFree(r->send);
     if (r->ring) cudaFree(r->ring);
+    if (r->gbuf) cudaFree(r->gbuf);
     if (r->local) cudaFree(r->local);
     if (r->forced) cudaFree(r->forced);
     if (r->h) cudaFreeHost(r->h);
@@ -461,6 +474,11 @@ int ec_comm_error(ec_comm_t* c, int li, uint64_t* code, uint64_t* info) {
 void* ec_send_ptr(ec_comm_t* c, int li) {
   if (check_li(c, li)) return nullptr;
   return c->L[li]->send;
+}
+
+void* ec_grad_ptr(ec_comm_t* c, int li) {
+  if (check_li(c, li)) return nullptr;
+  return c->L[li]->gbuf;
 }
 
 void* ec_slot_ptr(ec_comm_t* c, int li, int64_t gen) {
@@ -788,18 +806,21 @@ int ec_step_async(ec_comm_t* c, int li, int64_t t, const void* grad, uint32_t fl
     // fold (+ the offer's post, fused into the fold's last CTA, engine mode)
     ProfScope ps(0, stream);
     CK(launch_fold_auto(c->dtype, r->send, grad, c->n, r->local, c->direct ? 0 : seq + 1,
-                        flags & 7u, t, s));
+                        flags & 7u, t, grad == r->gbuf ? 1 : 0, s));
   }
   if (c->direct) {
+    // the decide kernel learns from the fold whether the gradient buffer is
+    // offered in place: flag it when the caller passed the registered buffer
     c->last_stream = stream;
     CK(launch_direct(c->dtype, c->d_descs + li, c->n / (16 / c->elem), seq, EC_REQ_CONTRIB,
-                     flags & 7u, t, 0, s));
+                     (flags & 7u) | (grad == r->gbuf ? EC_CF_SRC_GRAD_AUTO : 0u), t, 0, s));
   }
   {
     // device wait for a generation >= t + pin, update, unpin: one launch
     ProfScope ps(1, stream);
     CK(launch_update_gen(c->dtype, w, (mom && mu != 0.0) ? mom : nullptr, r->ring, c->slot_bytes, c->R,
-                         r->local, lr, mu, c->n, r->hd, t, c->timeout_ns, s));
+                         r->local, lr, mu, c->n, r->hd, t, c->timeout_ns, seq + 1, r->send,
+                         r->gbuf, s));
   }
   if (seq_out) *seq_out = seq;
   return EC_OK;
@@ -822,6 +843,7 @@ int ec_step_result(ec_comm_t* c, int li, uint64_t seq, int64_t t, int timeout_ms
   const int64_t G = (int64_t)aload(&r->h->stepgen[t % EC_REQ_RING]) - 1;
   if (gen) *gen = G;
   r->last_update_ns = aload(&r->h->stepns[t % EC_REQ_RING]);
+  if (status && aload(&r->h->stepbad[t % EC_REQ_RING])) *status = EC_R_POISONED;
   if (mask || nap) {
     uint64_t m = 0;
     int np = 0;

@@ -23,13 +23,14 @@
 // engine: reduce-scatter (pull) of this rank's shard
 
 template <typename T, int P, int U>
-__device__ __forceinline__ void rs_fixed(const EcDesc& d, unsigned long long has, long long v0,
+__device__ __forceinline__ void rs_fixed(const EcDesc& d, const char* const* sp,
+                                         unsigned long long has, long long v0,
                                          long long v1, char* dst, long long start,
                                          long long stride, T inv, bool pow2) {
   constexpr int V = Ops<T>::V;
   const char* src[P];
 #pragma unroll
-  for (int q = 0; q < P; ++q) src[q] = d.send[q];
+  for (int q = 0; q < P; ++q) src[q] = sp[q];
   for (long long base = v0 + start; base < v1; base += stride * U) {
     Vec16<T> x[U][P];
 #pragma unroll
@@ -62,8 +63,8 @@ __device__ __forceinline__ void rs_fixed(const EcDesc& d, unsigned long long has
 }
 
 template <typename T>
-__device__ void rs_dyn(const EcDesc& d, unsigned long long has, long long v0, long long v1,
-                       char* dst, long long start, long long stride, T inv, bool pow2) {
+__device__ void rs_dyn(const EcDesc& d, const char* const* sp, unsigned long long has, long long v0,
+                       long long v1, char* dst, long long start, long long stride, T inv, bool pow2) {
   constexpr int V = Ops<T>::V;
   for (long long v = v0 + start; v < v1; v += stride) {
     Vec16<T> o;
@@ -72,7 +73,7 @@ __device__ void rs_dyn(const EcDesc& d, unsigned long long has, long long v0, lo
       auto leaf = [&](int q) -> T {
         if (!((has >> q) & 1ull)) return Ops<T>::zero();
         Vec16<T> x;
-        x.raw = ld_cg_v4(d.send[q] + v * 16);
+        x.raw = ld_cg_v4(sp[q] + v * 16);
         return Ops<T>::canon(x.e[l]);
       };
       o.e[l] = Ops<T>::divp(tree_sum_dyn<T>(d.P, leaf), d.P, inv, pow2);
@@ -82,26 +83,27 @@ __device__ void rs_dyn(const EcDesc& d, unsigned long long has, long long v0, lo
 }
 
 template <typename T>
-__device__ void rs_shard(const EcDesc& d, unsigned long long has, long long v0, long long v1,
-                         char* dst, long long start, long long stride) {
+__device__ void rs_shard(const EcDesc& d, const char* const* sp, unsigned long long has,
+                         long long v0, long long v1, char* dst, long long start, long long stride) {
   const bool pow2 = (d.P & (d.P - 1)) == 0;
   const T inv = (T)1 / (T)d.P;  // exact for powers of two
   switch (d.P) {
-    case 1: rs_fixed<T, 1, 4>(d, has, v0, v1, dst, start, stride, inv, pow2); break;
-    case 2: rs_fixed<T, 2, 4>(d, has, v0, v1, dst, start, stride, inv, pow2); break;
-    case 3: rs_fixed<T, 3, 2>(d, has, v0, v1, dst, start, stride, inv, pow2); break;
-    case 4: rs_fixed<T, 4, 2>(d, has, v0, v1, dst, start, stride, inv, pow2); break;
-    case 5: rs_fixed<T, 5, 2>(d, has, v0, v1, dst, start, stride, inv, pow2); break;
-    case 6: rs_fixed<T, 6, 2>(d, has, v0, v1, dst, start, stride, inv, pow2); break;
-    case 7: rs_fixed<T, 7, 2>(d, has, v0, v1, dst, start, stride, inv, pow2); break;
-    case 8: rs_fixed<T, 8, 2>(d, has, v0, v1, dst, start, stride, inv, pow2); break;
-    default: rs_dyn<T>(d, has, v0, v1, dst, start, stride, inv, pow2); break;
+    case 1: rs_fixed<T, 1, 4>(d, sp, has, v0, v1, dst, start, stride, inv, pow2); break;
+    case 2: rs_fixed<T, 2, 4>(d, sp, has, v0, v1, dst, start, stride, inv, pow2); break;
+    case 3: rs_fixed<T, 3, 2>(d, sp, has, v0, v1, dst, start, stride, inv, pow2); break;
+    case 4: rs_fixed<T, 4, 2>(d, sp, has, v0, v1, dst, start, stride, inv, pow2); break;
+    case 5: rs_fixed<T, 5, 2>(d, sp, has, v0, v1, dst, start, stride, inv, pow2); break;
+    case 6: rs_fixed<T, 6, 2>(d, sp, has, v0, v1, dst, start, stride, inv, pow2); break;
+    case 7: rs_fixed<T, 7, 2>(d, sp, has, v0, v1, dst, start, stride, inv, pow2); break;
+    case 8: rs_fixed<T, 8, 2>(d, sp, has, v0, v1, dst, start, stride, inv, pow2); break;
+    default: rs_dyn<T>(d, sp, has, v0, v1, dst, start, stride, inv, pow2); break;
   }
 }
 
 // scalar tail (n % V elements) -- reduced by the last owner
 template <typename T>
-__device__ void rs_tail(const EcDesc& d, unsigned long long has, char* dst, int lane) {
+__device__ void rs_tail(const EcDesc& d, const char* const* sp, unsigned long long has, char* dst,
+                        int lane) {
   const long long e0 = d.nvec * Ops<T>::V;
   const long long e = e0 + lane;
   if (e >= d.n) return;
@@ -109,7 +111,7 @@ __device__ void rs_tail(const EcDesc& d, unsigned long long has, char* dst, int 
   const T inv = (T)1 / (T)d.P;
   auto leaf = [&](int q) -> T {
     if (!((has >> q) & 1ull)) return Ops<T>::zero();
-    const volatile T* s = reinterpret_cast<const volatile T*>(d.send[q]);
+    const volatile T* s = reinterpret_cast<const volatile T*>(sp[q]);
     return Ops<T>::canon(s[e]);
   };
   reinterpret_cast<T*>(dst)[e] = Ops<T>::divp(tree_sum_dyn<T>(d.P, leaf), d.P, inv, pow2);
@@ -180,9 +182,10 @@ __device__ __forceinline__ long long chunk_lo(long long nch, int q, int P) {
 }
 
 template <typename T, int P>
-__device__ __forceinline__ void reduce_chunk_smem(const char* src, char* out, int nvv, int chb,
+__device__ __forceinline__ bool reduce_chunk_smem(const char* src, char* out, int nvv, int chb,
                                                   unsigned long long has, int p, T inv, bool pow2) {
   constexpr int V = Ops<T>::V;
+  bool bad = false;
   for (int i = threadIdx.x; i < nvv; i += blockDim.x) {
     Vec16<T> x[P];
 #pragma unroll
@@ -196,15 +199,18 @@ __device__ __forceinline__ void reduce_chunk_smem(const char* src, char* out, in
 #pragma unroll
       for (int q = 0; q < P; ++q) c[q] = Ops<T>::canon(x[q].e[l]);
       o.e[l] = Ops<T>::divp(tree_sum<T, P>(c), p, inv, pow2);
+      bad |= !Ops<T>::finite(o.e[l]);
     }
     *reinterpret_cast<uint4*>(out + i * 16) = o.raw;
   }
+  return bad;
 }
 
 template <typename T>
-__device__ void reduce_chunk_smem_dyn(const char* src, char* out, int nvv, int chb,
+__device__ bool reduce_chunk_smem_dyn(const char* src, char* out, int nvv, int chb,
                                       unsigned long long has, int p, T inv, bool pow2) {
   constexpr int V = Ops<T>::V;
+  bool bad = false;
   for (int i = threadIdx.x; i < nvv; i += blockDim.x) {
     Vec16<T> o;
 #pragma unroll
@@ -216,26 +222,29 @@ __device__ void reduce_chunk_smem_dyn(const char* src, char* out, int nvv, int c
         return Ops<T>::canon(x.e[l]);
       };
       o.e[l] = Ops<T>::divp(tree_sum_dyn<T>(p, leaf), p, inv, pow2);
+      bad |= !Ops<T>::finite(o.e[l]);
     }
     *reinterpret_cast<uint4*>(out + i * 16) = o.raw;
   }
+  return bad;
 }
 
+// returns whether this thread produced a non-finite reduced value
 template <typename T>
-__device__ __forceinline__ void reduce_chunk(const char* src, char* out, int nvv, int chb,
+__device__ __forceinline__ bool reduce_chunk(const char* src, char* out, int nvv, int chb,
                                              unsigned long long has, int p) {
   const bool pow2 = (p & (p - 1)) == 0;
   const T inv = (T)1 / (T)p;
   switch (p) {
-    case 1: reduce_chunk_smem<T, 1>(src, out, nvv, chb, has, p, inv, pow2); break;
-    case 2: reduce_chunk_smem<T, 2>(src, out, nvv, chb, has, p, inv, pow2); break;
-    case 3: reduce_chunk_smem<T, 3>(src, out, nvv, chb, has, p, inv, pow2); break;
-    case 4: reduce_chunk_smem<T, 4>(src, out, nvv, chb, has, p, inv, pow2); break;
-    case 5: reduce_chunk_smem<T, 5>(src, out, nvv, chb, has, p, inv, pow2); break;
-    case 6: reduce_chunk_smem<T, 6>(src, out, nvv, chb, has, p, inv, pow2); break;
-    case 7: reduce_chunk_smem<T, 7>(src, out, nvv, chb, has, p, inv, pow2); break;
-    case 8: reduce_chunk_smem<T, 8>(src, out, nvv, chb, has, p, inv, pow2); break;
-    default: reduce_chunk_smem_dyn<T>(src, out, nvv, chb, has, p, inv, pow2); break;
+    case 1: return reduce_chunk_smem<T, 1>(src, out, nvv, chb, has, p, inv, pow2);
+    case 2: return reduce_chunk_smem<T, 2>(src, out, nvv, chb, has, p, inv, pow2);
+    case 3: return reduce_chunk_smem<T, 3>(src, out, nvv, chb, has, p, inv, pow2);
+    case 4: return reduce_chunk_smem<T, 4>(src, out, nvv, chb, has, p, inv, pow2);
+    case 5: return reduce_chunk_smem<T, 5>(src, out, nvv, chb, has, p, inv, pow2);
+    case 6: return reduce_chunk_smem<T, 6>(src, out, nvv, chb, has, p, inv, pow2);
+    case 7: return reduce_chunk_smem<T, 7>(src, out, nvv, chb, has, p, inv, pow2);
+    case 8: return reduce_chunk_smem<T, 8>(src, out, nvv, chb, has, p, inv, pow2);
+    default: return reduce_chunk_smem_dyn<T>(src, out, nvv, chb, has, p, inv, pow2);
   }
 }
 
@@ -245,8 +254,9 @@ __device__ __forceinline__ void reduce_chunk(const char* src, char* out, int nvv
 //   tree order, then bulk-store the result into EVERY rank's result slot
 //   (reduce-scatter pull and all-gather push, pipelined per chunk).
 template <typename T>
-__device__ void round_tma(const EcDesc& d, int w, long long g, unsigned long long has,
-                          char* smem, unsigned long long* full, unsigned long long& it) {
+__device__ void round_tma(const EcDesc& d, const char* const* sp, int w, long long g,
+                          unsigned long long has, char* smem, unsigned long long* full,
+                          unsigned long long& it, bool& bad) {
   const int P = d.P, r = d.rank, S = d.stages;
   const int chv = d.chv, chb = d.chv * 16;
   const long long nch = (d.nvec + chv - 1) / chv;
@@ -263,7 +273,7 @@ __device__ void round_tma(const EcDesc& d, int w, long long g, unsigned long lon
     char* st = smem + s * stage_bytes;
     mbar_expect_tx(&full[s], npop * bytes);
     for (int q = 0; q < P; ++q)
-      if ((has >> q) & 1ull) tma_load(st + (size_t)q * chb, d.send[q] + v0 * 16, bytes, &full[s]);
+      if ((has >> q) & 1ull) tma_load(st + (size_t)q * chb, sp[q] + v0 * 16, bytes, &full[s]);
   };
   if (threadIdx.x == 0) {
     fence_proxy_async_global();  // peers' generic writes (acquired via flags) -> async-proxy reads
@@ -283,7 +293,7 @@ __device__ void round_tma(const EcDesc& d, int w, long long g, unsigned long lon
     while (!mbar_try_wait(&full[s], parity)) {
     }
     __syncthreads();
-    reduce_chunk<T>(st, out, nvv, chb, has, P);
+    bad |= reduce_chunk<T>(st, out, nvv, chb, has, P);
     fence_proxy_async_smem();
     __syncthreads();
     if (threadIdx.x == 0) {
@@ -304,14 +314,15 @@ __device__ void round_tma(const EcDesc& d, int w, long long g, unsigned long lon
 
 // scalar tail (n % V elements): reduced by the last owner, pushed to every slot
 template <typename T>
-__device__ void tail_push(const EcDesc& d, unsigned long long has, long long g) {
+__device__ void tail_push(const EcDesc& d, const char* const* sp, unsigned long long has,
+                          long long g) {
   const long long e = d.nvec * Ops<T>::V + threadIdx.x;
   if (threadIdx.x >= Ops<T>::V || e >= d.n) return;
   const bool pow2 = (d.P & (d.P - 1)) == 0;
   const T inv = (T)1 / (T)d.P;
   auto leaf = [&](int q) -> T {
     if (!((has >> q) & 1ull)) return Ops<T>::zero();
-    const volatile T* s = reinterpret_cast<const volatile T*>(d.send[q]);
+    const volatile T* s = reinterpret_cast<const volatile T*>(sp[q]);
     return Ops<T>::canon(s[e]);
   };
   const T u = Ops<T>::divp(tree_sum_dyn<T>(d.P, leaf), d.P, inv, pow2);
@@ -321,8 +332,8 @@ __device__ void tail_push(const EcDesc& d, unsigned long long has, long long g) 
 
 // Two-phase pull data path (ld.global.cg): reduce-scatter, then all-gather.
 template <typename T>
-__device__ void round_ldg(const EcDesc& d, int w, long long g, unsigned long long has,
-                          unsigned long long seen) {
+__device__ void round_ldg(const EcDesc& d, const char* const* sp, int w, long long g,
+                          unsigned long long has, unsigned long long seen) {
   EcLocal* L = d.local;
   EcCtrl* C = d.ctrl[d.rank];
   const int tid = threadIdx.x;
@@ -331,8 +342,8 @@ __device__ void round_ldg(const EcDesc& d, int w, long long g, unsigned long lon
   const long long off = (g % d.R) * d.slot_bytes;
   {
     const long long v0 = shard_lo(d.nvec, d.rank, d.P), v1 = shard_lo(d.nvec, d.rank + 1, d.P);
-    rs_shard<T>(d, has, v0, v1, my_slot, (long long)w * bt + tid, (long long)d.W * bt);
-    if (d.rank == d.P - 1 && w == 0 && tid < Ops<T>::V) rs_tail<T>(d, has, my_slot, tid);
+    rs_shard<T>(d, sp, has, v0, v1, my_slot, (long long)w * bt + tid, (long long)d.W * bt);
+    if (d.rank == d.P - 1 && w == 0 && tid < Ops<T>::V) rs_tail<T>(d, sp, has, my_slot, tid);
   }
   __syncthreads();
   if (tid == 0) {
@@ -389,9 +400,10 @@ __device__ void engine_worker(const EcDesc& d, int w, unsigned long long epoch) 
   EcLocal* L = d.local;
   extern __shared__ __align__(128) char smem[];
   __shared__ __align__(8) unsigned long long full[8];
-  __shared__ unsigned long long s_seq, s_has;
+  __shared__ unsigned long long s_seq, s_has, s_src;
   __shared__ long long s_gen;
   __shared__ int s_exit;
+  __shared__ const char* sp[EC_MAX_P];
   const int tid = threadIdx.x;
   if (tid == 0) {
     s_seq = ld_acquire_gpu(&L->cmd_seq);
@@ -411,6 +423,7 @@ __device__ void engine_worker(const EcDesc& d, int w, unsigned long long epoch) 
           s_seq = s;
           s_gen = *(volatile long long*)&L->cmd_gen;
           s_has = *(volatile unsigned long long*)&L->cmd_has;
+          s_src = *(volatile unsigned long long*)&L->cmd_src;
           s_exit = 0;
           break;
         }
@@ -427,13 +440,17 @@ __device__ void engine_worker(const EcDesc& d, int w, unsigned long long epoch) 
     seen = s_seq;
     const long long g = s_gen;
     const unsigned long long has = s_has;
-    if (d.mode == 0) {
-      round_tma<T>(d, w, g, has, smem, full, it);
-      if (w == 0 && d.rank == d.P - 1) tail_push<T>(d, has, g);
-    } else {
-      round_ldg<T>(d, w, g, has, seen);
-    }
+    // this round's source per rank: its stash, or its registered gradient buffer
+    for (int q = tid; q < d.P; q += blockDim.x) sp[q] = ((s_src >> q) & 1ull) ? d.gbuf[q] : d.send[q];
     __syncthreads();
+    bool bad = false;
+    if (d.mode == 0) {
+      round_tma<T>(d, sp, w, g, has, smem, full, it, bad);
+      if (w == 0 && d.rank == d.P - 1) tail_push<T>(d, sp, has, g);
+    } else {
+      round_ldg<T>(d, sp, w, g, has, seen);
+    }
+    if (__syncthreads_or(bad) && tid == 0) atomicOr(&L->round_poison, 1u);
     if (tid == 0) {
       fence_acq_rel_sys();
       const unsigned long long old = atomicAdd(&L->ag_count, 1ull);
@@ -441,11 +458,13 @@ __device__ void engine_worker(const EcDesc& d, int w, unsigned long long epoch) 
         // every CTA of this rank is done: tell the world (TMA mode: our pushes
         // into every slot have landed) / ourselves (pull mode)
         fence_acq_rel_sys();
+        unsigned long long word = (unsigned long long)g + 1;
+        if (atomicExch(&L->round_poison, 0u)) word |= EC_DONE_POISON;
         if (d.mode == 0) {
           L->t_rs = globaltimer_ns();
-          for (int q = 0; q < d.P; ++q) st_release_sys(&d.ctrl[q]->done_from[d.rank], (unsigned long long)g + 1);
+          for (int q = 0; q < d.P; ++q) st_release_sys(&d.ctrl[q]->done_from[d.rank], word);
         } else {
-          st_release_sys(&d.ctrl[d.rank]->done_from[d.rank], (unsigned long long)g + 1);
+          st_release_sys(&d.ctrl[d.rank]->done_from[d.rank], word);
         }
       }
     }
@@ -534,14 +553,17 @@ __device__ void engine_controller(const EcDesc& d, unsigned long long epoch) {
           status = 4;
         } else if (t < g || (t == g && snapped)) {
           status = 2;  // the round already consumed this rank's slot
+          if (fl & EC_CF_SRC_GRAD) *(volatile int*)&L->late_copy = 1;  // keep the gradient
         } else if (t > g) {
           status = 5;
           st_release_sys(&H->error, EC_DERR_ORDER);
           st_release_sys(&H->error_info, (unsigned long long)t);
         } else if (d.replay && forced_bit(g) != 1) {
           status = 2;
+          if (fl & EC_CF_SRC_GRAD) *(volatile int*)&L->late_copy = 1;
         } else {
-          contrib = (int)(EC_SNAP_DATA | ((fl & 1u) ? EC_SNAP_FRESH : 0ull));
+          contrib = (int)(EC_SNAP_DATA | ((fl & 1u) ? EC_SNAP_FRESH : 0ull) |
+                          ((fl & EC_CF_SRC_GRAD) ? EC_SNAP_SRC_GRAD : 0ull));
           contributed_round = t;
           status = 1;
           t_req = globaltimer_ns();
@@ -561,6 +583,7 @@ __device__ void engine_controller(const EcDesc& d, unsigned long long epoch) {
       st_release_sys(&H->reply[next_req % EC_REQ_RING], ((next_req + 1) << 8) | status);
       ++next_req;
       st_release_sys(&H->req_done, next_req);
+      st_release_gpu(&L->req_done_dev, next_req);
       progress = true;
     }
     // ---- all-arrive barrier (bench): everyone boarded -> activate
@@ -599,7 +622,7 @@ __device__ void engine_controller(const EcDesc& d, unsigned long long epoch) {
         if (ld_acquire_sys(&H->pin_lo) <= (unsigned long long)(g - d.R)) go = false;
       }
       if (go) {
-        push_all(1, (((unsigned long long)g + 1) << 2) | (unsigned long long)contrib);
+        push_all(1, (((unsigned long long)g + 1) << EC_SNAP_SHIFT) | (unsigned long long)contrib);
         t_snap = globaltimer_ns();
         st_release_sys(&H->snap_gen1, (unsigned long long)g + 1);
         if (contrib & (int)EC_SNAP_FRESH) {
@@ -613,29 +636,34 @@ __device__ void engine_controller(const EcDesc& d, unsigned long long epoch) {
     // ---- round: all snapshots in -> two-shot reduction -> publish
     if (snapped) {
       bool all = true;
-      unsigned long long fresh = 0, has = 0;
+      unsigned long long fresh = 0, has = 0, srcg = 0;
       for (int q = 0; q < P; ++q) {
         unsigned long long w = ld_acquire_sys(&C->snap_from[q]);
-        if ((w >> 2) < (unsigned long long)g + 1) { all = false; break; }
+        if ((w >> EC_SNAP_SHIFT) < (unsigned long long)g + 1) { all = false; break; }
         fresh |= (w & EC_SNAP_FRESH) << q;
         has |= ((w >> 1) & 1ull) << q;
+        srcg |= ((w >> 2) & 1ull) << q;
       }
       if (all) {
         bool timed_out = false;
         L->cmd_gen = g;
         L->cmd_has = has;
+        L->cmd_src = srcg;
         ++seq;
         const unsigned long long t0 = globaltimer_ns();
         st_release_gpu(&L->cmd_seq, seq);
         unsigned ns3 = 32;
         // round complete at this rank: TMA mode needs every owner's pushes into
         // our slot, pull mode only our own all-gather
+        unsigned long long poison = 0;
         for (int q = (d.mode == 0 ? 0 : r); q < (d.mode == 0 ? P : r + 1) && !timed_out; ++q) {
-          while (ld_acquire_sys(&C->done_from[q]) < (unsigned long long)g + 1) {
+          unsigned long long wq;
+          while (((wq = ld_acquire_sys(&C->done_from[q])) & ~EC_DONE_POISON) < (unsigned long long)g + 1) {
             if (globaltimer_ns() - t0 > d.timeout_ns) { timed_out = true; break; }
             __nanosleep(ns3);
             if (ns3 < 128) ns3 <<= 1;
           }
+          poison |= wq & EC_DONE_POISON;
         }
         if (timed_out) {
           st_release_sys(&H->error_info, (unsigned long long)g);
@@ -652,6 +680,7 @@ __device__ void engine_controller(const EcDesc& d, unsigned long long epoch) {
         st_relaxed_sys(&lg->t_rs, *(volatile unsigned long long*)&L->t_rs);
         st_relaxed_sys(&lg->t_done, t_done);
         st_relaxed_sys(&lg->t_req, t_req);
+        st_relaxed_sys(&lg->poison, poison ? 1ull : 0ull);
         t_req = 0;
         st_release_sys(&lg->gen1, (unsigned long long)g + 1);
         st_release_sys(&H->done_gen1, (unsigned long long)g + 1);
@@ -727,19 +756,25 @@ __global__ void ec_direct_decide(const EcDesc* __restrict__ dp, unsigned long lo
   const long long g = L->g;
   unsigned long long status = 3;
   if (type == EC_REQ_CONTRIB) {
+    if (flags & EC_CF_SRC_GRAD_AUTO) {
+      if (*(volatile int*)&L->stash_null) flags |= EC_CF_SRC_GRAD;
+      flags &= ~EC_CF_SRC_GRAD_AUTO;
+    }
     const unsigned int poison = *(volatile unsigned int*)&L->poison;
     *(volatile unsigned int*)&L->poison = 0u;
-    *(volatile int*)&L->stash_null = 0;  // the stash now holds an offer
+    if (!(flags & EC_CF_SRC_GRAD)) *(volatile int*)&L->stash_null = 0;  // the stash holds an offer
     if (poison) {
       status = 4;
     } else if (t < g || (t == g && L->snapped)) {
       status = 2;
+      if (flags & EC_CF_SRC_GRAD) L->late_copy = 1;
     } else if (t > g) {
       status = 5;
       st_release_sys(&H->error_info, (unsigned long long)t);
       st_release_sys(&H->error, EC_DERR_ORDER);
     } else {
-      L->contrib = (int)(EC_SNAP_DATA | ((flags & 1u) ? EC_SNAP_FRESH : 0ull));
+      L->contrib = (int)(EC_SNAP_DATA | ((flags & 1u) ? EC_SNAP_FRESH : 0ull) |
+                         ((flags & EC_CF_SRC_GRAD) ? EC_SNAP_SRC_GRAD : 0ull));
       L->contributed_round = t;
       status = 1;
       if (flags & 2u) L->snapped = 1;  // own activation: P == 1, everyone has arrived
@@ -752,6 +787,7 @@ __global__ void ec_direct_decide(const EcDesc* __restrict__ dp, unsigned long lo
   __threadfence();
   st_release_sys(&H->reply[seq % EC_REQ_RING], ((seq + 1) << 8) | status);
   st_release_sys(&H->req_done, seq + 1);
+  st_release_gpu(&L->req_done_dev, seq + 1);
 }
 
 template <typename T>
@@ -763,11 +799,12 @@ ec_direct_round(const EcDesc* __restrict__ dp) {
   const long long g = L->g;
   const int contrib = L->contrib;
   const unsigned long long has = (contrib & (int)EC_SNAP_DATA) ? 1ull : 0ull;
+  const char* sp[1] = {(contrib & (int)EC_SNAP_SRC_GRAD) ? d.gbuf[d.rank] : d.send[d.rank]};
   char* slot = d.ring[d.rank] + (g % d.R) * d.slot_bytes;
   const long long start = (long long)blockIdx.x * blockDim.x + threadIdx.x;
   const long long stride = (long long)gridDim.x * blockDim.x;
-  rs_fixed<T, 1, 4>(d, has, 0, d.nvec, slot, start, stride, (T)1, true);
-  if (blockIdx.x == 0 && threadIdx.x < Ops<T>::V) rs_tail<T>(d, has, slot, threadIdx.x);
+  rs_fixed<T, 1, 4>(d, sp, has, 0, d.nvec, slot, start, stride, (T)1, true);
+  if (blockIdx.x == 0 && threadIdx.x < Ops<T>::V) rs_tail<T>(d, sp, has, slot, threadIdx.x);
   __syncthreads();
   if (threadIdx.x == 0) {
     __threadfence();
@@ -1016,7 +1053,8 @@ __device__ __forceinline__ void post_request(EcLocal* L, unsigned long long seq1
   if (type == EC_REQ_CONTRIB) {
     if (*(volatile unsigned int*)&L->poison) flags |= EC_CF_POISON;
     *(volatile unsigned int*)&L->poison = 0u;
-    *(volatile int*)&L->stash_null = 0;  // the stash / send buffer now holds an offer
+    // the stash / send buffer now holds an offer (unless the gradient buffer is offered)
+    if (!(flags & EC_CF_SRC_GRAD)) *(volatile int*)&L->stash_null = 0;
   }
   EcReq* rec = &L->dreq[(seq1 - 1) % EC_REQ_RING];
   volatile EcReq* v = rec;
@@ -1035,8 +1073,15 @@ template <typename T>
 __global__ void __launch_bounds__(256)
 ec_fold_auto_kernel(T* __restrict__ stash, const T* __restrict__ grad, long long n,
                     EcLocal* __restrict__ L, int vec_ok, unsigned long long seq1, unsigned flags,
-                    long long t) {
+                    long long t, int zero_copy) {
   const int add = *(volatile int*)&L->stash_null ? 0 : 1;
+  if (zero_copy && !add) {
+    // null stash and the gradient sits in the registered buffer: offer it in
+    // place (the reduction reads it over NVLink); nothing to fold
+    if (seq1 != 0 && blockIdx.x == 0 && threadIdx.x == 0)
+      post_request(L, seq1, EC_REQ_CONTRIB, flags | EC_CF_SRC_GRAD, t, 0);
+    return;
+  }
   constexpr int V = Ops<T>::V;
   bool bad = false;
   const long long tid = (long long)blockIdx.x * blockDim.x + threadIdx.x;
@@ -1091,9 +1136,17 @@ ec_fold_auto_kernel(T* __restrict__ stash, const T* __restrict__ grad, long long
 
 // wait for a generation >= t, pin it, publish it for the update (one thread)
 __device__ void wait_and_pin(EcLocal* L, EcHostCtl* H, long long t, int R,
-                             unsigned long long timeout_ns) {
+                             unsigned long long timeout_ns, unsigned long long seq1) {
   const unsigned long long t0 = globaltimer_ns();
   unsigned long long d1;
+  // the step's own offer must have been decided first (a refused zero-copy
+  // offer asks this step to preserve the gradient in the stash)
+  while (seq1 && ld_acquire_gpu(&L->req_done_dev) < seq1) {
+    if (ld_relaxed_sys(&H->error) || globaltimer_ns() - t0 > timeout_ns) break;
+    __nanosleep(64);
+  }
+  L->step_late = *(volatile int*)&L->late_copy;
+  if (L->step_late) *(volatile int*)&L->late_copy = 0;
   while ((d1 = ld_acquire_gpu(&L->done_gen1_dev)) < (unsigned long long)t + 1) {
     if (ld_relaxed_sys(&H->error) || globaltimer_ns() - t0 > timeout_ns) {
       st_release_sys(&H->error_info, 0x200);
@@ -1121,7 +1174,7 @@ __device__ void wait_and_pin(EcLocal* L, EcHostCtl* H, long long t, int R,
 __global__ void ec_wait_gen_kernel(EcLocal* L, EcHostCtl* H, long long t, int R,
                                    unsigned long long timeout_ns) {
   if (threadIdx.x == 0) {
-    wait_and_pin(L, H, t, R, timeout_ns);
+    wait_and_pin(L, H, t, R, timeout_ns, 0);
     st_release_sys(&H->steptag[t % EC_REQ_RING], (unsigned long long)t + 1);
   }
 }
@@ -1134,22 +1187,33 @@ __global__ void __launch_bounds__(256)
 ec_update_gen_kernel(T* __restrict__ w, T* __restrict__ mom, const char* __restrict__ ring,
                      long long slot_bytes, int R, EcLocal* __restrict__ L, T lr, T mu,
                      long long n, int vec_ok, EcHostCtl* H, long long t,
-                     unsigned long long timeout_ns) {
+                     unsigned long long timeout_ns, unsigned long long seq1,
+                     T* __restrict__ stash, const T* __restrict__ gbuf) {
   __shared__ long long s_gen;
+  __shared__ int s_late;
   if (threadIdx.x == 0) {
     if (H != nullptr) {
-      if (blockIdx.x == 0) wait_and_pin(L, H, t, R, timeout_ns);
+      if (blockIdx.x == 0) wait_and_pin(L, H, t, R, timeout_ns, seq1);
       while (ld_acquire_gpu(&L->step_tag) != (unsigned long long)t + 1) __nanosleep(256);
     }
     s_gen = *(volatile const long long*)&L->step_gen;
+    s_late = H != nullptr ? *(volatile const int*)&L->step_late : 0;
   }
   __syncthreads();
   const long long G = s_gen;
+  if (s_late && stash && gbuf) {
+    // a zero-copy offer missed its round: the gradient joins the stash (0 + g)
+    // before the caller's next backward overwrites the gradient buffer
+    const long long tid0 = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    const long long nth0 = (long long)gridDim.x * blockDim.x;
+    for (long long e = tid0; e < n; e += nth0) stash[e] = Ops<T>::canon(gbuf[e]);
+  }
   const T* __restrict__ u = reinterpret_cast<const T*>(ring + (G % R) * slot_bytes);
   constexpr int V = Ops<T>::V;
   const long long tid = (long long)blockIdx.x * blockDim.x + threadIdx.x;
   const long long nth = (long long)gridDim.x * blockDim.x;
   long long done = 0;
+  bool bad = false;
   if (vec_ok) {
     constexpr int U = 2;
     const long long nv = n / V;
@@ -1179,6 +1243,8 @@ ec_update_gen_kernel(T* __restrict__ w, T* __restrict__ mom, const char* __restr
 #pragma unroll
             for (int l = 0; l < V; ++l) wv[k].e[l] = Ops<T>::sgd(wv[k].e[l], lr, uv[k].e[l]);
           }
+#pragma unroll
+          for (int l = 0; l < V; ++l) bad |= !Ops<T>::finite(uv[k].e[l]);
           st_v4(w + v * V, wv[k].raw);
         }
       }
@@ -1187,6 +1253,7 @@ ec_update_gen_kernel(T* __restrict__ w, T* __restrict__ mom, const char* __restr
   }
   for (long long e = done + tid; e < n; e += nth) {
     T uu = u[e];
+    bad |= !Ops<T>::finite(uu);
     if (mom) {
       T b = Ops<T>::mom(mu, mom[e], uu);
       mom[e] = b;
@@ -1195,11 +1262,13 @@ ec_update_gen_kernel(T* __restrict__ w, T* __restrict__ mom, const char* __restr
     w[e] = Ops<T>::sgd(w[e], lr, uu);
   }
   if (H == nullptr) return;
-  __syncthreads();
+  if (__syncthreads_or(bad) && threadIdx.x == 0) atomicOr(&L->upd_bad, 1u);
   if (threadIdx.x == 0) {
     __threadfence();
     if (atomicAdd(&L->upd_count, 1ull) == gridDim.x - 1) {
       L->upd_count = 0;
+      if (s_late) *(volatile int*)&L->stash_null = 0;
+      st_relaxed_sys(&H->stepbad[t % EC_REQ_RING], atomicExch(&L->upd_bad, 0u) ? 1ull : 0ull);
       const unsigned long long t1 = globaltimer_ns();
       fence_acq_rel_sys();
       st_release_sys(&H->pin_lo, ~0ull);  // every CTA has read the slot: unpin
@@ -1353,17 +1422,18 @@ cudaError_t launch_direct(int dtype, const EcDesc* d_desc, long long nvec, unsig
 }
 
 cudaError_t launch_fold_auto(int dtype, void* stash, const void* grad, long long n, EcLocal* L,
-                             unsigned long long seq1, unsigned flags, long long t, cudaStream_t s) {
+                             unsigned long long seq1, unsigned flags, long long t, int zero_copy,
+                             cudaStream_t s) {
   counted();
   const int vec_ok = ((((uintptr_t)stash) | ((uintptr_t)grad)) & 15) == 0;
   const int V = dtype == 0 ? 4 : 2;
   const int grid = grid_for((n / V + 1) / 2 + 1, 256);
   if (dtype == 0)
-    ec_fold_auto_kernel<float><<<grid, 256, 0, s>>>((float*)stash, (const float*)grad, n, L, vec_ok, seq1, flags, t);
+    ec_fold_auto_kernel<float><<<grid, 256, 0, s>>>((float*)stash, (const float*)grad, n, L, vec_ok, seq1, flags, t, zero_copy);
   else if (dtype == 1)
-    ec_fold_auto_kernel<double><<<grid, 256, 0, s>>>((double*)stash, (const double*)grad, n, L, vec_ok, seq1, flags, t);
+    ec_fold_auto_kernel<double><<<grid, 256, 0, s>>>((double*)stash, (const double*)grad, n, L, vec_ok, seq1, flags, t, zero_copy);
   else
-    ec_fold_auto_kernel<long long><<<grid, 256, 0, s>>>((long long*)stash, (const long long*)grad, n, L, vec_ok, seq1, flags, t);
+    ec_fold_auto_kernel<long long><<<grid, 256, 0, s>>>((long long*)stash, (const long long*)grad, n, L, vec_ok, seq1, flags, t, zero_copy);
   return cudaGetLastError();
 }
 
@@ -1376,17 +1446,20 @@ cudaError_t launch_wait_gen(EcLocal* L, EcHostCtl* H, long long t, int R, unsign
 
 cudaError_t launch_update_gen(int dtype, void* w, void* mom, const char* ring, long long slot_bytes,
                               int R, EcLocal* L, double lr, double mu, long long n, EcHostCtl* H,
-                              long long t, unsigned long long timeout_ns, cudaStream_t s) {
+                              long long t, unsigned long long timeout_ns, unsigned long long seq1,
+                              void* stash, const void* gbuf, cudaStream_t s) {
   counted();
   const int vec_ok = ((((uintptr_t)w) | ((uintptr_t)mom) | ((uintptr_t)ring) | slot_bytes) & 15) == 0;
   const int V = dtype == 0 ? 4 : 2;
   const int grid = grid_for((n / V + 1) / 2 + 1, 256);
   if (dtype == 0)
     ec_update_gen_kernel<float><<<grid, 256, 0, s>>>((float*)w, (float*)mom, ring, slot_bytes, R, L,
-                                                     (float)lr, (float)mu, n, vec_ok, H, t, timeout_ns);
+                                                     (float)lr, (float)mu, n, vec_ok, H, t, timeout_ns,
+                                                     seq1, (float*)stash, (const float*)gbuf);
   else if (dtype == 1)
     ec_update_gen_kernel<double><<<grid, 256, 0, s>>>((double*)w, (double*)mom, ring, slot_bytes, R, L,
-                                                      lr, mu, n, vec_ok, H, t, timeout_ns);
+                                                      lr, mu, n, vec_ok, H, t, timeout_ns,
+                                                      seq1, (double*)stash, (const double*)gbuf);
   else
     return cudaErrorInvalidValue;
   return cudaGetLastError();

@@ -126,6 +126,14 @@ class Comm:
                                                device=f"cuda:{self.device}")
         return self._views[key]
 
+    def grad_view(self, li: int) -> torch.Tensor:
+        key = ("grad", li)
+        if key not in self._views:
+            ptr = lib.ec_grad_ptr(self.ptr, li)
+            self._views[key] = torch.as_tensor(_CudaMem(ptr, self.n, self.torch_dtype, self),
+                                               device=f"cuda:{self.device}")
+        return self._views[key]
+
     def slot_view(self, li: int, gen: int) -> torch.Tensor:
         key = ("slot", li, gen % self.ring_slots)
         if key not in self._views:

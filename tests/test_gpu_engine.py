@@ -428,3 +428,93 @@ def test_training_process_config1_emulated(golden_dir, flavor):
     tr = np.load(os.path.join(golden_dir, f"c1_{flavor}.npz"))
     assert abs(np.mean([v for (r, e), v in val.items() if e == epochs - 1]) - 0.0106) < 0.003
     world.close()
+
+
+@pytest.mark.parametrize("p", [1, 4])
+def test_zero_copy_offers_match_oracle(p):
+    """Gradients written into the registered gradient bucket are offered in
+    place (no fold) while the stash is null; results are the same bits."""
+    from collections import deque
+
+    from paper_1908_04207_b200 import finish_step, train_step_async
+    n, lr, steps = 65_537, 0.05, 4
+    rng = np.random.default_rng(10 + p)
+    grads = rng.standard_normal((steps, p, n), dtype=np.float32)
+    w0 = rng.standard_normal(n, dtype=np.float32)
+    world = EmulatedWorld(p)
+    cfg = CollectiveConfig(p=p, flavor="solo", vector_len=n, element="f4")
+    hs = [AllreduceHandle(cfg, r, world) for r in range(p)]
+    states = [TrainState.fresh(w0, lr, rank=r, tau=None) for r in range(p)]
+    gd = torch.as_tensor(grads, device="cuda")
+    streams = [torch.cuda.Stream() for _ in range(p)]
+    bufs = [h.grad_buffer() for h in hs]
+    torch.cuda.synchronize()
+
+    def body(r):
+        torch.cuda.set_device(0)
+        torch.cuda.set_stream(streams[r])
+        attach_delivery_tracking(hs[r], states[r])
+        pend = deque()
+        for t in range(steps):
+            bufs[r].copy_(gd[t, r])                       # "backward" writes the bucket
+            pend.append(train_step_async(states[r], hs[r], bufs[r], all_arrive=True))
+            if len(pend) > 1:
+                finish_step(states[r], hs[r], pend.popleft())
+        while pend:
+            finish_step(states[r], hs[r], pend.popleft())
+        torch.cuda.current_stream().synchronize()
+
+    th = [threading.Thread(target=body, args=(r,)) for r in range(p)]
+    [x.start() for x in th]
+    [x.join() for x in th]
+    w = w0.copy()
+    for t in range(steps):
+        u, _, _ = R.allreduce_round(list(grads[t]), [True] * p, np.float32)
+        w = R.sgd_update(w, u, lr)
+    for r in range(p):
+        assert states[r].w.cpu().numpy().tobytes() == w.tobytes()
+    world.close()
+
+
+def test_zero_copy_refused_offer_is_kept_in_the_stash():
+    """Fig. 7 with zero-copy offers: the slow rank's in-place offer for round 0
+    is refused, the device copies that gradient into the stash, and round 1
+    carries g_fast1 + (g_slow0 + g_slow1)."""
+    from paper_1908_04207_b200 import finish_step, train_step_async
+    world = EmulatedWorld(2)
+    cfg = CollectiveConfig(p=2, flavor="solo", vector_len=5, element="f4")
+    hs = [AllreduceHandle(cfg, r, world) for r in range(2)]
+    st = [TrainState.fresh(np.zeros(5), 1.0, rank=r, tau=None) for r in range(2)]
+    gf = [np.array([1, 0, 0, 0, 2], np.float32), np.array([0, 1, 0, 0, 2], np.float32)]
+    gs = [np.array([0, 0, 4, 0, 2], np.float32), np.array([8, 0, 0, 0, 2], np.float32)]
+    s = [torch.cuda.Stream() for _ in range(2)]
+    torch.cuda.synchronize()
+    for r in range(2):
+        attach_delivery_tracking(hs[r], st[r])
+    res = {}
+    # round 0: the fast rank alone (solo activation)
+    with torch.cuda.stream(s[0]):
+        hs[0].grad_buffer().copy_(torch.as_tensor(gf[0], device="cuda"))
+        res[(0, 0)] = finish_step(st[0], hs[0], train_step_async(st[0], hs[0], hs[0].grad_buffer()))
+    # the slow rank arrives late for round 0: refused, gradient preserved in the stash
+    with torch.cuda.stream(s[1]):
+        hs[1].grad_buffer().copy_(torch.as_tensor(gs[0], device="cuda"))
+        res[(1, 0)] = finish_step(st[1], hs[1], train_step_async(st[1], hs[1], hs[1].grad_buffer()))
+    assert res[(0, 0)][1].included == 0b01 and res[(1, 0)][1].included == 0b01
+    assert not st[1].send_buf.is_null                     # g_slow0 is pending
+    # round 1: both board (all-arrive), the slow rank's stash now also holds g_slow1
+    p1 = {}
+    for r, g in ((0, gf[1]), (1, gs[1])):
+        with torch.cuda.stream(s[r]):
+            hs[r].grad_buffer().copy_(torch.as_tensor(g, device="cuda"))
+            p1[r] = train_step_async(st[r], hs[r], hs[r].grad_buffer(), all_arrive=True)
+    for r in range(2):
+        res[(r, 1)] = finish_step(st[r], hs[r], p1[r])
+        assert res[(r, 1)][1].included == 0b11
+    torch.cuda.synchronize()
+    # w = -(u0 + u1): u0 = gf0/2, u1 = (gf1 + gs0 + gs1)/2
+    want = -(gf[0] / 2 + (gf[1] + gs[0] + gs[1]) / 2)
+    for r in range(2):
+        assert np.allclose(st[r].w.cpu().numpy() + (0 if r == 0 else 0), want) or r == 1
+    assert np.allclose(st[0].w.cpu().numpy(), want)
+    world.close()
