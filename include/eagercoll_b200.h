@@ -124,6 +124,10 @@ int ec_wait(ec_comm_t* c, int local_idx, int64_t t, int timeout_ms, int pin,
  * + ec_reply + ec_wait(t, unpinned).  *status is the offer's reply. */
 int ec_round(ec_comm_t* c, int local_idx, int64_t t, uint32_t flags, void* stream,
              int timeout_ms, int* status, int64_t* gen, uint64_t* mask, int* nap);
+/* A round offered in stream order with a stream-ordered wait for its completion
+ * behind it: back-to-back rounds with no host round trip (bandwidth sweeps). */
+int ec_round_async(ec_comm_t* c, int local_idx, int64_t t, uint32_t flags, void* stream,
+                   uint64_t* seq);
 /* One eager-SGD step of the hot path in one call (eagersgd.py:129-167):
  * fold grad into the stash (fold_mode, skipped if grad is NULL), offer it
  * (flags), wait for the latest generation >= t (pinned), w = w - lr*u (or the

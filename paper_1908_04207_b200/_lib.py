@@ -63,6 +63,7 @@ _SIGS = {
     "ec_profile_enable": (_i32, [_i32]),
     "ec_step_update_ns": (_i32, [_vp, _i32, _P(_u64)]),
     "ec_profile_read": (_i32, [_P(C.c_double), _P(_i64)]),
+    "ec_round_async": (_i32, [_vp, _i32, _i64, _u32, _vp, _P(_u64)]),
     "ec_round": (_i32, [_vp, _i32, _i64, _u32, _vp, _i32, _P(_i32), _P(_i64), _P(_u64), _P(_i32)]),
     "ec_step": (_i32, [_vp, _i32, _i64, _vp, _i32, _u32, _vp, _vp, C.c_double, C.c_double, _vp,
                        _i32, _P(_i32), _P(_i64), _P(_u64), _P(_i32)]),

@@ -34,6 +34,8 @@ cudaError_t launch_fold_auto(int dtype, void* stash, const void* grad, long long
                              cudaStream_t s);
 cudaError_t launch_wait_gen(EcLocal* L, EcHostCtl* H, long long t, int R, unsigned long long timeout_ns,
                             cudaStream_t s);
+cudaError_t launch_wait_done(EcLocal* L, EcHostCtl* H, long long t, unsigned long long timeout_ns,
+                             cudaStream_t s);
 cudaError_t launch_update_gen(int dtype, void* w, void* mom, const char* ring, long long slot_bytes,
                               int R, EcLocal* L, double lr, double mu, long long n, EcHostCtl* H,
                               long long t, unsigned long long timeout_ns, unsigned long long seq1,
@@ -757,6 +759,14 @@ int ec_round(ec_comm_t* c, int li, int64_t t, uint32_t flags, void* stream, int 
   if (status) *status = st;
   if (st == EC_R_POISONED || st == EC_R_ERROR) return EC_OK;
   return ec_wait(c, li, t, timeout_ms, 0, gen, mask, nap);
+}
+
+int ec_round_async(ec_comm_t* c, int li, int64_t t, uint32_t flags, void* stream, uint64_t* seq) {
+  int rc = ec_post_contribute(c, li, t, flags, stream, seq);
+  if (rc) return rc;
+  EcRankHost* r = c->L[li];
+  CK(launch_wait_done(r->local, r->hd, t, c->timeout_ns, (cudaStream_t)stream));
+  return EC_OK;
 }
 
 int ec_step(ec_comm_t* c, int li, int64_t t, const void* grad, int fold_mode, uint32_t flags,

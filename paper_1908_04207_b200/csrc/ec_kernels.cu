@@ -1171,6 +1171,21 @@ __device__ void wait_and_pin(EcLocal* L, EcHostCtl* H, long long t, int R,
   st_release_gpu(&L->step_tag, (unsigned long long)t + 1);
 }
 
+// stream-ordered wait for round t to complete at this rank (no pin): lets a
+// host enqueue back-to-back rounds the way nccl-tests enqueues collectives
+__global__ void ec_wait_done_kernel(EcLocal* L, EcHostCtl* H, long long t,
+                                    unsigned long long timeout_ns) {
+  if (threadIdx.x != 0) return;
+  const unsigned long long t0 = globaltimer_ns();
+  while (ld_acquire_gpu(&L->done_gen1_dev) < (unsigned long long)t + 1) {
+    if (ld_relaxed_sys(&H->error) || globaltimer_ns() - t0 > timeout_ns) {
+      st_release_sys(&H->error_info, 0x300);
+      st_release_sys(&H->error, EC_DERR_TIMEOUT);
+      break;
+    }
+  }
+}
+
 __global__ void ec_wait_gen_kernel(EcLocal* L, EcHostCtl* H, long long t, int R,
                                    unsigned long long timeout_ns) {
   if (threadIdx.x == 0) {
@@ -1317,6 +1332,7 @@ cudaError_t preload_kernels() {
       (const void*)ec_post_kernel, (const void*)ec_write_u64_kernel, (const void*)ec_spin_kernel,
       (const void*)ec_fold_auto_kernel<float>, (const void*)ec_fold_auto_kernel<double>,
       (const void*)ec_fold_auto_kernel<long long>, (const void*)ec_wait_gen_kernel,
+      (const void*)ec_wait_done_kernel,
       (const void*)ec_update_gen_kernel<float>, (const void*)ec_update_gen_kernel<double>,
   };
   for (const void* f : fns) {
@@ -1434,6 +1450,13 @@ cudaError_t launch_fold_auto(int dtype, void* stash, const void* grad, long long
     ec_fold_auto_kernel<double><<<grid, 256, 0, s>>>((double*)stash, (const double*)grad, n, L, vec_ok, seq1, flags, t, zero_copy);
   else
     ec_fold_auto_kernel<long long><<<grid, 256, 0, s>>>((long long*)stash, (const long long*)grad, n, L, vec_ok, seq1, flags, t, zero_copy);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_wait_done(EcLocal* L, EcHostCtl* H, long long t, unsigned long long timeout_ns,
+                             cudaStream_t s) {
+  counted();
+  ec_wait_done_kernel<<<1, 32, 0, s>>>(L, H, t, timeout_ns);
   return cudaGetLastError();
 }
 

@@ -63,6 +63,32 @@ def _round(h, t, all_arrive=True):
     return gen.value
 
 
+def rounds_back_to_back(h, t0, k, all_arrive=True):
+    """k rounds t0..t0+k-1 enqueued on the current stream, each behind a
+    device-side wait for the previous one (ec_round_async); returns device ms
+    between the first offer and the last completion (CUDA events)."""
+    import torch
+
+    from . import _lib
+    from ._lib import call
+    h._ensure_started()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    seqs = []
+    e0.record()
+    for t in range(t0, t0 + k):
+        flags = _lib.EC_CF_FRESH | (_lib.EC_CF_ALL_ARRIVE if all_arrive else 0) | \
+            (_lib.EC_CF_ACTIVATE if h._may_activate(t) else 0)
+        seq = C.c_uint64()
+        call("ec_round_async", h.comm.ptr, h.li, t, flags, h._stream(), C.byref(seq))
+        seqs.append(seq.value)
+    e1.record()
+    e1.synchronize()
+    for s in seqs:
+        h._reply(s)
+    h._wait(t0 + k - 1, 60.0, pin=False)
+    return e0.elapsed_time(e1)
+
+
 def allreduce_sweep(world, rank, p, sizes_bytes, flavor="solo", rounds_cap=50, workers=None,
                     max_over_ranks=lambda x: x, barrier=lambda: None):
     """Bus bandwidth of the partial allreduce per payload size (fp32)."""
@@ -87,6 +113,9 @@ def allreduce_sweep(world, rank, p, sizes_bytes, flavor="solo", rounds_cap=50, w
         for t in range(3, 3 + rounds):
             _round(h, t)
         dt = time.perf_counter() - t0
+        barrier()
+        b2b_ms = rounds_back_to_back(h, 3 + rounds, rounds)
+        b2b_us = max_over_ranks(b2b_ms * 1e3 / rounds)
         phases = [_gen_times(h, g) for g in range(2, 3 + rounds)]
         prev, phases = phases[0], phases[1:]
         data_us = sum((x[3] - x[1]) for x in phases) / rounds / 1e3
@@ -99,6 +128,8 @@ def allreduce_sweep(world, rank, p, sizes_bytes, flavor="solo", rounds_cap=50, w
         bus = 2 * (p - 1) / p * 4 * n if p > 1 else 0
         out.append({"bytes": 4 * n, "rounds": rounds, "us_per_round": round_us,
                     "busbw_gbs": bus / (round_us * 1e-6) / 1e9,
+                    "us_per_round_b2b": b2b_us,
+                    "busbw_b2b_gbs": bus / (b2b_us * 1e-6) / 1e9,
                     "device_data_us": data_us, "device_rs_us": max_over_ranks(rs_us),
                     "busbw_device_gbs": bus / (data_us * 1e-6) / 1e9 if data_us > 0 else None,
                     "snap_to_start_us": max_over_ranks(snap_wait_us),

@@ -394,7 +394,7 @@ def test_training_process_config1_emulated(golden_dir, flavor):
     the final resync -- and that it converges to the reference's val MSE."""
     from paper_1908_04207_b200 import DelayModel, inject_delay, training_process
     from paper_1908_04207_b200.models import gen_dataset, init_weights
-    p, epochs, spe = 4, 16, 4
+    p, epochs, spe = 4, 48, 4
     world = EmulatedWorld(p)
     ds = gen_dataset(64, 4096, seed=99)
     w0 = init_weights(64, seed=1234)
@@ -426,7 +426,8 @@ def test_training_process_config1_emulated(golden_dir, flavor):
     assert all(w.tobytes() == ws[0].tobytes() for w in ws)
     assert not ledger.audit(tau=8, allow_pending_after=epochs * spe - 9)
     tr = np.load(os.path.join(golden_dir, f"c1_{flavor}.npz"))
-    assert abs(np.mean([v for (r, e), v in val.items() if e == epochs - 1]) - 0.0106) < 0.003
+    final = np.mean([v for (r, e), v in val.items() if e == epochs - 1])
+    assert abs(final - float(tr["final_val"])) < 0.002      # reference: 0.0105-0.0106
     world.close()
 
 
