@@ -852,6 +852,12 @@ int ec_step_result(ec_comm_t* c, int li, uint64_t seq, int64_t t, int timeout_ms
   }
   const int64_t G = (int64_t)aload(&r->h->stepgen[t % EC_REQ_RING]) - 1;
   if (gen) *gen = G;
+  // the device mirror of done runs ahead of the host-visible log: wait for it
+  while ((int64_t)aload(&r->h->done_gen1) <= G) {
+    if ((rc = device_error(r))) return rc;
+    if (bo.expired(timeout_ms)) return fail(EC_E_TIMEOUT, "rank %d log of generation %lld", r->rank, (long long)G);
+    bo.pause();
+  }
   r->last_update_ns = aload(&r->h->stepns[t % EC_REQ_RING]);
   if (status && aload(&r->h->stepbad[t % EC_REQ_RING])) *status = EC_R_POISONED;
   if (mask || nap) {

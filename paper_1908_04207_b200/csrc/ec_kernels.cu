@@ -462,7 +462,7 @@ __device__ void engine_worker(const EcDesc& d, int w, unsigned long long epoch) 
         if (atomicExch(&L->round_poison, 0u)) word |= EC_DONE_POISON;
         if (d.mode == 0) {
           L->t_rs = globaltimer_ns();
-          for (int q = 0; q < d.P; ++q) st_release_sys(&d.ctrl[q]->done_from[d.rank], word);
+          for (int q = 0; q < d.P; ++q) st_relaxed_sys(&d.ctrl[q]->done_from[d.rank], word);
         } else {
           st_release_sys(&d.ctrl[d.rank]->done_from[d.rank], word);
         }
@@ -497,13 +497,16 @@ __device__ void engine_controller(const EcDesc& d, unsigned long long epoch) {
   unsigned ns = 32;
 
   // write this rank's word into every rank's control block (peer stores over NVLink)
+  // (one sys-scope fence, then relaxed stores: a fence-based release; every
+  // sys fence on this serial path costs a PCIe/NVLink drain)
   auto push_all = [&](int which, unsigned long long v) {
+    fence_acq_rel_sys();
     for (int q = 0; q < P; ++q) {
       unsigned long long* base;
       if (which == 0) base = &d.ctrl[q]->act_from[r];
       else if (which == 1) base = &d.ctrl[q]->snap_from[r];
       else base = &d.ctrl[q]->arrive_from[r];
-      st_release_sys(base, v);
+      st_relaxed_sys(base, v);
     }
   };
   auto activate = [&]() {
@@ -515,14 +518,15 @@ __device__ void engine_controller(const EcDesc& d, unsigned long long epoch) {
     return (int)((d.forced[gen] >> r) & 1ull);
   };
 
-  unsigned iter = 0;
+  unsigned long long last_host_poll = 0;
   while (true) {
     bool progress = false;
-    // Host-mapped words cost a PCIe round trip: poll them when the device
-    // doorbell (bumped by every stream-posted request) says so, and otherwise
-    // only every 16th pass (host-posted requests, stop).
-    ++iter;
-    const bool poll_host = (iter & 15u) == 0 || ld_acquire_gpu(&L->posted) > next_req;
+    // Host-mapped words cost a PCIe round trip: read them only every ~8 us
+    // (host-posted requests, stop); stream-posted requests arrive through the
+    // device ring and doorbell.
+    const unsigned long long now = globaltimer_ns();
+    const bool poll_host = now - last_host_poll > 8000ull;
+    if (poll_host) last_host_poll = now;
     if (poll_host && !stopping && ld_relaxed_sys(&H->stop)) {
       stopping = true;
       stop_t0 = globaltimer_ns();
@@ -580,9 +584,9 @@ __device__ void engine_controller(const EcDesc& d, unsigned long long epoch) {
       } else if (type == EC_REQ_HOLD) {
         hold_from = arg;
       }
-      st_release_sys(&H->reply[next_req % EC_REQ_RING], ((next_req + 1) << 8) | status);
+      st_relaxed_sys(&H->reply[next_req % EC_REQ_RING], ((next_req + 1) << 8) | status);
       ++next_req;
-      st_release_sys(&H->req_done, next_req);
+      st_relaxed_sys(&H->req_done, next_req);
       st_release_gpu(&L->req_done_dev, next_req);
       progress = true;
     }
@@ -624,7 +628,7 @@ __device__ void engine_controller(const EcDesc& d, unsigned long long epoch) {
       if (go) {
         push_all(1, (((unsigned long long)g + 1) << EC_SNAP_SHIFT) | (unsigned long long)contrib);
         t_snap = globaltimer_ns();
-        st_release_sys(&H->snap_gen1, (unsigned long long)g + 1);
+        st_relaxed_sys(&H->snap_gen1, (unsigned long long)g + 1);
         if (contrib & (int)EC_SNAP_FRESH) {
           hold_from = EC_INF_GEN;  // stash delivered (eagersgd.py:117-124)
           *(volatile int*)&L->stash_null = 1;
@@ -682,9 +686,10 @@ __device__ void engine_controller(const EcDesc& d, unsigned long long epoch) {
         st_relaxed_sys(&lg->t_req, t_req);
         st_relaxed_sys(&lg->poison, poison ? 1ull : 0ull);
         t_req = 0;
-        st_release_sys(&lg->gen1, (unsigned long long)g + 1);
-        st_release_sys(&H->done_gen1, (unsigned long long)g + 1);
-        st_release_gpu(&L->done_gen1_dev, (unsigned long long)g + 1);
+        st_release_gpu(&L->done_gen1_dev, (unsigned long long)g + 1);  // device waiters first
+        fence_acq_rel_sys();                     // log entry before the host-visible flags
+        st_relaxed_sys(&lg->gen1, (unsigned long long)g + 1);
+        st_relaxed_sys(&H->done_gen1, (unsigned long long)g + 1);
         ++g;
         snapped = 0;
         contrib = 0;
