@@ -103,6 +103,7 @@ struct alignas(128) EcLocal {
   int step_late;                   // latched late_copy for the current async step's update
   unsigned int round_poison;       // this rank's CTAs saw a non-finite reduced value
   unsigned int upd_bad;            // the async step's update read a non-finite u
+  unsigned long long pin_dev;      // device-side pin (async steps): lowest gen still read
   EcReq dreq[EC_REQ_RING];         // stream-posted requests (device copy of the ring)
 };
 
@@ -123,8 +124,10 @@ struct alignas(64) EcLog {
 
 struct alignas(128) EcHostCtl {
   unsigned long long stop;          // host -> engine: drain and exit
-  unsigned long long pin_lo;        // host -> engine
-  unsigned long long pad0[14];
+  unsigned long long pin_lo;        // host -> engine: lowest generation the host still reads
+  unsigned long long pin_seq;       // host -> engine: bumped with every host pin
+  unsigned long long pin_ack;       // engine -> host: last pin_seq the controller has seen
+  unsigned long long pad0[12];
   unsigned long long done_gen1;     // engine -> host: last completed generation + 1
   unsigned long long req_done;      // engine -> host: requests consumed
   unsigned long long error;
@@ -186,10 +189,14 @@ __device__ __forceinline__ void st_release_sys(unsigned long long* p, unsigned l
 __device__ __forceinline__ void st_release_gpu(unsigned long long* p, unsigned long long v) {
   asm volatile("st.release.gpu.global.u64 [%0], %1;" :: "l"(p), "l"(v) : "memory");
 }
+__device__ __forceinline__ void st_relaxed_gpu(unsigned long long* p, unsigned long long v) {
+  asm volatile("st.relaxed.gpu.global.u64 [%0], %1;" :: "l"(p), "l"(v) : "memory");
+}
 __device__ __forceinline__ void st_relaxed_sys(unsigned long long* p, unsigned long long v) {
   asm volatile("st.relaxed.sys.global.u64 [%0], %1;" :: "l"(p), "l"(v) : "memory");
 }
 __device__ __forceinline__ void fence_sc_sys() { asm volatile("fence.sc.sys;" ::: "memory"); }
+__device__ __forceinline__ void fence_sc_gpu() { asm volatile("fence.sc.gpu;" ::: "memory"); }
 __device__ __forceinline__ void fence_acq_rel_sys() { asm volatile("fence.acq_rel.sys;" ::: "memory"); }
 
 __device__ __forceinline__ uint4 ld_cg_v4(const void* p) {

@@ -260,6 +260,7 @@ int ec_comm_create(int world_size, int rank_lo, int n_local, int device, int64_t
     init.hold_from = EC_INF_GEN;
     init.contributed_round = -1;
     init.stash_null = 1;
+    init.pin_dev = ~0ull;
     if ((e = cudaMemcpy(r->local, &init, sizeof(init), cudaMemcpyHostToDevice)) != cudaSuccess) {
       ec_comm_destroy(c);
       return fail(EC_E_CUDA, "init local: %s", cudaGetErrorString(e));
@@ -656,13 +657,21 @@ int ec_wait(ec_comm_t* c, int li, int64_t t, int timeout_ms, int pin, int64_t* g
     bo.pause();
   }
   long long G = (long long)d1 - 1;
-  if (pin) {
-    // Dekker handshake with the engine's pre-write check (ec_kernels.cu): publish
-    // the pin, then make sure the engine had not already passed the check for
-    // the round that would reuse G's slot.
+  if (pin && !c->direct) {
+    // Pin handshake with the controller's pre-snapshot check (ec_kernels.cu):
+    // publish the pin, wait until the controller has acknowledged seeing it
+    // (it refreshes the host pin every few us), then make sure the engine had
+    // not already passed the check for the round that would reuse G's slot.
     while (true) {
       __atomic_store_n(&r->h->pin_lo, (unsigned long long)G, __ATOMIC_SEQ_CST);
-      __atomic_thread_fence(__ATOMIC_SEQ_CST);
+      const unsigned long long ps = __atomic_add_fetch(&r->h->pin_seq, 1ull, __ATOMIC_SEQ_CST);
+      Backoff ab;
+      while (c->running && aload(&r->h->pin_ack) < ps) {  // a parked engine re-reads at start
+        if ((rc = device_error(r))) return rc;
+        if (ab.expired(timeout_ms < 0 ? 10000 : timeout_ms))
+          return fail(EC_E_TIMEOUT, "rank %d: engine did not acknowledge the pin", r->rank);
+        ab.pause();
+      }
       long long D = (long long)aload(&r->h->done_gen1) - 1;
       if (D < G + c->R - 1) break;
       G = D;

@@ -519,6 +519,9 @@ __device__ void engine_controller(const EcDesc& d, unsigned long long epoch) {
   };
 
   unsigned long long last_host_poll = 0;
+  // host pin, refreshed with every host poll and acknowledged (ec_wait's pin
+  // waits for the ack, so the per-round check never reads host memory)
+  unsigned long long host_pin = ld_relaxed_sys(&H->pin_lo);
   while (true) {
     bool progress = false;
     // Host-mapped words cost a PCIe round trip: read them only every ~8 us
@@ -527,9 +530,14 @@ __device__ void engine_controller(const EcDesc& d, unsigned long long epoch) {
     const unsigned long long now = globaltimer_ns();
     const bool poll_host = now - last_host_poll > 8000ull;
     if (poll_host) last_host_poll = now;
-    if (poll_host && !stopping && ld_relaxed_sys(&H->stop)) {
-      stopping = true;
-      stop_t0 = globaltimer_ns();
+    if (poll_host) {
+      const unsigned long long ps = ld_acquire_sys(&H->pin_seq);
+      host_pin = ld_relaxed_sys(&H->pin_lo);
+      st_release_sys(&H->pin_ack, ps);  // release: orders the pin_lo read before the ack
+      if (!stopping && ld_relaxed_sys(&H->stop)) {
+        stopping = true;
+        stop_t0 = globaltimer_ns();
+      }
     }
     // ---- requests, strictly in sequence order: stream-posted ones sit in the
     // device ring (cheap), host-posted ones only in the host-mapped ring
@@ -620,10 +628,15 @@ __device__ void engine_controller(const EcDesc& d, unsigned long long epoch) {
       }
       if (go && g >= d.R) {
         // Result-slot reuse guard: peers write our slot g % R once the round
-        // starts, so never snapshot g while the host still reads generation
-        // g - R (pin_lo <= g - R).  SC fence pairs with ec_wait's pin store.
-        fence_sc_sys();
-        if (ld_acquire_sys(&H->pin_lo) <= (unsigned long long)(g - d.R)) go = false;
+        // starts, so never snapshot g while a reader still needs generation
+        // g - R.  Device readers pin in device memory (SC fence pairs with
+        // wait_and_pin); the host pin is the acknowledged cached value.
+        fence_sc_gpu();
+        const unsigned long long gr = (unsigned long long)(g - d.R);
+        if (ld_acquire_gpu(&L->pin_dev) <= gr || host_pin <= gr) {
+          go = false;
+          if (host_pin <= gr) last_host_poll = 0;  // re-read the host pin promptly
+        }
       }
       if (go) {
         push_all(1, (((unsigned long long)g + 1) << EC_SNAP_SHIFT) | (unsigned long long)contrib);
@@ -1162,10 +1175,11 @@ __device__ void wait_and_pin(EcLocal* L, EcHostCtl* H, long long t, int R,
     __nanosleep(64);
   }
   long long G = (long long)d1 - 1;
-  // pin G (Dekker with the controller's check before snapshotting G + R)
+  // pin G (Dekker with the controller's check before snapshotting G + R;
+  // both sides on this GPU, so gpu-scope SC fences suffice)
   while (true) {
-    st_relaxed_sys(&H->pin_lo, (unsigned long long)G);
-    fence_sc_sys();
+    st_relaxed_gpu(&L->pin_dev, (unsigned long long)G);
+    fence_sc_gpu();
     const long long D = (long long)ld_acquire_gpu(&L->done_gen1_dev) - 1;
     if (D < G + R - 1) break;
     G = D;
@@ -1290,8 +1304,7 @@ ec_update_gen_kernel(T* __restrict__ w, T* __restrict__ mom, const char* __restr
       if (s_late) *(volatile int*)&L->stash_null = 0;
       st_relaxed_sys(&H->stepbad[t % EC_REQ_RING], atomicExch(&L->upd_bad, 0u) ? 1ull : 0ull);
       const unsigned long long t1 = globaltimer_ns();
-      fence_acq_rel_sys();
-      st_release_sys(&H->pin_lo, ~0ull);  // every CTA has read the slot: unpin
+      st_release_gpu(&L->pin_dev, ~0ull);  // every CTA has read the slot: unpin
       st_relaxed_sys(&H->stepns[t % EC_REQ_RING], t1 - *(volatile unsigned long long*)&L->upd_t0);
       st_release_sys(&H->steptag[t % EC_REQ_RING], (unsigned long long)t + 1);
     }
