@@ -809,7 +809,7 @@ __global__ void ec_direct_decide(const EcDesc* __restrict__ dp, unsigned long lo
 }
 
 template <typename T>
-__global__ void __launch_bounds__(256)
+__global__ void __launch_bounds__(256, 6)
 ec_direct_round(const EcDesc* __restrict__ dp) {
   const EcDesc& d = *dp;
   EcLocal* L = d.local;
@@ -860,7 +860,7 @@ ec_direct_round(const EcDesc* __restrict__ dp) {
 // standalone streaming kernels
 
 template <typename T, int MODE>
-__global__ void __launch_bounds__(256)
+__global__ void __launch_bounds__(256, 6)
 ec_fold_kernel(T* __restrict__ stash, const T* __restrict__ grad, long long n,
                unsigned int* nonfinite, int vec_ok) {
   constexpr int V = Ops<T>::V;
@@ -906,7 +906,7 @@ ec_fold_kernel(T* __restrict__ stash, const T* __restrict__ grad, long long n,
 }
 
 template <typename T>
-__global__ void __launch_bounds__(256)
+__global__ void __launch_bounds__(256, 6)
 ec_update_kernel(T* __restrict__ w, const T* __restrict__ u, T lr, long long n, int vec_ok) {
   constexpr int V = Ops<T>::V;
   constexpr int U = 4;
@@ -941,7 +941,7 @@ ec_update_kernel(T* __restrict__ w, const T* __restrict__ u, T lr, long long n, 
 }
 
 template <typename T>
-__global__ void __launch_bounds__(256)
+__global__ void __launch_bounds__(256, 6)
 ec_momentum_kernel(T* __restrict__ w, T* __restrict__ buf, const T* __restrict__ u, T lr, T mu,
                    long long n, int vec_ok) {
   constexpr int V = Ops<T>::V;
@@ -998,7 +998,7 @@ __device__ __forceinline__ void reduce_vec(const EcSrcs& s, unsigned long long h
 }
 
 template <typename T>
-__global__ void __launch_bounds__(256)
+__global__ void __launch_bounds__(256, 6)
 ec_reduce_kernel(EcSrcs s, int p, unsigned long long has, T* __restrict__ dst, long long n,
                  int div, int vec_ok) {
   constexpr int V = Ops<T>::V;
@@ -1088,7 +1088,7 @@ __device__ __forceinline__ void post_request(EcLocal* L, unsigned long long seq1
 // fold with the device-decided mode; with seq1 != 0 the last CTA also posts the
 // offer (fused fold + post: one launch, the offer leaves as the stash is ready)
 template <typename T>
-__global__ void __launch_bounds__(256)
+__global__ void __launch_bounds__(256, 6)
 ec_fold_auto_kernel(T* __restrict__ stash, const T* __restrict__ grad, long long n,
                     EcLocal* __restrict__ L, int vec_ok, unsigned long long seq1, unsigned flags,
                     long long t, int zero_copy) {
@@ -1217,7 +1217,7 @@ __global__ void ec_wait_gen_kernel(EcLocal* L, EcHostCtl* H, long long t, int R,
 // also performs the wait (block 0) and the last CTA releases the pin
 // (fused wait + update + unpin: one launch)
 template <typename T>
-__global__ void __launch_bounds__(256)
+__global__ void __launch_bounds__(256, 6)
 ec_update_gen_kernel(T* __restrict__ w, T* __restrict__ mom, const char* __restrict__ ring,
                      long long slot_bytes, int R, EcLocal* __restrict__ L, T lr, T mu,
                      long long n, int vec_ok, EcHostCtl* H, long long t,
@@ -1323,9 +1323,23 @@ __global__ void ec_post_kernel(EcLocal* L, unsigned long long seq1, unsigned int
 unsigned long long g_ec_launches = 0;
 static inline void counted(int n = 1) { __atomic_add_fetch(&g_ec_launches, (unsigned long long)n, __ATOMIC_RELAXED); }
 
+// One full wave of the kernel: SMs x resident blocks (grid-stride loops take
+// the rest), queried once per kernel; never more blocks than work.
+static int g_num_sms = 0;
+static int sms() {
+  if (!g_num_sms) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&g_num_sms, cudaDevAttrMultiProcessorCount, dev);
+    if (g_num_sms <= 0) g_num_sms = 148;
+  }
+  return g_num_sms;
+}
+// streaming kernels are __launch_bounds__(256, 6): exactly one wave is
+// SMs x 6 blocks, grid-stride loops do the rest (no second-wave tail)
 static inline int grid_for(long long work, int threads) {
   long long b = (work + threads - 1) / threads;
-  const long long cap = 148LL * 8;
+  const long long cap = (long long)sms() * 6;
   if (b > cap) b = cap;
   if (b < 1) b = 1;
   return (int)b;
