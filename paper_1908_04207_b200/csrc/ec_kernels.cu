@@ -1213,11 +1213,69 @@ __global__ void ec_wait_gen_kernel(EcLocal* L, EcHostCtl* H, long long t, int R,
   }
 }
 
+// w = w - lr*u (or the momentum form), 16-byte vectors, U in flight per thread;
+// returns whether this thread read a non-finite u
+template <typename T, bool MOM, int U>
+__device__ __forceinline__ bool update_body(T* __restrict__ w, T* __restrict__ mom,
+                                            const T* __restrict__ u, T lr, T mu, long long n,
+                                            int vec_ok) {
+  constexpr int V = Ops<T>::V;
+  const long long tid = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  const long long nth = (long long)gridDim.x * blockDim.x;
+  long long done = 0;
+  bool bad = false;
+  if (vec_ok) {
+    const long long nv = n / V;
+    for (long long base = tid; base < nv; base += nth * U) {
+      Vec16<T> wv[U], uv[U], bv[MOM ? U : 1];
+#pragma unroll
+      for (int k = 0; k < U; ++k) {
+        const long long v = base + k * nth;
+        if (v < nv) {
+          wv[k].raw = ld_stream_v4(w + v * V);
+          uv[k].raw = ld_cg_v4(u + v * V);
+          if (MOM) bv[MOM ? k : 0].raw = ld_stream_v4(mom + v * V);
+        }
+      }
+#pragma unroll
+      for (int k = 0; k < U; ++k) {
+        const long long v = base + k * nth;
+        if (v < nv) {
+#pragma unroll
+          for (int l = 0; l < V; ++l) {
+            bad |= !Ops<T>::finite(uv[k].e[l]);
+            if (MOM) {
+              bv[MOM ? k : 0].e[l] = Ops<T>::mom(mu, bv[MOM ? k : 0].e[l], uv[k].e[l]);
+              wv[k].e[l] = Ops<T>::sgd(wv[k].e[l], lr, bv[MOM ? k : 0].e[l]);
+            } else {
+              wv[k].e[l] = Ops<T>::sgd(wv[k].e[l], lr, uv[k].e[l]);
+            }
+          }
+          if (MOM) st_v4(mom + v * V, bv[MOM ? k : 0].raw);
+          st_v4(w + v * V, wv[k].raw);
+        }
+      }
+    }
+    done = nv * V;
+  }
+  for (long long e = done + tid; e < n; e += nth) {
+    T uu = u[e];
+    bad |= !Ops<T>::finite(uu);
+    if (MOM) {
+      T b = Ops<T>::mom(mu, mom[e], uu);
+      mom[e] = b;
+      uu = b;
+    }
+    w[e] = Ops<T>::sgd(w[e], lr, uu);
+  }
+  return bad;
+}
+
 // update from the slot of the step's generation; with H != nullptr the kernel
 // also performs the wait (block 0) and the last CTA releases the pin
 // (fused wait + update + unpin: one launch)
-template <typename T>
-__global__ void __launch_bounds__(256, 6)
+template <typename T, bool MOM>
+__global__ void __launch_bounds__(256, 4)
 ec_update_gen_kernel(T* __restrict__ w, T* __restrict__ mom, const char* __restrict__ ring,
                      long long slot_bytes, int R, EcLocal* __restrict__ L, T lr, T mu,
                      long long n, int vec_ok, EcHostCtl* H, long long t,
@@ -1243,58 +1301,7 @@ ec_update_gen_kernel(T* __restrict__ w, T* __restrict__ mom, const char* __restr
     for (long long e = tid0; e < n; e += nth0) stash[e] = Ops<T>::canon(gbuf[e]);
   }
   const T* __restrict__ u = reinterpret_cast<const T*>(ring + (G % R) * slot_bytes);
-  constexpr int V = Ops<T>::V;
-  const long long tid = (long long)blockIdx.x * blockDim.x + threadIdx.x;
-  const long long nth = (long long)gridDim.x * blockDim.x;
-  long long done = 0;
-  bool bad = false;
-  if (vec_ok) {
-    constexpr int U = 2;
-    const long long nv = n / V;
-    for (long long base = tid; base < nv; base += nth * U) {
-      Vec16<T> wv[U], uv[U], bv[U];
-#pragma unroll
-      for (int k = 0; k < U; ++k) {
-        const long long v = base + k * nth;
-        if (v < nv) {
-          wv[k].raw = ld_stream_v4(w + v * V);
-          uv[k].raw = ld_cg_v4(u + v * V);
-          if (mom) bv[k].raw = ld_stream_v4(mom + v * V);
-        }
-      }
-#pragma unroll
-      for (int k = 0; k < U; ++k) {
-        const long long v = base + k * nth;
-        if (v < nv) {
-          if (mom) {
-#pragma unroll
-            for (int l = 0; l < V; ++l) {
-              bv[k].e[l] = Ops<T>::mom(mu, bv[k].e[l], uv[k].e[l]);
-              wv[k].e[l] = Ops<T>::sgd(wv[k].e[l], lr, bv[k].e[l]);
-            }
-            st_v4(mom + v * V, bv[k].raw);
-          } else {
-#pragma unroll
-            for (int l = 0; l < V; ++l) wv[k].e[l] = Ops<T>::sgd(wv[k].e[l], lr, uv[k].e[l]);
-          }
-#pragma unroll
-          for (int l = 0; l < V; ++l) bad |= !Ops<T>::finite(uv[k].e[l]);
-          st_v4(w + v * V, wv[k].raw);
-        }
-      }
-    }
-    done = nv * V;
-  }
-  for (long long e = done + tid; e < n; e += nth) {
-    T uu = u[e];
-    bad |= !Ops<T>::finite(uu);
-    if (mom) {
-      T b = Ops<T>::mom(mu, mom[e], uu);
-      mom[e] = b;
-      uu = b;
-    }
-    w[e] = Ops<T>::sgd(w[e], lr, uu);
-  }
+  const bool bad = update_body<T, MOM, MOM ? 2 : 4>(w, mom, u, lr, mu, n, vec_ok);
   if (H == nullptr) return;
   if (__syncthreads_or(bad) && threadIdx.x == 0) atomicOr(&L->upd_bad, 1u);
   if (threadIdx.x == 0) {
@@ -1365,7 +1372,8 @@ cudaError_t preload_kernels() {
       (const void*)ec_fold_auto_kernel<float>, (const void*)ec_fold_auto_kernel<double>,
       (const void*)ec_fold_auto_kernel<long long>, (const void*)ec_wait_gen_kernel,
       (const void*)ec_wait_done_kernel,
-      (const void*)ec_update_gen_kernel<float>, (const void*)ec_update_gen_kernel<double>,
+      (const void*)ec_update_gen_kernel<float, false>, (const void*)ec_update_gen_kernel<double, false>,
+      (const void*)ec_update_gen_kernel<float, true>, (const void*)ec_update_gen_kernel<double, true>,
   };
   for (const void* f : fns) {
     cudaFuncAttributes a;
@@ -1506,15 +1514,18 @@ cudaError_t launch_update_gen(int dtype, void* w, void* mom, const char* ring, l
   counted();
   const int vec_ok = ((((uintptr_t)w) | ((uintptr_t)mom) | ((uintptr_t)ring) | slot_bytes) & 15) == 0;
   const int V = dtype == 0 ? 4 : 2;
-  const int grid = grid_for((n / V + 1) / 2 + 1, 256);
-  if (dtype == 0)
-    ec_update_gen_kernel<float><<<grid, 256, 0, s>>>((float*)w, (float*)mom, ring, slot_bytes, R, L,
-                                                     (float)lr, (float)mu, n, vec_ok, H, t, timeout_ns,
-                                                     seq1, (float*)stash, (const float*)gbuf);
-  else if (dtype == 1)
-    ec_update_gen_kernel<double><<<grid, 256, 0, s>>>((double*)w, (double*)mom, ring, slot_bytes, R, L,
-                                                      lr, mu, n, vec_ok, H, t, timeout_ns,
-                                                      seq1, (double*)stash, (const double*)gbuf);
+  // __launch_bounds__(256, 4): one wave is SMs x 4 blocks
+  long long gb = ((n / V + 1) / 4 + 255) / 256 + 1;
+  const int grid = (int)(gb < (long long)sms() * 4 ? gb : (long long)sms() * 4);
+  if (dtype == 0) {
+    auto kern = mom ? ec_update_gen_kernel<float, true> : ec_update_gen_kernel<float, false>;
+    kern<<<grid, 256, 0, s>>>((float*)w, (float*)mom, ring, slot_bytes, R, L, (float)lr, (float)mu, n,
+                              vec_ok, H, t, timeout_ns, seq1, (float*)stash, (const float*)gbuf);
+  } else if (dtype == 1) {
+    auto kern = mom ? ec_update_gen_kernel<double, true> : ec_update_gen_kernel<double, false>;
+    kern<<<grid, 256, 0, s>>>((double*)w, (double*)mom, ring, slot_bytes, R, L, lr, mu, n, vec_ok, H,
+                              t, timeout_ns, seq1, (double*)stash, (const double*)gbuf);
+  }
   else
     return cudaErrorInvalidValue;
   return cudaGetLastError();
