@@ -208,6 +208,62 @@ def run_training_rank(world, rank, p, flavor, *, epochs=48, steps_per_epoch=4, d
             "w": st.w.detach().cpu().numpy(), "handles": (h, hr)}
 
 
+def lstm_bench(world, rank, p, steps=20, warmup=3, batch=16, max_len=None, max_over=lambda x: x):
+    """BASELINE config 4: eager-SGD on the UCF101-shaped LSTM, one flavor after
+    the other, inherent imbalance only (variable sequence lengths).  The
+    gradient is produced by backward straight into the registered bucket and
+    offered zero-copy; reports aggregate steps/s, mean nap and speedup vs sync."""
+    from collections import deque
+
+    import numpy as np
+    import torch
+
+    from .collectives import AllreduceHandle, CollectiveConfig
+    from .eagersgd import TrainState, attach_delivery_tracking, finish_step, train_step_async
+    from .lstm import SyntheticUCF101, VideoLSTM, bind_flat, lstm_grad_step, n_params
+    torch.manual_seed(1234)
+    dev = torch.device("cuda", world.device)
+    data = SyntheticUCF101(batch=batch, device=dev, max_len=max_len)
+    out = {}
+    for i, flavor in enumerate(("sync", "solo", "majority")):
+        model = VideoLSTM().to(dev)
+        n = n_params(model)
+        h = AllreduceHandle(CollectiveConfig(p=p, flavor=flavor, vector_len=n, element="f4",
+                                             seed=1234), rank, world, cid=4000 + i)
+        st = TrainState.fresh(torch.zeros(n, device=dev), 0.01, rank=rank, tau=None)
+        bind_flat(model, st.w, h.grad_buffer())
+        attach_delivery_tracking(h, st)
+        naps, losses = [], []
+        pend = deque()
+
+        def run(k, t0):
+            for s in range(k):
+                loss = lstm_grad_step(model, h.grad_buffer(), data.batch_for(rank, t0 + s))
+                pend.append(train_step_async(st, h, h.grad_buffer(), loss=loss))
+                while len(pend) > 1:
+                    _, res, _ = finish_step(st, h, pend.popleft())
+                    naps.append(res.nap)
+            while pend:
+                lo, res, _ = finish_step(st, h, pend.popleft())
+                naps.append(res.nap)
+                losses.append(float(lo))
+
+        run(warmup, 0)
+        naps.clear()
+        world._barrier()
+        t0 = time.perf_counter()
+        run(steps, warmup)
+        torch.cuda.current_stream().synchronize()
+        wall = max_over(time.perf_counter() - t0)
+        out[flavor] = {"steps_per_s": p * steps / wall, "mean_nap": float(np.mean(naps)),
+                       "params": n, "wall_s": wall}
+        h.close()
+        del model
+    for f in out:
+        out[f]["speedup_vs_sync"] = out[f]["steps_per_s"] / out["sync"]["steps_per_s"]
+    return out
+
+
 def summarize(records):
     """harness.py:347-370"""
     import numpy as np
@@ -244,7 +300,7 @@ def _main(argv=None):
     from .transport import DelayModel
     from .world import ProcessWorld
     ap = argparse.ArgumentParser()
-    ap.add_argument("mode", choices=("sweep", "latency", "train"))
+    ap.add_argument("mode", choices=("sweep", "latency", "train", "lstm"))
     ap.add_argument("--flavors", default="solo,majority")
     ap.add_argument("--sizes", default="1K,4K,16K,64K,256K,1M,4M,16M,64M,100M,256M,1G")
     ap.add_argument("--workers", default="")
@@ -302,6 +358,9 @@ def _main(argv=None):
                                     world.release(cid)
                                 except Exception:
                                     pass
+    elif args.mode == "lstm":
+        result["lstm"] = lstm_bench(world, rank, p, steps=args.rounds if args.rounds != 64 else 20,
+                                    max_over=max_over)
     elif args.mode == "train":
         # BASELINE config 1 on GPUs: hyperplane, random_subset 0.2 ms k=1 seed 11
         import numpy as np
