@@ -42,7 +42,11 @@ class VideoLSTM(torch.nn.Module):
         self.head = torch.nn.Linear(hidden, classes)
 
     def forward(self, x, lengths):
-        out, _ = self.lstm(x)
+        # cuDNN's RNN path synchronises the device internally, which would wait
+        # on the resident collective engine forever; torch's native LSTM
+        # (cuBLAS GEMMs + fused cell kernels) does not
+        with torch.backends.cudnn.flags(enabled=False):
+            out, _ = self.lstm(x)
         last = out[torch.arange(x.shape[0], device=x.device), lengths - 1]
         return self.head(last)
 
@@ -94,7 +98,8 @@ def lstm_grad_step(model: VideoLSTM, bucket: torch.Tensor, batch):
     bucket.zero_()
     logits = model(x, lens)
     loss = torch.nn.functional.cross_entropy(logits, y)
-    loss.backward()
+    with torch.backends.cudnn.flags(enabled=False):
+        loss.backward()
     off = 0
     for p in model.parameters():   # autograd accumulates in place; re-home if it did not
         k = p.numel()
