@@ -77,6 +77,16 @@ int ec_comm_export(ec_comm_t* c, int local_idx, void* blob, size_t cap, size_t* 
 int ec_comm_import(ec_comm_t* c, int peer_rank, const void* blob, size_t len);
 /* Replay mode: force generation g's inclusion mask to masks[g] (g < n). */
 int ec_comm_set_replay(ec_comm_t* c, int local_idx, const uint64_t* masks, int64_t n);
+/* NVLS ("fast" reduction mode, fp32, one rank per GPU): the NVSwitch reduces.
+ * One rank ec_nvls_create()s the multicast object and shares the fabric-handle
+ * blob; every rank ec_nvls_attach()es it (the creator passes NULL); after all
+ * ranks attached, every rank ec_nvls_bind()s its memory, which also switches the
+ * data phase to multimem.ld_reduce / multimem.st.  Summation order inside the
+ * switch is unspecified: never bit-exact, within fp32 rounding of the sum. */
+int ec_nvls_supported(int device);
+int ec_nvls_create(ec_comm_t* c, void* blob, size_t cap, size_t* len);
+int ec_nvls_attach(ec_comm_t* c, const void* blob, size_t len);
+int ec_nvls_bind(ec_comm_t* c);
 /* Start (or resume) the persistent engine kernel on the comm's own stream. */
 int ec_comm_start(ec_comm_t* c);
 /* Drain and stop the engine at a round boundary so device-wide syncs return;

@@ -39,13 +39,17 @@ from .world import ELEMENTS, EmulatedWorld, ProcessWorld
 
 SOLO, MAJORITY, SYNC = "solo", "majority", "sync"
 FLAVORS = (SOLO, MAJORITY, SYNC)
-REDUCTION_MODES = ("fixed_order",)
+# fixed_order: tree_order_sum's association, bit-exact (default, parity mode);
+# fast: any association -- one rank per GPU uses the NVSwitch reduction (NVLS)
+# when the fabric supports it, else the fixed-order engine
+REDUCTION_MODES = ("fixed_order", "fast")
 
 
 @dataclass(frozen=True)
 class CollectiveConfig:
     """collectives.py:43-67, plus `element="f4"` (the product's fp32 path) and
-    `reduction_mode` (only the bit-exact "fixed_order" association)."""
+    `reduction_mode`: "fixed_order" (bit-exact tree order) or "fast" (NVSwitch
+    in-switch reduction; results within fp32 rounding, identical on all ranks)."""
 
     p: int
     flavor: str

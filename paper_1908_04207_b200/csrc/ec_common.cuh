@@ -49,6 +49,7 @@ struct alignas(128) EcCtrl {
   unsigned long long rsdone_from[EC_MAX_P];  // gen+1: source's reduced shard ready
   unsigned long long arrive_from[EC_MAX_P];  // gen+1: source boarded (all-arrive)
   unsigned long long done_from[EC_MAX_P];    // gen+1: source's data for gen is in our slot
+  unsigned long long staged_from[EC_MAX_P];  // gen+1: source staged its offer (NVLS mode)
 };
 
 struct alignas(64) EcReq {
@@ -104,6 +105,7 @@ struct alignas(128) EcLocal {
   unsigned int round_poison;       // this rank's CTAs saw a non-finite reduced value
   unsigned int upd_bad;            // the async step's update read a non-finite u
   unsigned long long pin_dev;      // device-side pin (async steps): lowest gen still read
+  unsigned long long stage_count;  // NVLS: CTAs that staged this round (monotone)
   EcReq dreq[EC_REQ_RING];         // stream-posted requests (device copy of the ring)
 };
 
@@ -147,7 +149,8 @@ struct alignas(128) EcHostCtl {
 struct EcDesc {
   int rank, P, flavor, dtype;
   int R, W, replay, vec;              // ring slots, worker CTAs, replay flag, elems / 16 B
-  int mode;                           // data phase: 0 = fused TMA, 1 = two-phase ld.cg pull
+  int mode;                           // data phase: 0 = fused TMA, 1 = two-phase ld.cg pull,
+                                      // 2 = NVLS (multimem.ld_reduce / multimem.st, fast mode)
   int chv, stages;                    // TMA chunk (16-B vectors) and pipeline depth
   int smem_bytes;
   long long n, nvec;                  // elements, whole 16-B vectors
@@ -158,6 +161,9 @@ struct EcDesc {
   char* send[EC_MAX_P];
   char* ring[EC_MAX_P];
   char* gbuf[EC_MAX_P];               // registered gradient buffers (zero-copy offers)
+  char* mc_stage;                     // NVLS: multicast view of the staging region
+  char* mc_ring;                      // NVLS: multicast view of the result ring
+  char* uc_stage;                     // NVLS: this rank's unicast view of the staging region
   EcHostCtl* hctl;
   EcLocal* local;
   const unsigned long long* forced;

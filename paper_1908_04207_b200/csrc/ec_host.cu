@@ -1,5 +1,6 @@
 // Host side of the eagercoll_b200 C ABI: communicator, IPC peer mapping,
 // request ring, waits and launches.  See include/eagercoll_b200.h.
+#include <cuda.h>
 #include <cuda_runtime.h>
 #include <errno.h>
 #include <immintrin.h>
@@ -142,6 +143,12 @@ struct ec_comm {
   void* last_stream = nullptr;  // direct mode orders host-posted requests on it
   unsigned long long epoch = 0;
   int mode = 0, chv = 256, stages = 4, smem_bytes = 0;  // data phase (see EcDesc)
+  // NVLS (reduction_mode "fast"): multicast object over every rank's GPU
+  CUmemGenericAllocationHandle mc_handle = 0, mc_phys = 0;
+  bool mc_created = false, mc_attached = false, mc_phys_made = false;
+  CUdeviceptr mc_va = 0, uc_va = 0;
+  size_t mc_size = 0;
+  char* ring_cuda = nullptr;  // the cudaMalloc'd ring, restored when NVLS is torn down
 };
 
 static int check_li(ec_comm_t* c, int li) {
@@ -156,6 +163,215 @@ static int device_error(EcRankHost* r) {
     return fail(EC_E_DEVICE, "engine error %llu (info 0x%llx) at rank %d", e,
                 aload(&r->h->error_info), r->rank);
   }
+  return EC_OK;
+}
+
+
+// ---- NVLS: NVSwitch multicast objects through the driver API ----------------
+// (entry points fetched at run time: the library must load where no driver is
+// installed, e.g. the build container)
+typedef CUresult (*PFN_mcCreate)(CUmemGenericAllocationHandle*, const CUmulticastObjectProp*);
+typedef CUresult (*PFN_mcAddDevice)(CUmemGenericAllocationHandle, CUdevice);
+typedef CUresult (*PFN_mcBindMem)(CUmemGenericAllocationHandle, size_t, CUmemGenericAllocationHandle, size_t, size_t, unsigned long long);
+typedef CUresult (*PFN_mcGran)(size_t*, const CUmulticastObjectProp*, CUmulticastGranularity_flags);
+typedef CUresult (*PFN_memCreate)(CUmemGenericAllocationHandle*, size_t, const CUmemAllocationProp*, unsigned long long);
+typedef CUresult (*PFN_memRelease)(CUmemGenericAllocationHandle);
+typedef CUresult (*PFN_addrReserve)(CUdeviceptr*, size_t, size_t, CUdeviceptr, unsigned long long);
+typedef CUresult (*PFN_addrFree)(CUdeviceptr, size_t);
+typedef CUresult (*PFN_memMap)(CUdeviceptr, size_t, size_t, CUmemGenericAllocationHandle, unsigned long long);
+typedef CUresult (*PFN_memUnmap)(CUdeviceptr, size_t);
+typedef CUresult (*PFN_setAccess)(CUdeviceptr, size_t, const CUmemAccessDesc*, size_t);
+typedef CUresult (*PFN_export)(void*, CUmemGenericAllocationHandle, CUmemAllocationHandleType, unsigned long long);
+typedef CUresult (*PFN_import)(CUmemGenericAllocationHandle*, void*, CUmemAllocationHandleType);
+typedef CUresult (*PFN_devGet)(CUdevice*, int);
+typedef CUresult (*PFN_devAttr)(int*, CUdevice_attribute, CUdevice);
+typedef CUresult (*PFN_mcUnbind)(CUmemGenericAllocationHandle, CUdevice, size_t, size_t);
+
+struct DrvApi {
+  PFN_mcCreate mcCreate = nullptr;
+  PFN_mcAddDevice mcAddDevice = nullptr;
+  PFN_mcBindMem mcBindMem = nullptr;
+  PFN_mcGran mcGran = nullptr;
+  PFN_memCreate memCreate = nullptr;
+  PFN_memRelease memRelease = nullptr;
+  PFN_addrReserve addrReserve = nullptr;
+  PFN_addrFree addrFree = nullptr;
+  PFN_memMap memMap = nullptr;
+  PFN_memUnmap memUnmap = nullptr;
+  PFN_setAccess setAccess = nullptr;
+  PFN_export exportH = nullptr;
+  PFN_import importH = nullptr;
+  PFN_devGet devGet = nullptr;
+  PFN_devAttr devAttr = nullptr;
+  PFN_mcUnbind mcUnbind = nullptr;
+  bool ok = false;
+};
+
+static DrvApi& drv() {
+  static DrvApi d;
+  static bool tried = false;
+  if (tried) return d;
+  tried = true;
+  auto get = [](const char* name, void** fn) -> bool {
+    cudaDriverEntryPointQueryResult q;
+    return cudaGetDriverEntryPoint(name, fn, cudaEnableDefault, &q) == cudaSuccess &&
+           q == cudaDriverEntryPointSuccess && *fn;
+  };
+  d.ok = get("cuMulticastCreate", (void**)&d.mcCreate) && get("cuMulticastAddDevice", (void**)&d.mcAddDevice) &&
+         get("cuMulticastBindMem", (void**)&d.mcBindMem) && get("cuMulticastGetGranularity", (void**)&d.mcGran) &&
+         get("cuMemCreate", (void**)&d.memCreate) && get("cuMemRelease", (void**)&d.memRelease) &&
+         get("cuMemAddressReserve", (void**)&d.addrReserve) && get("cuMemAddressFree", (void**)&d.addrFree) &&
+         get("cuMemMap", (void**)&d.memMap) && get("cuMemUnmap", (void**)&d.memUnmap) &&
+         get("cuMemSetAccess", (void**)&d.setAccess) &&
+         get("cuMemExportToShareableHandle", (void**)&d.exportH) &&
+         get("cuMemImportFromShareableHandle", (void**)&d.importH) && get("cuDeviceGet", (void**)&d.devGet) &&
+         get("cuDeviceGetAttribute", (void**)&d.devAttr) && get("cuMulticastUnbind", (void**)&d.mcUnbind);
+  return d;
+}
+
+#define DRV(call)                                                                 \
+  do {                                                                            \
+    CUresult r_ = (call);                                                         \
+    if (r_ != CUDA_SUCCESS) return fail(EC_E_CUDA, "%s failed (%d)", #call, (int)r_); \
+  } while (0)
+
+static size_t nvls_size(ec_comm_t* c, size_t gran) {
+  const size_t want = (size_t)c->slot_bytes * (1 + c->R);  // staging + result ring
+  return ((want + gran - 1) / gran) * gran;
+}
+
+static int nvls_prop(ec_comm_t* c, CUmulticastObjectProp* prop, size_t* gran) {
+  DrvApi& D = drv();
+  memset(prop, 0, sizeof(*prop));
+  prop->numDevices = c->P;
+  prop->handleTypes = CU_MEM_HANDLE_TYPE_FABRIC;
+  prop->size = (size_t)c->slot_bytes * (1 + c->R);
+  DRV(D.mcGran(gran, prop, CU_MULTICAST_GRANULARITY_MINIMUM));
+  prop->size = nvls_size(c, *gran);
+  return EC_OK;
+}
+
+static void nvls_teardown(ec_comm_t* c) {
+  DrvApi& D = drv();
+  if (!D.ok) return;
+  if (c->mode == 2 && c->ring_cuda) {
+    c->L[0]->ring = c->ring_cuda;
+    c->ring[c->rank_lo] = c->ring_cuda;
+    c->mode = 0;
+  }
+  if (c->mc_va) {
+    D.memUnmap(c->mc_va, c->mc_size);
+    D.addrFree(c->mc_va, c->mc_size);
+    c->mc_va = 0;
+  }
+  if (c->uc_va) {
+    D.memUnmap(c->uc_va, c->mc_size);
+    D.addrFree(c->uc_va, c->mc_size);
+    c->uc_va = 0;
+  }
+  if (c->mc_phys_made) {
+    CUdevice dev;
+    if (D.devGet(&dev, c->device) == CUDA_SUCCESS) D.mcUnbind(c->mc_handle, dev, 0, c->mc_size);
+    D.memRelease(c->mc_phys);
+    c->mc_phys_made = false;
+  }
+  if (c->mc_created || c->mc_attached) {
+    D.memRelease(c->mc_handle);
+    c->mc_created = c->mc_attached = false;
+  }
+}
+
+extern "C" int ec_nvls_supported(int device) {
+  DrvApi& D = drv();
+  if (!D.ok) return 0;
+  CUdevice dev;
+  if (D.devGet(&dev, device) != CUDA_SUCCESS) return 0;
+  int mc = 0, fab = 0;
+  D.devAttr(&mc, CU_DEVICE_ATTRIBUTE_MULTICAST_SUPPORTED, dev);
+  D.devAttr(&fab, CU_DEVICE_ATTRIBUTE_HANDLE_TYPE_FABRIC_SUPPORTED, dev);
+  return mc && fab;
+}
+
+extern "C" int ec_nvls_create(ec_comm_t* c, void* blob, size_t cap, size_t* len) {
+  if (!c) return fail(EC_E_ARG, "null communicator");
+  if (c->n_local != 1 || c->dtype != EC_F32 || c->P < 2)
+    return fail(EC_E_ARG, "NVLS needs one fp32 rank per GPU and P >= 2");
+  if (cap < sizeof(CUmemFabricHandle)) return fail(EC_E_ARG, "blob too small");
+  DrvApi& D = drv();
+  if (!D.ok) return fail(EC_E_STATE, "driver multicast API unavailable");
+  CK(cudaSetDevice(c->device));
+  CUmulticastObjectProp prop;
+  size_t gran = 0;
+  int rc = nvls_prop(c, &prop, &gran);
+  if (rc) return rc;
+  DRV(D.mcCreate(&c->mc_handle, &prop));
+  c->mc_created = true;
+  c->mc_size = prop.size;
+  CUmemFabricHandle fh;
+  DRV(D.exportH(&fh, c->mc_handle, CU_MEM_HANDLE_TYPE_FABRIC, 0));
+  memcpy(blob, &fh, sizeof(fh));
+  if (len) *len = sizeof(fh);
+  return EC_OK;
+}
+
+extern "C" int ec_nvls_attach(ec_comm_t* c, const void* blob, size_t len) {
+  if (!c) return fail(EC_E_ARG, "null communicator");
+  DrvApi& D = drv();
+  if (!D.ok) return fail(EC_E_STATE, "driver multicast API unavailable");
+  CK(cudaSetDevice(c->device));
+  if (!c->mc_created) {
+    if (len < sizeof(CUmemFabricHandle)) return fail(EC_E_ARG, "blob too short");
+    CUmemFabricHandle fh;
+    memcpy(&fh, blob, sizeof(fh));
+    DRV(D.importH(&c->mc_handle, &fh, CU_MEM_HANDLE_TYPE_FABRIC));
+    c->mc_attached = true;
+    CUmulticastObjectProp prop;
+    size_t gran = 0;
+    int rc = nvls_prop(c, &prop, &gran);
+    if (rc) return rc;
+    c->mc_size = prop.size;
+  }
+  CUdevice dev;
+  DRV(D.devGet(&dev, c->device));
+  DRV(D.mcAddDevice(c->mc_handle, dev));
+  return EC_OK;
+}
+
+extern "C" int ec_nvls_bind(ec_comm_t* c) {
+  if (!c) return fail(EC_E_ARG, "null communicator");
+  if (c->running) return fail(EC_E_STATE, "bind NVLS before the engine starts");
+  DrvApi& D = drv();
+  if (!D.ok || !(c->mc_created || c->mc_attached)) return fail(EC_E_STATE, "attach first");
+  CK(cudaSetDevice(c->device));
+  CUmemAllocationProp p;
+  memset(&p, 0, sizeof(p));
+  p.type = CU_MEM_ALLOCATION_TYPE_PINNED;
+  p.location.type = CU_MEM_LOCATION_TYPE_DEVICE;
+  p.location.id = c->device;
+  p.requestedHandleTypes = CU_MEM_HANDLE_TYPE_FABRIC;
+  DRV(D.memCreate(&c->mc_phys, c->mc_size, &p, 0));
+  c->mc_phys_made = true;
+  DRV(D.mcBindMem(c->mc_handle, 0, c->mc_phys, 0, c->mc_size, 0));
+  CUmemAccessDesc acc;
+  memset(&acc, 0, sizeof(acc));
+  acc.location.type = CU_MEM_LOCATION_TYPE_DEVICE;
+  acc.location.id = c->device;
+  acc.flags = CU_MEM_ACCESS_FLAGS_PROT_READWRITE;
+  const size_t align = 2ull << 20;
+  DRV(D.addrReserve(&c->uc_va, c->mc_size, align, 0, 0));
+  DRV(D.memMap(c->uc_va, c->mc_size, 0, c->mc_phys, 0));
+  DRV(D.setAccess(c->uc_va, c->mc_size, &acc, 1));
+  DRV(D.addrReserve(&c->mc_va, c->mc_size, align, 0, 0));
+  DRV(D.memMap(c->mc_va, c->mc_size, 0, c->mc_handle, 0));
+  DRV(D.setAccess(c->mc_va, c->mc_size, &acc, 1));
+  CK(cudaMemset((void*)c->uc_va, 0, c->mc_size));
+  CK(cudaDeviceSynchronize());
+  // the result ring now lives in the multicast-bound region (after the staging slot)
+  EcRankHost* r = c->L[0];
+  c->ring_cuda = r->ring;
+  r->ring = (char*)c->uc_va + c->slot_bytes;
+  c->ring[c->rank_lo] = r->ring;
+  c->mode = 2;
   return EC_OK;
 }
 
@@ -386,6 +602,11 @@ static int upload_descs(ec_comm_t* c) {
       x.ring[q] = c->ring[q];
       x.gbuf[q] = c->gbuf[q];
     }
+    if (c->mode == 2) {
+      x.mc_stage = (char*)c->mc_va;
+      x.mc_ring = (char*)c->mc_va + c->slot_bytes;
+      x.uc_stage = (char*)c->uc_va;
+    }
     x.hctl = r->hd;
     x.local = r->local;
     x.forced = r->forced;
@@ -450,6 +671,7 @@ int ec_comm_destroy(ec_comm_t* c) {
       cudaIpcCloseMemHandle(c->gbuf[q]);
     }
   }
+  nvls_teardown(c);
   for (EcRankHost* r : c->L) {
     if (r->ctrl) cudaFree(r->ctrl);
     if (r->send) cudaFree(r->send);

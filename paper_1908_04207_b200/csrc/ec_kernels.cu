@@ -395,6 +395,100 @@ __device__ void round_ldg(const EcDesc& d, const char* const* sp, int w, long lo
   }
 }
 
+// ---------------------------------------------------------------------------
+// NVLS data phase (reduction_mode "fast", fp32, one rank per GPU): the NVSwitch
+// reduces.  Every rank stages its offer (or zeros) into its copy of a
+// multicast-bound region; the owner of each shard reads the switch-reduced
+// sum with multimem.ld_reduce and broadcasts u = sum / P into every rank's
+// result slot with multimem.st.  Per GPU that moves S + S/P each way instead
+// of the two-shot's 2(P-1)/P * S, at the price of the switch's (unspecified)
+// summation order -- never the fixed-order mode.
+
+__device__ __forceinline__ void fence_proxy_alias() { asm volatile("fence.proxy.alias;" ::: "memory"); }
+
+__device__ __forceinline__ float4 mm_ld_reduce_v4(const void* p) {
+  float4 r;
+  asm volatile("multimem.ld_reduce.relaxed.sys.global.add.v4.f32 {%0,%1,%2,%3}, [%4];"
+               : "=f"(r.x), "=f"(r.y), "=f"(r.z), "=f"(r.w) : "l"(p) : "memory");
+  return r;
+}
+__device__ __forceinline__ void mm_st_v4(void* p, float4 v) {
+  asm volatile("multimem.st.relaxed.sys.global.v4.f32 [%0], {%1,%2,%3,%4};"
+               :: "l"(p), "f"(v.x), "f"(v.y), "f"(v.z), "f"(v.w) : "memory");
+}
+__device__ __forceinline__ float mm_ld_reduce_f32(const void* p) {
+  float r;
+  asm volatile("multimem.ld_reduce.relaxed.sys.global.add.f32 %0, [%1];" : "=f"(r) : "l"(p) : "memory");
+  return r;
+}
+__device__ __forceinline__ void mm_st_f32(void* p, float v) {
+  asm volatile("multimem.st.relaxed.sys.global.f32 [%0], %1;" :: "l"(p), "f"(v) : "memory");
+}
+
+template <typename T>
+__device__ void round_nvls(const EcDesc& d, const char* const* sp, int w, long long g,
+                           unsigned long long has, unsigned long long seen, bool& bad) {
+  EcLocal* L = d.local;
+  EcCtrl* C = d.ctrl[d.rank];
+  const int tid = threadIdx.x, P = d.P, r = d.rank;
+  const long long bt = blockDim.x, start = (long long)w * bt + tid, stride = (long long)d.W * bt;
+  // 1. stage my offer (or zeros for a null snapshot) into my copy of the region
+  const bool mine = (has >> r) & 1ull;
+  const char* src = sp[r];
+  for (long long v = start; v < d.nvec; v += stride)
+    st_v4(d.uc_stage + v * 16, mine ? ld_stream_v4(src + v * 16) : make_uint4(0, 0, 0, 0));
+  if (w == 0 && tid < 4) {
+    const long long e = d.nvec * 4 + tid;
+    if (e < d.n) reinterpret_cast<float*>(d.uc_stage)[e] = mine ? reinterpret_cast<const float*>(src)[e] : 0.0f;
+  }
+  __syncthreads();
+  if (tid == 0) {
+    fence_proxy_alias();
+    __threadfence();
+    if (atomicAdd(&L->stage_count, 1ull) + 1 == (unsigned long long)d.W * seen) {
+      fence_acq_rel_sys();
+      for (int q = 0; q < P; ++q) st_relaxed_sys(&d.ctrl[q]->staged_from[r], (unsigned long long)g + 1);
+    }
+    // 2. every rank staged
+    const unsigned long long t0 = globaltimer_ns();
+    for (int q = 0; q < P; ++q) {
+      while (ld_acquire_sys(&C->staged_from[q]) < (unsigned long long)g + 1) {
+        if (globaltimer_ns() - t0 > d.timeout_ns) {
+          st_release_sys(&d.hctl->error_info, 0x400 + q);
+          st_release_sys(&d.hctl->error, EC_DERR_TIMEOUT);
+          break;
+        }
+      }
+    }
+    fence_proxy_alias();
+  }
+  __syncthreads();
+  // 3. my shard: switch-reduced sum, / P, broadcast into every rank's slot
+  const bool pow2 = (P & (P - 1)) == 0;
+  const float inv = 1.0f / (float)P;
+  const long long off = (g % d.R) * d.slot_bytes;
+  const long long v0 = shard_lo(d.nvec, r, P), v1 = shard_lo(d.nvec, r + 1, P);
+  for (long long v = v0 + start; v < v1; v += stride) {
+    float4 s = mm_ld_reduce_v4(d.mc_stage + v * 16);
+    float4 u;
+    u.x = Ops<float>::divp(s.x, P, inv, pow2);
+    u.y = Ops<float>::divp(s.y, P, inv, pow2);
+    u.z = Ops<float>::divp(s.z, P, inv, pow2);
+    u.w = Ops<float>::divp(s.w, P, inv, pow2);
+    bad |= !(isfinite(u.x) && isfinite(u.y) && isfinite(u.z) && isfinite(u.w));
+    mm_st_v4(d.mc_ring + off + v * 16, u);
+  }
+  if (r == P - 1 && w == 0 && tid < 4) {
+    const long long e = d.nvec * 4 + tid;
+    if (e < d.n) {
+      const float u = Ops<float>::divp(mm_ld_reduce_f32(d.mc_stage + e * 4), P, inv, pow2);
+      bad |= !isfinite(u);
+      mm_st_f32(d.mc_ring + off + e * 4, u);
+    }
+  }
+  fence_proxy_alias();
+}
+
 template <typename T>
 __device__ void engine_worker(const EcDesc& d, int w, unsigned long long epoch) {
   EcLocal* L = d.local;
@@ -447,6 +541,8 @@ __device__ void engine_worker(const EcDesc& d, int w, unsigned long long epoch) 
     if (d.mode == 0) {
       round_tma<T>(d, sp, w, g, has, smem, full, it, bad);
       if (w == 0 && d.rank == d.P - 1) tail_push<T>(d, sp, has, g);
+    } else if (d.mode == 2) {
+      round_nvls<T>(d, sp, w, g, has, seen, bad);
     } else {
       round_ldg<T>(d, sp, w, g, has, seen);
     }
@@ -460,7 +556,7 @@ __device__ void engine_worker(const EcDesc& d, int w, unsigned long long epoch) 
         fence_acq_rel_sys();
         unsigned long long word = (unsigned long long)g + 1;
         if (atomicExch(&L->round_poison, 0u)) word |= EC_DONE_POISON;
-        if (d.mode == 0) {
+        if (d.mode != 1) {
           L->t_rs = globaltimer_ns();
           for (int q = 0; q < d.P; ++q) st_relaxed_sys(&d.ctrl[q]->done_from[d.rank], word);
         } else {
@@ -673,7 +769,7 @@ __device__ void engine_controller(const EcDesc& d, unsigned long long epoch) {
         // round complete at this rank: TMA mode needs every owner's pushes into
         // our slot, pull mode only our own all-gather
         unsigned long long poison = 0;
-        for (int q = (d.mode == 0 ? 0 : r); q < (d.mode == 0 ? P : r + 1) && !timed_out; ++q) {
+        for (int q = (d.mode != 1 ? 0 : r); q < (d.mode != 1 ? P : r + 1) && !timed_out; ++q) {
           unsigned long long wq;
           while (((wq = ld_acquire_sys(&C->done_from[q])) & ~EC_DONE_POISON) < (unsigned long long)g + 1) {
             if (globaltimer_ns() - t0 > d.timeout_ns) { timed_out = true; break; }
@@ -1290,6 +1386,7 @@ ec_update_gen_kernel(T* __restrict__ w, T* __restrict__ mom, const char* __restr
     }
     s_gen = *(volatile const long long*)&L->step_gen;
     s_late = H != nullptr ? *(volatile const int*)&L->step_late : 0;
+    asm volatile("fence.proxy.alias;" ::: "memory");  // slot may be written via a multicast alias
   }
   __syncthreads();
   const long long G = s_gen;

@@ -71,6 +71,7 @@ class Comm:
                  C.byref(self.ptr))
         self.running = False
         self.closed = False
+        self.nvls = False
         self.lock = threading.Lock()
         self._views: dict = {}
         self.replay_masks: dict = {}
@@ -328,9 +329,28 @@ class ProcessWorld(_WorldBase):
         blobs = self._all_gather(comm.export(0))
         for q, blob in enumerate(blobs):
             comm.import_peer(q, blob)
+        if (cfg.reduction_mode == "fast" and cfg.element == "f4" and self.p > 1
+                and all(self._all_gather(bool(lib.ec_nvls_supported(self.device))))):
+            self._setup_nvls(comm)
         self.comms[cid] = comm
         self.barrier()
         return comm, 0
+
+    def _setup_nvls(self, comm: "Comm") -> None:
+        """Multicast object over every rank's GPU (fabric handle shared over the
+        process group); see ec_nvls_create/attach/bind."""
+        blob = b""
+        if self.rank == 0:
+            buf = (C.c_char * 256)()
+            n = C.c_size_t()
+            call("ec_nvls_create", comm.ptr, buf, 256, C.byref(n))
+            blob = bytes(buf[: n.value])
+        blob = self._all_gather(blob)[0]
+        call("ec_nvls_attach", comm.ptr, blob, len(blob))
+        self.barrier()                       # every device added before any bind
+        call("ec_nvls_bind", comm.ptr)
+        comm.nvls = True
+        self.barrier()
 
     def pause(self, timeout_ms: int = 30000) -> None:
         # Every rank must have stopped posting before any engine parks, otherwise

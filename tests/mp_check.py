@@ -132,6 +132,34 @@ def main():
         h.close()
         assert st.w.cpu().numpy().tobytes() == w.tobytes()
 
+    def nvls_fast_mode():
+        """reduction_mode="fast": the NVSwitch reduces (when the fabric has
+        NVLS); same u on every rank, within fp32 rounding of the fixed-order sum."""
+        from paper_1908_04207_b200 import _lib as L
+        n = 2_000_003
+        rng = np.random.default_rng(77)
+        contrib = rng.standard_normal((world, n), dtype=np.float32)
+        want, inc, _ = R.allreduce_round(list(contrib), [True] * world, np.float32)
+        cfg = CollectiveConfig(p=world, flavor="solo", vector_len=n, element="f4",
+                               reduction_mode="fast")
+        h = AllreduceHandle(cfg, rank, pw, cid=next_cid())
+        vec = torch.as_tensor(contrib[rank], device="cuda")
+        us = []
+        for t in range(3):
+            h._contribute(t, vec, fresh=True, activate=True, all_arrive=True)
+            gen, res = h.wait_blocking(t)
+            assert gen == t and res.included == inc
+            us.append(res.u.cpu().numpy())
+        nv = h.comm.nvls
+        h.close()
+        rel = float(np.linalg.norm(us[0].astype(np.float64) - want) / np.linalg.norm(want))
+        assert rel < 1e-6, rel
+        digest = [hash(u.tobytes()) for u in us]
+        alld = [None] * world
+        dist.all_gather_object(alld, digest)
+        assert all(d == alld[0] for d in alld), "ranks disagree"
+        return {"nvls": nv, "rel_err_vs_fixed_order": rel}
+
     def replay_c1():
         if world != 4:
             return {"skipped": f"c1 traces have p=4, world={world}"}
@@ -179,6 +207,7 @@ def main():
     check("solo_first_arrival", solo_first_arrival)
     check("majority_prefix", majority_prefix)
     check("eager_sgd_all_arrive", eager_sgd_all_arrive)
+    check("nvls_fast_mode", nvls_fast_mode)
     check("replay_c1", replay_c1)
 
     gathered = [None] * world

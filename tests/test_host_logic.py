@@ -42,7 +42,7 @@ def test_abi_argument_errors_without_gpu():
 def test_collective_config_validation():
     CollectiveConfig(p=2, flavor="solo", vector_len=3)
     for kw in (dict(p=0), dict(flavor="x"), dict(vector_len=0), dict(element="f2"),
-               dict(p=65), dict(reduction_mode="fast")):
+               dict(p=65), dict(reduction_mode="fastest")):
         args = dict(p=2, flavor="solo", vector_len=3)
         args.update(kw)
         with pytest.raises(ValueError):
