@@ -338,17 +338,32 @@ class ProcessWorld(_WorldBase):
 
     def _setup_nvls(self, comm: "Comm") -> None:
         """Multicast object over every rank's GPU (fabric handle shared over the
-        process group); see ec_nvls_create/attach/bind."""
-        blob = b""
+        process group); see ec_nvls_create/attach/bind.  Any rank failing before
+        the bind leaves every rank on the fixed-order engine (a valid "fast")."""
+        import warnings
+        msg = (True, b"")
         if self.rank == 0:
-            buf = (C.c_char * 256)()
-            n = C.c_size_t()
-            call("ec_nvls_create", comm.ptr, buf, 256, C.byref(n))
-            blob = bytes(buf[: n.value])
-        blob = self._all_gather(blob)[0]
-        call("ec_nvls_attach", comm.ptr, blob, len(blob))
-        self.barrier()                       # every device added before any bind
-        call("ec_nvls_bind", comm.ptr)
+            try:
+                buf = (C.c_char * 256)()
+                n = C.c_size_t()
+                call("ec_nvls_create", comm.ptr, buf, 256, C.byref(n))
+                msg = (True, bytes(buf[: n.value]))
+            except Exception as e:  # noqa: BLE001 - reported below, collectively
+                msg = (False, str(e).encode())
+        ok, blob = self._all_gather(msg)[0]
+        if not ok:
+            warnings.warn(f"NVLS unavailable ({blob.decode()}); fast mode uses the fixed-order engine")
+            return
+        err = ""
+        try:
+            call("ec_nvls_attach", comm.ptr, blob, len(blob))
+        except Exception as e:  # noqa: BLE001
+            err = str(e)
+        errs = [x for x in self._all_gather(err) if x]
+        if errs:
+            warnings.warn(f"NVLS attach failed ({errs[0]}); fast mode uses the fixed-order engine")
+            return
+        call("ec_nvls_bind", comm.ptr)       # every device was added before any bind
         comm.nvls = True
         self.barrier()
 

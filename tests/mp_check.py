@@ -25,6 +25,10 @@ import torch.distributed as dist  # noqa: E402
 
 
 def main():
+    if os.environ.get("EC_DEBUG_DUMP"):
+        import faulthandler
+        faulthandler.dump_traceback_later(float(os.environ["EC_DEBUG_DUMP"]), exit=True)
+    only = os.environ.get("EC_ONLY")
     rank = int(os.environ["RANK"])
     world = int(os.environ["WORLD_SIZE"])
     local = int(os.environ.get("LOCAL_RANK", rank))
@@ -47,6 +51,8 @@ def main():
         return cid[0]
 
     def check(name, fn):
+        if only and name not in only.split(","):
+            return
         try:
             out = fn()
             results[name] = {"ok": True, **(out or {})}
