@@ -240,11 +240,19 @@ static size_t nvls_size(ec_comm_t* c, size_t gran) {
   return ((want + gran - 1) / gran) * gran;
 }
 
+// POSIX file descriptors (passed between the ranks' processes over a Unix
+// socket) work without IMEX channels; fabric handles are plain bytes but need them
+static CUmemAllocationHandleType nvls_handle_type() {
+  const char* e = getenv("EC_NVLS_HANDLE");
+  return (e && strcmp(e, "fabric") == 0) ? CU_MEM_HANDLE_TYPE_FABRIC
+                                         : CU_MEM_HANDLE_TYPE_POSIX_FILE_DESCRIPTOR;
+}
+
 static int nvls_prop(ec_comm_t* c, CUmulticastObjectProp* prop, size_t* gran) {
   DrvApi& D = drv();
   memset(prop, 0, sizeof(*prop));
   prop->numDevices = c->P;
-  prop->handleTypes = CU_MEM_HANDLE_TYPE_FABRIC;
+  prop->handleTypes = nvls_handle_type();
   prop->size = (size_t)c->slot_bytes * (1 + c->R);
   DRV(D.mcGran(gran, prop, CU_MULTICAST_GRANULARITY_MINIMUM));
   prop->size = nvls_size(c, *gran);
@@ -307,10 +315,17 @@ extern "C" int ec_nvls_create(ec_comm_t* c, void* blob, size_t cap, size_t* len)
   DRV(D.mcCreate(&c->mc_handle, &prop));
   c->mc_created = true;
   c->mc_size = prop.size;
-  CUmemFabricHandle fh;
-  DRV(D.exportH(&fh, c->mc_handle, CU_MEM_HANDLE_TYPE_FABRIC, 0));
-  memcpy(blob, &fh, sizeof(fh));
-  if (len) *len = sizeof(fh);
+  if (nvls_handle_type() == CU_MEM_HANDLE_TYPE_FABRIC) {
+    CUmemFabricHandle fh;
+    DRV(D.exportH(&fh, c->mc_handle, CU_MEM_HANDLE_TYPE_FABRIC, 0));
+    memcpy(blob, &fh, sizeof(fh));
+    if (len) *len = sizeof(fh);
+  } else {
+    int fd = -1;  // the caller passes this descriptor to the other ranks (SCM_RIGHTS)
+    DRV(D.exportH(&fd, c->mc_handle, CU_MEM_HANDLE_TYPE_POSIX_FILE_DESCRIPTOR, 0));
+    memcpy(blob, &fd, sizeof(fd));
+    if (len) *len = sizeof(fd);
+  }
   return EC_OK;
 }
 
@@ -320,10 +335,17 @@ extern "C" int ec_nvls_attach(ec_comm_t* c, const void* blob, size_t len) {
   if (!D.ok) return fail(EC_E_STATE, "driver multicast API unavailable");
   CK(cudaSetDevice(c->device));
   if (!c->mc_created) {
-    if (len < sizeof(CUmemFabricHandle)) return fail(EC_E_ARG, "blob too short");
-    CUmemFabricHandle fh;
-    memcpy(&fh, blob, sizeof(fh));
-    DRV(D.importH(&c->mc_handle, &fh, CU_MEM_HANDLE_TYPE_FABRIC));
+    if (nvls_handle_type() == CU_MEM_HANDLE_TYPE_FABRIC) {
+      if (len < sizeof(CUmemFabricHandle)) return fail(EC_E_ARG, "blob too short");
+      CUmemFabricHandle fh;
+      memcpy(&fh, blob, sizeof(fh));
+      DRV(D.importH(&c->mc_handle, &fh, CU_MEM_HANDLE_TYPE_FABRIC));
+    } else {
+      if (len < sizeof(int)) return fail(EC_E_ARG, "blob too short");
+      int fd;
+      memcpy(&fd, blob, sizeof(fd));  // a descriptor valid in THIS process
+      DRV(D.importH(&c->mc_handle, (void*)(uintptr_t)fd, CU_MEM_HANDLE_TYPE_POSIX_FILE_DESCRIPTOR));
+    }
     c->mc_attached = true;
     CUmulticastObjectProp prop;
     size_t gran = 0;
@@ -348,7 +370,7 @@ extern "C" int ec_nvls_bind(ec_comm_t* c) {
   p.type = CU_MEM_ALLOCATION_TYPE_PINNED;
   p.location.type = CU_MEM_LOCATION_TYPE_DEVICE;
   p.location.id = c->device;
-  p.requestedHandleTypes = CU_MEM_HANDLE_TYPE_FABRIC;
+  p.requestedHandleTypes = nvls_handle_type();
   DRV(D.memCreate(&c->mc_phys, c->mc_size, &p, 0));
   c->mc_phys_made = true;
   DRV(D.mcBindMem(c->mc_handle, 0, c->mc_phys, 0, c->mc_size, 0));

@@ -340,20 +340,57 @@ class ProcessWorld(_WorldBase):
         """Multicast object over every rank's GPU (fabric handle shared over the
         process group); see ec_nvls_create/attach/bind.  Any rank failing before
         the bind leaves every rank on the fixed-order engine (a valid "fast")."""
+        import os
+        import socket
+        import struct
+        import tempfile
         import warnings
+        fabric = os.environ.get("EC_NVLS_HANDLE") == "fabric"
+        path = os.path.join(tempfile.gettempdir(), f"ec_nvls_{os.getppid()}_{id(comm)}")
+        path = self._all_gather(path)[0]
         msg = (True, b"")
+        srv = None
         if self.rank == 0:
             try:
                 buf = (C.c_char * 256)()
                 n = C.c_size_t()
                 call("ec_nvls_create", comm.ptr, buf, 256, C.byref(n))
                 msg = (True, bytes(buf[: n.value]))
+                if not fabric:     # the descriptor travels over a Unix socket (SCM_RIGHTS)
+                    if os.path.exists(path):
+                        os.unlink(path)
+                    srv = socket.socket(socket.AF_UNIX, socket.SOCK_STREAM)
+                    srv.bind(path)
+                    srv.listen(self.p)
             except Exception as e:  # noqa: BLE001 - reported below, collectively
                 msg = (False, str(e).encode())
         ok, blob = self._all_gather(msg)[0]
         if not ok:
             warnings.warn(f"NVLS unavailable ({blob.decode()}); fast mode uses the fixed-order engine")
             return
+        if not fabric:
+            if self.rank == 0:
+                fd = struct.unpack("i", blob[:4])[0]
+                for _ in range(self.p - 1):
+                    conn, _ = srv.accept()
+                    socket.send_fds(conn, [b"x"], [fd])
+                    conn.close()
+            else:
+                cli = socket.socket(socket.AF_UNIX, socket.SOCK_STREAM)
+                for _ in range(200):
+                    try:
+                        cli.connect(path)
+                        break
+                    except OSError:
+                        import time
+                        time.sleep(0.05)
+                _, fds, _, _ = socket.recv_fds(cli, 16, 1)
+                cli.close()
+                blob = struct.pack("i", fds[0])
+            self.barrier()
+            if srv is not None:
+                srv.close()
+                os.unlink(path)
         err = ""
         try:
             call("ec_nvls_attach", comm.ptr, blob, len(blob))

@@ -59,6 +59,8 @@ def main():
         except Exception as e:
             results[name] = {"ok": False, "error": f"{type(e).__name__}: {e}",
                              "tb": traceback.format_exc()[-1500:]}
+            print(f"rank {rank} check {name} FAILED: {e}\n{traceback.format_exc()[-1500:]}",
+                  flush=True)
         dist.barrier()
 
     golden = np.load(os.path.join(ROOT, "tests", "golden", "tree_sums.npz"))
