@@ -8,6 +8,7 @@ prints one JSON object with every check's outcome; the exit code is non-zero
 if any check failed on any rank.  Driven by tests/test_multigpu.py.
 """
 
+import hashlib
 import json
 import os
 import sys
@@ -162,7 +163,7 @@ def main():
         h.close()
         rel = float(np.linalg.norm(us[0].astype(np.float64) - want) / np.linalg.norm(want))
         assert rel < 1e-6, rel
-        digest = [hash(u.tobytes()) for u in us]
+        digest = [hashlib.sha1(u.tobytes()).hexdigest() for u in us]
         alld = [None] * world
         dist.all_gather_object(alld, digest)
         assert all(d == alld[0] for d in alld), "ranks disagree"
