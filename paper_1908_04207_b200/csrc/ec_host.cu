@@ -129,6 +129,7 @@ struct BlobV1 {
 
 struct ec_comm {
   int P = 0, rank_lo = 0, n_local = 0, device = 0, dtype = 0, flavor = 0, R = 2, W = 0;
+  bool W_default = true;
   long long n = 0, slot_bytes = 0;
   int elem = 4;
   unsigned long long timeout_ns = 60ull * 1000000000ull;
@@ -394,6 +395,9 @@ extern "C" int ec_nvls_bind(ec_comm_t* c) {
   r->ring = (char*)c->uc_va + c->slot_bytes;
   c->ring[c->rank_lo] = r->ring;
   c->mode = 2;
+  // the switch round trip is long: the NVLS data phase wants more CTAs
+  // (measured P=4, 1 GiB: W=64 363 GB/s, W=128 558, W=144 561 busbw)
+  if (c->W_default && c->n_local == 1) c->W = 128;
   return EC_OK;
 }
 
@@ -432,6 +436,7 @@ int ec_comm_create(int world_size, int rank_lo, int n_local, int device, int64_t
     const char* env = getenv("EC_WORKERS");
     workers_per_rank = env ? atoi(env) : 0;
   }
+  const bool w_default = workers_per_rank <= 0;
   if (workers_per_rank <= 0) {
     const bool ldg = getenv("EC_DATA") && strcmp(getenv("EC_DATA"), "ldg") == 0;
     if (n_local == 1) {
@@ -442,6 +447,7 @@ int ec_comm_create(int world_size, int rank_lo, int n_local, int device, int64_t
       if (workers_per_rank < 1) workers_per_rank = 1;
     }
   }
+  c->W_default = w_default;
   c->W = workers_per_rank;
   c->direct = world_size == 1 && !getenv("EC_FORCE_ENGINE");
   // Data phase: fused TMA (default) or two-phase ld.cg pull (EC_DATA=ldg).

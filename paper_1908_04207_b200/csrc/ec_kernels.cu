@@ -435,8 +435,20 @@ __device__ void round_nvls(const EcDesc& d, const char* const* sp, int w, long l
   // 1. stage my offer (or zeros for a null snapshot) into my copy of the region
   const bool mine = (has >> r) & 1ull;
   const char* src = sp[r];
-  for (long long v = start; v < d.nvec; v += stride)
-    st_v4(d.uc_stage + v * 16, mine ? ld_stream_v4(src + v * 16) : make_uint4(0, 0, 0, 0));
+  {
+    long long v = start;
+    if (mine) {
+      for (; v + 3 * stride < d.nvec; v += 4 * stride) {
+        uint4 x[4];
+#pragma unroll
+        for (int k = 0; k < 4; ++k) x[k] = ld_stream_v4(src + (v + k * stride) * 16);
+#pragma unroll
+        for (int k = 0; k < 4; ++k) st_v4(d.uc_stage + (v + k * stride) * 16, x[k]);
+      }
+    }
+    for (; v < d.nvec; v += stride)
+      st_v4(d.uc_stage + v * 16, mine ? ld_stream_v4(src + v * 16) : make_uint4(0, 0, 0, 0));
+  }
   if (w == 0 && tid < 4) {
     const long long e = d.nvec * 4 + tid;
     if (e < d.n) reinterpret_cast<float*>(d.uc_stage)[e] = mine ? reinterpret_cast<const float*>(src)[e] : 0.0f;
@@ -461,6 +473,7 @@ __device__ void round_nvls(const EcDesc& d, const char* const* sp, int w, long l
       }
     }
     fence_proxy_alias();
+    if (w == 0) L->t_rs = globaltimer_ns();   // staged everywhere (timeline stamp)
   }
   __syncthreads();
   // 3. my shard: switch-reduced sum, / P, broadcast into every rank's slot
@@ -468,7 +481,26 @@ __device__ void round_nvls(const EcDesc& d, const char* const* sp, int w, long l
   const float inv = 1.0f / (float)P;
   const long long off = (g % d.R) * d.slot_bytes;
   const long long v0 = shard_lo(d.nvec, r, P), v1 = shard_lo(d.nvec, r + 1, P);
-  for (long long v = v0 + start; v < v1; v += stride) {
+  // NVLS_U switch reductions in flight per thread before their broadcasts:
+  // the switch round trip is long, so memory-level parallelism sets the rate
+  constexpr int NVLS_U = 8;
+  long long v = v0 + start;
+  for (; v + (NVLS_U - 1) * stride < v1; v += NVLS_U * stride) {
+    float4 s[NVLS_U];
+#pragma unroll
+    for (int k = 0; k < NVLS_U; ++k) s[k] = mm_ld_reduce_v4(d.mc_stage + (v + k * stride) * 16);
+#pragma unroll
+    for (int k = 0; k < NVLS_U; ++k) {
+      float4 u;
+      u.x = Ops<float>::divp(s[k].x, P, inv, pow2);
+      u.y = Ops<float>::divp(s[k].y, P, inv, pow2);
+      u.z = Ops<float>::divp(s[k].z, P, inv, pow2);
+      u.w = Ops<float>::divp(s[k].w, P, inv, pow2);
+      bad |= !(isfinite(u.x) && isfinite(u.y) && isfinite(u.z) && isfinite(u.w));
+      mm_st_v4(d.mc_ring + off + (v + k * stride) * 16, u);
+    }
+  }
+  for (; v < v1; v += stride) {
     float4 s = mm_ld_reduce_v4(d.mc_stage + v * 16);
     float4 u;
     u.x = Ops<float>::divp(s.x, P, inv, pow2);
@@ -557,7 +589,7 @@ __device__ void engine_worker(const EcDesc& d, int w, unsigned long long epoch) 
         unsigned long long word = (unsigned long long)g + 1;
         if (atomicExch(&L->round_poison, 0u)) word |= EC_DONE_POISON;
         if (d.mode != 1) {
-          L->t_rs = globaltimer_ns();
+          if (d.mode == 0) L->t_rs = globaltimer_ns();
           for (int q = 0; q < d.P; ++q) st_relaxed_sys(&d.ctrl[q]->done_from[d.rank], word);
         } else {
           st_release_sys(&d.ctrl[d.rank]->done_from[d.rank], word);

@@ -90,7 +90,7 @@ def rounds_back_to_back(h, t0, k, all_arrive=True):
 
 
 def allreduce_sweep(world, rank, p, sizes_bytes, flavor="solo", rounds_cap=50, workers=None,
-                    max_over_ranks=lambda x: x, barrier=lambda: None):
+                    max_over_ranks=lambda x: x, barrier=lambda: None, reduction_mode="fixed_order"):
     """Bus bandwidth of the partial allreduce per payload size (fp32)."""
     import torch
 
@@ -102,7 +102,8 @@ def allreduce_sweep(world, rank, p, sizes_bytes, flavor="solo", rounds_cap=50, w
         cid += 1
         if workers is not None:
             world.workers = workers
-        cfg = CollectiveConfig(p=p, flavor=flavor, vector_len=n, element="f4", seed=1234)
+        cfg = CollectiveConfig(p=p, flavor=flavor, vector_len=n, element="f4", seed=1234,
+                               reduction_mode=reduction_mode)
         h = AllreduceHandle(cfg, rank, world, cid=cid)
         h.send_buffer().normal_()
         rounds = int(max(5, min(rounds_cap, (2 << 30) // max(1, 4 * n))))
@@ -134,7 +135,8 @@ def allreduce_sweep(world, rank, p, sizes_bytes, flavor="solo", rounds_cap=50, w
                     "busbw_device_gbs": bus / (data_us * 1e-6) / 1e9 if data_us > 0 else None,
                     "snap_to_start_us": max_over_ranks(snap_wait_us),
                     "done_to_next_snap_us": max_over_ranks(turnaround_us),
-                    "workers": h.comm.world.workers if workers is None else workers})
+                    "workers": h.comm.world.workers if workers is None else workers,
+                    "nvls": bool(getattr(h.comm, "nvls", False))})
         h.close()
     return out
 
@@ -310,6 +312,7 @@ def _main(argv=None):
     ap.add_argument("--rounds", type=int, default=64)
     ap.add_argument("--delay", default="linear_skew:1.0")
     ap.add_argument("--epochs", type=int, default=48)
+    ap.add_argument("--reduction-mode", default="fixed_order", choices=("fixed_order", "fast"))
     args = ap.parse_args(argv)
     if os.environ.get("EC_DEBUG_DUMP"):
         import faulthandler
@@ -350,7 +353,7 @@ def _main(argv=None):
                         try:
                             result[key] = allreduce_sweep(
                                 world, rank, p, sizes, f, workers=w, max_over_ranks=max_over,
-                                barrier=world.barrier)
+                                barrier=world.barrier, reduction_mode=args.reduction_mode)
                         except Exception as e:  # a geometry that cannot launch
                             result[key] = {"error": str(e)[:200]}
                             for cid in [c for c in world.comms if c >= 1000]:
