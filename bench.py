@@ -236,18 +236,22 @@ def main():
         from collections import deque
         pend = deque()
         upd_ns = []
+        v = C.c_uint64()
 
         def fin(p):
+            t0 = time.perf_counter()
             out = finish_step(st, h, p)
-            v = C.c_uint64()
             _lib.lib.ec_step_update_ns(h.comm.ptr, h.li, C.byref(v))
             upd_ns.append(v.value)
+            host_t[1] += time.perf_counter() - t0
             return out
 
         for i in range(k):
             if pre is not None:
                 pre(i)
+            t0 = time.perf_counter()
             pend.append(train_step_async(st, h, grad_fn(st.t), all_arrive=all_arrive))
+            host_t[0] += time.perf_counter() - t0
             if len(pend) > args.lag:
                 _, res, _g = fin(pend.popleft())
                 if naps is not None:
@@ -261,9 +265,10 @@ def main():
         return upd_ns
 
     # ---- main timed loop: inputs resident in HBM (working set >> 126 MB L2)
+    host_t = [0.0, 0.0]       # host seconds in train_step_async (issue) / finish_step
     run_steps(args.warmup, lambda t: grads[t % 2])
     quiesce()
-    _lib.lib.ec_profile_enable(1)
+    host_t = [0.0, 0.0]
     launches0 = _lib.lib.ec_launch_count()
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     naps = []
@@ -274,21 +279,36 @@ def main():
         host_ms = (time.perf_counter() - h0) * 1e3
         ev1.synchronize()
     launches = _lib.lib.ec_launch_count() - launches0
-    _lib.lib.ec_profile_enable(0)
-    prof_ms, prof_n = (C.c_double * 2)(), (C.c_int64 * 2)()
-    _lib.lib.ec_profile_read(prof_ms, prof_n)
+    host_issue_us, host_finish_us = (x / args.steps * 1e6 for x in host_t)
     ms = ev0.elapsed_time(ev1)
     timeline = device_timeline(h, st.t, args.steps, max_over_ranks) if world > 1 else None
     quiesce()
     ms_max = max_over_ranks(ms)
     value = world * args.steps / (ms_max / 1e3)
 
-    fold_ms = prof_ms[0] / max(1, prof_n[0])      # CUDA events around each launch, timed region
+    # per-launch CUDA events (fold launches, engine mode) in a separate, untimed
+    # run: events between launches perturb the step they measure
+    fold_ms = 0.0
+    if world > 1:
+        _lib.lib.ec_profile_enable(1)
+        run_steps(min(args.steps, 20), lambda t: grads[t % 2])
+        _lib.lib.ec_profile_enable(0)
+        prof_ms, prof_n = (C.c_double * 2)(), (C.c_int64 * 2)()
+        _lib.lib.ec_profile_read(prof_ms, prof_n)
+        fold_ms = prof_ms[0] / max(1, prof_n[0])
+        quiesce()
     # the update launch also waits on the device for the round (fused wait+update+unpin):
     # its compute time is the kernel's own %globaltimer stamp, averaged over the region
     upd_ms = sum(upd_ns) / max(1, len(upd_ns)) / 1e6
     peak, peak_kind = _peaks()
-    upd_gbs = 12 * n / (upd_ms / 1e3) / 1e9
+    # world of one: decide + round + update are ONE launch (ec_direct_step_kernel:
+    # reads the gradient and w, writes the slot u and w = 16 B/element); with
+    # peers the round runs in the engine and the update reads u from the slot
+    # (ec_update_gen_kernel: reads u and w, writes w = 12 B/element)
+    direct = world == 1
+    upd_kernel = "ec_direct_step_kernel<float>" if direct else "ec_update_gen_kernel<float>"
+    upd_bytes = (16 if direct else 12) * n
+    upd_gbs = upd_bytes / (upd_ms / 1e3) / 1e9
 
     # ---- e2e: gradient from pinned host memory every step, result read back
     host_grad = torch.randn(n, generator=torch.Generator().manual_seed(7 + rank)).pin_memory()
@@ -336,22 +356,26 @@ def main():
                        "mean_nap": float(np.mean(naps))},
             "e2e": {"value": e2e_value, "unit": "steps/s", "h2d_bytes_per_step": 4 * n,
                     "d2h_bytes_per_step": 16},
-            "roofline": {"bound": "hbm", "kernel": "ec_update_gen_kernel<float>",
+            "roofline": {"bound": "hbm", "kernel": upd_kernel,
                          "achieved": upd_gbs, "peak": peak, "unit": "GB/s",
-                         "frac": upd_gbs / peak, "traffic": _traffic("update"),
-                         "bytes_per_launch": 12 * n, "avg_launch_ms": upd_ms,
+                         "frac": upd_gbs / peak,
+                         "traffic": _traffic("direct_step" if direct else "update"),
+                         "bytes_per_launch": upd_bytes, "avg_launch_ms": upd_ms,
                          "peak_source": peak_kind},
             "local_kernels": {
                 "fold": {"zero_copy": True,
-                         "note": "the gradient is offered in place from the registered bucket "
-                                 "while the stash is null; the fold launch only posts the offer",
-                         "avg_launch_ms": fold_ms,
-                         "ncu_fold_into_null_stash": _ncu("fold")},
-                "update": {"bytes_per_launch": 12 * n, "avg_launch_ms": upd_ms, "gbs": upd_gbs,
-                           "frac": upd_gbs / peak},
+                         "note": ("world of one: no fold launch -- the step kernel offers the "
+                                  "registered bucket in place" if direct else
+                                  "the gradient is offered in place from the registered bucket "
+                                  "while the stash is null; the fold launch only posts the offer"),
+                         "avg_launch_ms": fold_ms if not direct else None},
+                "update" if not direct else "round_and_update": {
+                    "kernel": upd_kernel, "bytes_per_launch": upd_bytes, "avg_launch_ms": upd_ms,
+                    "gbs": upd_gbs, "frac": upd_gbs / peak},
             },
             "timeline_us": timeline,
             "host_ms_per_step": host_ms / args.steps,
+            "host_us_per_step": {"issue": host_issue_us, "finish_incl_wait": host_finish_us},
             "cpu_baseline": cpu,
             "clocks": clk.summary(),
             "gpu_launches": int(launches),

@@ -106,6 +106,10 @@ struct alignas(128) EcLocal {
   unsigned int upd_bad;            // the async step's update read a non-finite u
   unsigned long long pin_dev;      // device-side pin (async steps): lowest gen still read
   unsigned long long stage_count;  // NVLS: CTAs that staged this round (monotone)
+  unsigned long long dec_tag;      // direct step: seq + 1 once block 0 decided the step's offer
+  unsigned long long dec_status;   // direct step: the decision's reply status
+  int dec_fold;                    // direct step: fold the gradient into the stash in-pass
+  int pad6;
   EcReq dreq[EC_REQ_RING];         // stream-posted requests (device copy of the ring)
 };
 

@@ -42,6 +42,11 @@ cudaError_t launch_update_gen(int dtype, void* w, void* mom, const char* ring, l
                               long long t, unsigned long long timeout_ns, unsigned long long seq1,
                               void* stash, const void* gbuf, cudaStream_t s);
 cudaError_t launch_write_u64(unsigned long long* p, unsigned long long v, cudaStream_t s);
+cudaError_t launch_direct_step(int dtype, const EcDesc* d_desc, unsigned long long seq,
+                               unsigned int flags, void* w, void* mom, const void* ring,
+                               long long slot_bytes, const void* src0, const void* src1,
+                               double lr, double mu, long long n, long long t,
+                               unsigned long long timeout_ns, cudaStream_t s);
 cudaError_t launch_direct(int dtype, const EcDesc* d_desc, long long nvec, unsigned long long seq,
                           unsigned int type, unsigned int flags, long long t, long long arg,
                           cudaStream_t s);
@@ -1071,18 +1076,25 @@ int ec_step_async(ec_comm_t* c, int li, int64_t t, const void* grad, uint32_t fl
     std::lock_guard<std::mutex> g(r->mu);
     if ((rc = reserve_seq(c, r, &seq))) return rc;
   }
-  {
-    // fold (+ the offer's post, fused into the fold's last CTA, engine mode)
+  const bool zero_copy = grad == r->gbuf;
+  if (!(c->direct && zero_copy)) {
+    // fold (+ the offer's post, fused into the fold's last CTA, engine mode).
+    // A world of one offering its registered buffer needs no fold launch: the
+    // step kernel offers it in place, or folds it into a pending stash in-pass
     ProfScope ps(0, stream);
     CK(launch_fold_auto(c->dtype, r->send, grad, c->n, r->local, c->direct ? 0 : seq + 1,
-                        flags & 7u, t, grad == r->gbuf ? 1 : 0, s));
+                        flags & 7u, t, zero_copy ? 1 : 0, s));
   }
   if (c->direct) {
-    // the decide kernel learns from the fold whether the gradient buffer is
-    // offered in place: flag it when the caller passed the registered buffer
+    // decide + round + update in one launch (see ec_direct_step_kernel)
     c->last_stream = stream;
-    CK(launch_direct(c->dtype, c->d_descs + li, c->n / (16 / c->elem), seq, EC_REQ_CONTRIB,
-                     (flags & 7u) | (grad == r->gbuf ? EC_CF_SRC_GRAD_AUTO : 0u), t, 0, s));
+    ProfScope ps(1, stream);
+    CK(launch_direct_step(c->dtype, c->d_descs + li, seq,
+                          (flags & 7u) | (grad == r->gbuf ? EC_CF_SRC_GRAD_AUTO : 0u), w,
+                          (mom && mu != 0.0) ? mom : nullptr, r->ring, c->slot_bytes, r->send,
+                          r->gbuf, lr, mu, c->n, t, c->timeout_ns, s));
+    if (seq_out) *seq_out = seq;
+    return EC_OK;
   }
   {
     // device wait for a generation >= t + pin, update, unpin: one launch

@@ -893,10 +893,10 @@ template __global__ void ec_engine<long long>(const EcDesc*, int, unsigned long 
 // whole step is profilable with ncu.  Same state words, replies and log as the
 // engine (EcLocal / EcHostCtl), so the host API cannot tell the difference.
 
-__global__ void ec_direct_decide(const EcDesc* __restrict__ dp, unsigned long long seq,
-                                 unsigned int type, unsigned int flags, long long t, long long arg) {
-  if (threadIdx.x != 0) return;
-  const EcDesc& d = *dp;
+// decide one request against the device state (no host-visible stores);
+// returns the reply status (EC_R_*)
+__device__ unsigned long long direct_decide_core(const EcDesc& d, unsigned int type,
+                                                 unsigned int flags, long long t, long long arg) {
   EcLocal* L = d.local;
   EcHostCtl* H = d.hctl;
   const long long g = L->g;
@@ -930,11 +930,26 @@ __global__ void ec_direct_decide(const EcDesc* __restrict__ dp, unsigned long lo
   } else if (type == EC_REQ_HOLD) {
     L->hold_from = arg;
   }
+  return status;
+}
+
+__device__ void direct_reply(const EcDesc& d, unsigned long long seq, unsigned long long status) {
+  EcLocal* L = d.local;
+  EcHostCtl* H = d.hctl;
   __threadfence();
   st_release_sys(&H->reply[seq % EC_REQ_RING], ((seq + 1) << 8) | status);
   st_release_sys(&H->req_done, seq + 1);
   st_release_gpu(&L->req_done_dev, seq + 1);
 }
+
+__global__ void ec_direct_decide(const EcDesc* __restrict__ dp, unsigned long long seq,
+                                 unsigned int type, unsigned int flags, long long t, long long arg) {
+  if (threadIdx.x == 0) direct_reply(*dp, seq, direct_decide_core(*dp, type, flags, t, arg));
+}
+
+struct DirectStepReport;
+__device__ void direct_publish(const EcDesc& d, long long g, int contrib, unsigned long long has,
+                               const DirectStepReport* step);
 
 template <typename T>
 __global__ void __launch_bounds__(256, 6)
@@ -957,30 +972,59 @@ ec_direct_round(const EcDesc* __restrict__ dp) {
     const unsigned long long old = atomicAdd(&L->rs_count, 1ull);
     if (old + 1 == gridDim.x) {
       L->rs_count = 0;
-      EcHostCtl* H = d.hctl;
-      const unsigned long long fresh = (contrib & (int)EC_SNAP_FRESH) ? 1ull : 0ull;
-      EcLog* lg = &H->log[g % EC_LOG_RING];
-      st_relaxed_sys(&lg->mask, fresh);
-      st_relaxed_sys(&lg->has, has);
-      st_relaxed_sys(&lg->nap, fresh);
-      const unsigned long long tn = globaltimer_ns();
-      st_relaxed_sys(&lg->t_snap, tn);
-      st_relaxed_sys(&lg->t_cmd, tn);
-      st_relaxed_sys(&lg->t_rs, tn);
-      st_relaxed_sys(&lg->t_done, tn);
-      st_release_sys(&lg->gen1, (unsigned long long)g + 1);
-      if (fresh) {
-        L->hold_from = EC_INF_GEN;
-        L->stash_null = 1;
-      }
-      L->g = g + 1;
-      L->snapped = 0;
-      L->contrib = 0;
-      __threadfence();
-      st_release_sys(&H->snap_gen1, (unsigned long long)g + 1);
-      st_release_sys(&H->done_gen1, (unsigned long long)g + 1);
-      st_release_gpu(&L->done_gen1_dev, (unsigned long long)g + 1);
+      direct_publish(d, g, contrib, has, nullptr);
     }
+  }
+}
+
+// the last CTA of a direct round: log, stash/hold state, next generation.
+// Every host-visible word is a plain store ordered by ONE sys fence before the
+// flags the host polls (a release per word would drain PCIe once per word).
+// With step != nullptr it also reports the fused step (ec_direct_step_kernel):
+// the request's reply and the step's generation / finiteness / time.
+struct DirectStepReport {
+  unsigned long long seq, status, t0;
+  long long t;
+  bool bad;
+};
+
+__device__ void direct_publish(const EcDesc& d, long long g, int contrib, unsigned long long has,
+                               const DirectStepReport* step = nullptr) {
+  EcLocal* L = d.local;
+  EcHostCtl* H = d.hctl;
+  const unsigned long long fresh = (contrib & (int)EC_SNAP_FRESH) ? 1ull : 0ull;
+  EcLog* lg = &H->log[g % EC_LOG_RING];
+  st_relaxed_sys(&lg->mask, fresh);
+  st_relaxed_sys(&lg->has, has);
+  st_relaxed_sys(&lg->nap, fresh);
+  const unsigned long long tn = globaltimer_ns();
+  st_relaxed_sys(&lg->t_snap, tn);
+  st_relaxed_sys(&lg->t_cmd, tn);
+  st_relaxed_sys(&lg->t_rs, tn);
+  st_relaxed_sys(&lg->t_done, tn);
+  if (fresh) {
+    L->hold_from = EC_INF_GEN;
+    L->stash_null = 1;
+  }
+  L->g = g + 1;
+  L->snapped = 0;
+  L->contrib = 0;
+  if (step) {
+    const long long ts = step->t % EC_REQ_RING;
+    st_relaxed_sys(&H->stepgen[ts], (unsigned long long)g + 1);
+    st_relaxed_sys(&H->stepbad[ts], step->bad ? 1ull : 0ull);
+    st_relaxed_sys(&H->stepns[ts], tn - step->t0);
+  }
+  fence_acq_rel_sys();
+  st_relaxed_sys(&lg->gen1, (unsigned long long)g + 1);
+  st_relaxed_sys(&H->snap_gen1, (unsigned long long)g + 1);
+  st_relaxed_sys(&H->done_gen1, (unsigned long long)g + 1);
+  st_relaxed_gpu(&L->done_gen1_dev, (unsigned long long)g + 1);
+  if (step) {
+    st_relaxed_sys(&H->reply[step->seq % EC_REQ_RING], ((step->seq + 1) << 8) | step->status);
+    st_relaxed_sys(&H->req_done, step->seq + 1);
+    st_relaxed_gpu(&L->req_done_dev, step->seq + 1);
+    st_relaxed_sys(&H->steptag[step->t % EC_REQ_RING], (unsigned long long)step->t + 1);
   }
 }
 
@@ -1403,12 +1447,12 @@ __device__ __forceinline__ bool update_body(T* __restrict__ w, T* __restrict__ m
 // also performs the wait (block 0) and the last CTA releases the pin
 // (fused wait + update + unpin: one launch)
 template <typename T, bool MOM>
-__global__ void __launch_bounds__(256, 4)
-ec_update_gen_kernel(T* __restrict__ w, T* __restrict__ mom, const char* __restrict__ ring,
-                     long long slot_bytes, int R, EcLocal* __restrict__ L, T lr, T mu,
-                     long long n, int vec_ok, EcHostCtl* H, long long t,
-                     unsigned long long timeout_ns, unsigned long long seq1,
-                     T* __restrict__ stash, const T* __restrict__ gbuf) {
+__device__ __forceinline__ void update_gen_body(T* __restrict__ w, T* __restrict__ mom,
+                                                const char* __restrict__ ring, long long slot_bytes,
+                                                int R, EcLocal* __restrict__ L, T lr, T mu,
+                                                long long n, int vec_ok, EcHostCtl* H, long long t,
+                                                unsigned long long timeout_ns, unsigned long long seq1,
+                                                T* __restrict__ stash, const T* __restrict__ gbuf) {
   __shared__ long long s_gen;
   __shared__ int s_late;
   if (threadIdx.x == 0) {
@@ -1443,6 +1487,182 @@ ec_update_gen_kernel(T* __restrict__ w, T* __restrict__ mom, const char* __restr
       st_release_gpu(&L->pin_dev, ~0ull);  // every CTA has read the slot: unpin
       st_relaxed_sys(&H->stepns[t % EC_REQ_RING], t1 - *(volatile unsigned long long*)&L->upd_t0);
       st_release_sys(&H->steptag[t % EC_REQ_RING], (unsigned long long)t + 1);
+    }
+  }
+}
+
+template <typename T, bool MOM>
+__global__ void __launch_bounds__(256, 4)
+ec_update_gen_kernel(T* __restrict__ w, T* __restrict__ mom, const char* __restrict__ ring,
+                     long long slot_bytes, int R, EcLocal* __restrict__ L, T lr, T mu,
+                     long long n, int vec_ok, EcHostCtl* H, long long t,
+                     unsigned long long timeout_ns, unsigned long long seq1,
+                     T* __restrict__ stash, const T* __restrict__ gbuf) {
+  update_gen_body<T, MOM>(w, mom, ring, slot_bytes, R, L, lr, mu, n, vec_ok, H, t, timeout_ns, seq1,
+                          stash, gbuf);
+}
+
+// Direct mode (world of one) async step: decide the step's offer (block 0;
+// the other CTAs wait for its device-state decision, dec_tag), then -- when it
+// opened round t, the common case -- ONE pass per element: u = (0 + x) / 1
+// into the slot and w -= lr*u (or the momentum form) from the register copy of
+// u, so the update never re-reads the slot.  x is the registered gradient
+// buffer (zero-copy offer, null stash), the stash (folded by ec_fold_auto), or
+// -- FOLD, a zero-copy call that met a non-null stash -- stash + g, folded in
+// this same pass.  Bit-identical to fold + decide + round + update as separate
+// launches (same expressions, same order).  Host-visible stores (reply, log,
+// step report) are all made by the last CTA behind one sys fence.  Anything
+// else (a refused offer, no activation) runs the ordinary wait + update body.
+template <typename T, bool MOM, bool FOLD>
+__device__ __forceinline__ bool direct_pass(const T* __restrict__ src, const T* __restrict__ g2,
+                                            T* __restrict__ stash, T* __restrict__ slot,
+                                            T* __restrict__ w, T* __restrict__ mom, T lr, T mu,
+                                            long long n, int vec_ok, bool has) {
+  constexpr int V = Ops<T>::V;
+  constexpr int U = (MOM || FOLD) ? 2 : 4;
+  const long long tid = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  const long long nth = (long long)gridDim.x * blockDim.x;
+  bool bad = false;
+  auto reduce1 = [&](T x) -> T {   // rs_fixed<T, 1>: tree of one canonical leaf, / 1
+    T c[1] = {Ops<T>::canon(x)};
+    return Ops<T>::divp(tree_sum<T, 1>(c), 1, (T)1, true);
+  };
+  long long done = 0;
+  if (vec_ok) {
+    const long long nv = n / V;
+    for (long long base = tid; base < nv; base += nth * U) {
+      Vec16<T> xv[U], wv[U], bv[MOM ? U : 1], gv[FOLD ? U : 1];
+#pragma unroll
+      for (int k = 0; k < U; ++k) {
+        const long long v = base + k * nth;
+        if (v < nv) {
+          xv[k].raw = has ? ld_stream_v4(src + v * V) : make_uint4(0, 0, 0, 0);
+          if (FOLD) gv[FOLD ? k : 0].raw = ld_stream_v4(g2 + v * V);
+          wv[k].raw = ld_stream_v4(w + v * V);
+          if (MOM) bv[MOM ? k : 0].raw = ld_stream_v4(mom + v * V);
+        }
+      }
+#pragma unroll
+      for (int k = 0; k < U; ++k) {
+        const long long v = base + k * nth;
+        if (v < nv) {
+          if (FOLD) {
+#pragma unroll
+            for (int l = 0; l < V; ++l) xv[k].e[l] = Ops<T>::add(xv[k].e[l], gv[FOLD ? k : 0].e[l]);
+            st_v4(stash + v * V, xv[k].raw);
+          }
+          Vec16<T> uv;
+#pragma unroll
+          for (int l = 0; l < V; ++l) {
+            uv.e[l] = reduce1(xv[k].e[l]);
+            bad |= !Ops<T>::finite(uv.e[l]);
+            if (MOM) {
+              bv[MOM ? k : 0].e[l] = Ops<T>::mom(mu, bv[MOM ? k : 0].e[l], uv.e[l]);
+              wv[k].e[l] = Ops<T>::sgd(wv[k].e[l], lr, bv[MOM ? k : 0].e[l]);
+            } else {
+              wv[k].e[l] = Ops<T>::sgd(wv[k].e[l], lr, uv.e[l]);
+            }
+          }
+          st_v4(slot + v * V, uv.raw);
+          if (MOM) st_v4(mom + v * V, bv[MOM ? k : 0].raw);
+          st_v4(w + v * V, wv[k].raw);
+        }
+      }
+    }
+    done = nv * V;
+  }
+  for (long long e = done + tid; e < n; e += nth) {
+    T x = has ? src[e] : Ops<T>::zero();
+    if (FOLD) {
+      x = Ops<T>::add(x, g2[e]);
+      stash[e] = x;
+    }
+    T uu = reduce1(x);
+    slot[e] = uu;
+    bad |= !Ops<T>::finite(uu);
+    if (MOM) {
+      T b = Ops<T>::mom(mu, mom[e], uu);
+      mom[e] = b;
+      uu = b;
+    }
+    w[e] = Ops<T>::sgd(w[e], lr, uu);
+  }
+  return bad;
+}
+
+template <typename T, bool MOM>
+__global__ void __launch_bounds__(256, 3)
+ec_direct_step_kernel(const EcDesc* __restrict__ dp, unsigned long long seq, unsigned int flags,
+                      T* __restrict__ w, T* __restrict__ mom, T lr, T mu, int vec_ok, long long t,
+                      unsigned long long timeout_ns) {
+  const EcDesc& d = *dp;
+  EcLocal* L = d.local;
+  EcHostCtl* H = d.hctl;
+  __shared__ int s_fused, s_contrib, s_fold;
+  __shared__ long long s_g;
+  __shared__ unsigned long long s_status, s_t0;
+  // launched with programmatic stream serialization: this grid may become
+  // resident while the previous step's grid drains; nothing it wrote may be
+  // read before this wait
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+  if (threadIdx.x == 0) {
+    if (blockIdx.x == 0) {
+      const unsigned long long t0 = globaltimer_ns();
+      // a zero-copy call that meets a pending stash folds into it in this pass
+      const int fold = (flags & EC_CF_SRC_GRAD_AUTO) && !*(volatile int*)&L->stash_null;
+      const unsigned long long status = direct_decide_core(d, EC_REQ_CONTRIB, flags, t, 0);
+      L->dec_status = status;
+      L->dec_fold = fold;
+      L->upd_t0 = t0;
+      __threadfence();
+      st_release_gpu(&L->dec_tag, seq + 1);
+    } else {
+      while (ld_acquire_gpu(&L->dec_tag) != seq + 1) __nanosleep(64);
+    }
+    s_g = *(volatile long long*)&L->g;
+    s_contrib = *(volatile int*)&L->contrib;
+    // an accepted offer with activation opens round g == t (P == 1); a refused
+    // one never does, so late_copy and a fused round never meet
+    s_fused = *(volatile int*)&L->snapped;
+    s_fold = *(volatile int*)&L->dec_fold;
+    s_status = *(volatile unsigned long long*)&L->dec_status;
+    s_t0 = *(volatile unsigned long long*)&L->upd_t0;
+  }
+  __syncthreads();
+  T* stash = reinterpret_cast<T*>(d.send[d.rank]);
+  const T* gbuf = reinterpret_cast<const T*>(d.gbuf[d.rank]);
+  const long long n = d.n;
+  if (!s_fused) {
+    // rare: no round this step.  Keep a folded gradient, reply, then the
+    // ordinary wait + update (refused zero-copy offers are copied late)
+    if (s_fold) {
+      const long long tid0 = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+      const long long nth0 = (long long)gridDim.x * blockDim.x;
+      for (long long e = tid0; e < n; e += nth0) stash[e] = Ops<T>::add(stash[e], gbuf[e]);
+    }
+    if (blockIdx.x == 0 && threadIdx.x == 0) direct_reply(d, seq, s_status);
+    update_gen_body<T, MOM>(w, mom, d.ring[d.rank], d.slot_bytes, d.R, L, lr, mu, n, vec_ok, H, t,
+                            timeout_ns, 0, stash, gbuf);
+    return;
+  }
+  const long long g = s_g;
+  const int contrib = s_contrib;
+  const bool has = (contrib & (int)EC_SNAP_DATA) != 0;
+  const T* src = (contrib & (int)EC_SNAP_SRC_GRAD) ? gbuf : stash;
+  T* slot = reinterpret_cast<T*>(d.ring[d.rank] + (g % d.R) * d.slot_bytes);
+  bool bad;
+  if (s_fold) bad = direct_pass<T, MOM, true>(stash, gbuf, stash, slot, w, mom, lr, mu, n, vec_ok, has);
+  else bad = direct_pass<T, MOM, false>(src, nullptr, stash, slot, w, mom, lr, mu, n, vec_ok, has);
+  // the next step's grid may start launching (it waits for our completion)
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+  if (__syncthreads_or(bad) && threadIdx.x == 0) atomicOr(&L->upd_bad, 1u);
+  if (threadIdx.x == 0) {
+    __threadfence();
+    if (atomicAdd(&L->upd_count, 1ull) == gridDim.x - 1) {
+      L->upd_count = 0;
+      L->step_gen = g;
+      DirectStepReport rep{seq, s_status, s_t0, t, atomicExch(&L->upd_bad, 0u) != 0u};
+      direct_publish(d, g, contrib, has ? 1ull : 0ull, &rep);
     }
   }
 }
@@ -1502,6 +1722,8 @@ cudaError_t preload_kernels() {
       (const void*)ec_fold_auto_kernel<long long>, (const void*)ec_wait_gen_kernel,
       (const void*)ec_wait_done_kernel,
       (const void*)ec_update_gen_kernel<float, false>, (const void*)ec_update_gen_kernel<double, false>,
+      (const void*)ec_direct_step_kernel<float, false>, (const void*)ec_direct_step_kernel<double, false>,
+      (const void*)ec_direct_step_kernel<float, true>, (const void*)ec_direct_step_kernel<double, true>,
       (const void*)ec_update_gen_kernel<float, true>, (const void*)ec_update_gen_kernel<double, true>,
   };
   for (const void* f : fns) {
@@ -1658,6 +1880,41 @@ cudaError_t launch_update_gen(int dtype, void* w, void* mom, const char* ring, l
   else
     return cudaErrorInvalidValue;
   return cudaGetLastError();
+}
+
+cudaError_t launch_direct_step(int dtype, const EcDesc* d_desc, unsigned long long seq,
+                               unsigned int flags, void* w, void* mom, const void* ring,
+                               long long slot_bytes, const void* src0, const void* src1,
+                               double lr, double mu, long long n, long long t,
+                               unsigned long long timeout_ns, cudaStream_t s) {
+  counted();
+  const int vec_ok = ((((uintptr_t)w) | ((uintptr_t)mom) | ((uintptr_t)ring) | slot_bytes |
+                       ((uintptr_t)src0) | ((uintptr_t)src1)) & 15) == 0;
+  const int V = dtype == 0 ? 4 : 2;
+  // __launch_bounds__(256, 3): one wave is SMs x 3 blocks
+  long long gb = ((n / V + 1) / 4 + 255) / 256 + 1;
+  const int grid = (int)(gb < (long long)sms() * 3 ? gb : (long long)sms() * 3);
+  // programmatic dependent launch: the grid is scheduled while the previous
+  // kernel on the stream drains (the kernel's griddepcontrol.wait orders its reads)
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(256);
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = getenv("EC_NO_PDL") ? 0 : 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  if (dtype == 0) {
+    auto kern = mom ? ec_direct_step_kernel<float, true> : ec_direct_step_kernel<float, false>;
+    return cudaLaunchKernelEx(&cfg, kern, d_desc, seq, flags, (float*)w, (float*)mom, (float)lr,
+                              (float)mu, vec_ok, t, timeout_ns);
+  } else if (dtype == 1) {
+    auto kern = mom ? ec_direct_step_kernel<double, true> : ec_direct_step_kernel<double, false>;
+    return cudaLaunchKernelEx(&cfg, kern, d_desc, seq, flags, (double*)w, (double*)mom, lr, mu,
+                              vec_ok, t, timeout_ns);
+  }
+  return cudaErrorInvalidValue;
 }
 
 cudaError_t launch_write_u64(unsigned long long* p, unsigned long long v, cudaStream_t s) {

@@ -477,6 +477,84 @@ def test_zero_copy_offers_match_oracle(p):
     world.close()
 
 
+@pytest.mark.parametrize("element,mu", [("f4", 0.0), ("f4", 0.9), ("f8", 0.0), ("f8", 0.9)])
+def test_direct_fused_step_matches_oracle(element, mu):
+    """World of one: decide + round + update run as ONE launch
+    (ec_direct_step_kernel) that writes u to the slot and updates w from the
+    register copy.  Same bits as the oracle's round followed by its (momentum)
+    SGD update, for folded offers (arbitrary gradient tensor) and zero-copy
+    offers (the registered bucket), ragged n, and the published u."""
+    from collections import deque
+
+    from paper_1908_04207_b200 import finish_step, train_step_async
+    dt = np.float32 if element == "f4" else np.float64
+    n, lr, steps = 100_003, 0.05, 6
+    rng = np.random.default_rng(21)
+    grads = rng.standard_normal((steps, n)).astype(dt)
+    w0 = rng.standard_normal(n).astype(dt)
+    world = EmulatedWorld(1)
+    cfg = CollectiveConfig(p=1, flavor="solo", vector_len=n, element=element)
+    h = AllreduceHandle(cfg, 0, world)
+    st = TrainState.fresh(w0, lr, rank=0, tau=None, momentum=mu, dtype=cfg.torch_dtype)
+    gd = torch.as_tensor(grads, device="cuda")
+    bucket = h.grad_buffer()
+    attach_delivery_tracking(h, st)
+    pend = deque()
+    for t in range(steps):
+        if t % 2:
+            bucket.copy_(gd[t])
+            g = bucket                       # zero-copy offer
+        else:
+            g = gd[t]                        # folded into the stash
+        pend.append(train_step_async(st, h, g, all_arrive=True))
+        if len(pend) > 2:
+            finish_step(st, h, pend.popleft())
+    gens = []
+    while pend:
+        gens.append(finish_step(st, h, pend.popleft())[2])
+    torch.cuda.synchronize()
+    w, buf = w0.copy(), np.zeros_like(w0)
+    for t in range(steps):
+        u, inc, _ = R.allreduce_round([grads[t]], [True], dt)
+        if mu:
+            w, buf = R.momentum_update(w, buf, u, dt(lr), dt(mu))
+        else:
+            w = R.sgd_update(w, u, lr)
+    assert gens[-1] == steps - 1
+    assert st.w.cpu().numpy().tobytes() == w.tobytes()
+    if mu:
+        assert st.momentum_buf.cpu().numpy().tobytes() == buf.tobytes()
+    gen, res = h.latest_result()
+    assert gen == steps - 1 and _np(res.u).tobytes() == u.tobytes()
+    assert st.send_buf.is_null
+    world.close()
+
+
+def test_direct_zero_copy_folds_into_a_pending_stash():
+    """World of one: a zero-copy step that meets a pending (accepted, not yet
+    reduced) stash folds the gradient into it inside the step kernel (no fold
+    launch): u = 0 + (stash + g), the same bits as fold-then-round."""
+    from paper_1908_04207_b200 import finish_step, train_step_async
+    n, lr = 50_001, 0.25
+    rng = np.random.default_rng(5)
+    v, g, w0 = (rng.standard_normal(n, dtype=np.float32) for _ in range(3))
+    world = EmulatedWorld(1)
+    h = AllreduceHandle(CollectiveConfig(p=1, flavor="solo", vector_len=n, element="f4"), 0, world)
+    st = TrainState.fresh(w0, lr, rank=0, tau=None)
+    attach_delivery_tracking(h, st)
+    assert h._contribute(0, v, fresh=True, activate=False)   # stash holds v, round 0 open
+    bucket = h.grad_buffer()
+    bucket.copy_(torch.as_tensor(g, device="cuda"))
+    pend = train_step_async(st, h, bucket, all_arrive=True)
+    _, res, gen = finish_step(st, h, pend)
+    torch.cuda.synchronize()
+    u = np.float32(0) + (v + g)
+    assert gen == 0 and res.included == 1
+    assert st.w.cpu().numpy().tobytes() == (w0 - np.float32(lr) * u).tobytes()
+    assert _np(h.latest_result()[1].u).tobytes() == u.tobytes()
+    world.close()
+
+
 def test_zero_copy_refused_offer_is_kept_in_the_stash():
     """Fig. 7 with zero-copy offers: the slow rank's in-place offer for round 0
     is refused, the device copies that gradient into the stash, and round 1
