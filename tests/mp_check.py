@@ -33,6 +33,9 @@ def main():
     rank = int(os.environ["RANK"])
     world = int(os.environ["WORLD_SIZE"])
     local = int(os.environ.get("LOCAL_RANK", rank))
+    # EC_RANKS_PER_GPU=2 runs e.g. P=8 on a 4-GPU box (functional coverage of
+    # the P=8 geometry; two engines share each GPU)
+    local //= int(os.environ.get("EC_RANKS_PER_GPU", "1"))
     torch.cuda.set_device(local)
     dist.init_process_group("gloo")
     from oracle import restated as R
@@ -90,7 +93,11 @@ def main():
                 assert res.u.cpu().numpy().tobytes() == want.tobytes(), f"n={n} t={t}"
             h.close()
 
+    shared_gpus = int(os.environ.get("EC_RANKS_PER_GPU", "1")) > 1
+
     def solo_first_arrival():
+        if shared_gpus:   # engines of two processes time-slice one GPU (no MPS)
+            return {"skipped": "arrival-order check needs one rank per GPU"}
         cfg = CollectiveConfig(p=world, flavor="solo", vector_len=1000, element="f4")
         h = AllreduceHandle(cfg, rank, pw, cid=next_cid())
         contrib = np.random.default_rng(1).standard_normal((world, 1000), dtype=np.float32)
@@ -105,6 +112,8 @@ def main():
         return {"included": res.included}
 
     def majority_prefix():
+        if shared_gpus:
+            return {"skipped": "arrival-order check needs one rank per GPU"}
         seeds = []
         for seed in (31, 32, 33, 34):
             cfg = CollectiveConfig(p=world, flavor="majority", vector_len=16, element="f8", seed=seed)
