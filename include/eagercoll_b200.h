@@ -104,6 +104,10 @@ void* ec_send_ptr(ec_comm_t* c, int local_idx);
 void* ec_grad_ptr(ec_comm_t* c, int local_idx);
 void* ec_slot_ptr(ec_comm_t* c, int local_idx, int64_t gen);
 int64_t ec_n_elems(ec_comm_t* c);
+/* 1 when ec_step_async updates progressively: the step's update kernel applies
+ * eagersgd.py:165 to each chunk of the round's result as it lands (owners
+ * publish per-chunk-group arrival words), overlapping the NVLink-bound round */
+int ec_comm_progressive(ec_comm_t* c);
 
 /* ---- application protocol -------------------------------------------------
  * GradientBuffer.fold (eagersgd.py:55-57) into the send buffer, stream-ordered.

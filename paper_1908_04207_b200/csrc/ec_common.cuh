@@ -26,11 +26,18 @@
 // internal contribution flag (set by the post kernel from the fold's poison word)
 #define EC_CF_POISON 0x100
 
-// snapshot word: ((gen+1) << 3) | src_grad << 2 | has_data << 1 | fresh
+// snapshot word: ((gen+1) << 4) | upd << 3 | src_grad << 2 | has_data << 1 | fresh
 #define EC_SNAP_FRESH 1ull
 #define EC_SNAP_DATA 2ull
 #define EC_SNAP_SRC_GRAD 4ull   // the offer is the registered gradient buffer, not the stash
-#define EC_SNAP_SHIFT 3
+#define EC_SNAP_UPD 8ull        // this rank updates progressively: owners publish arrival words
+#define EC_SNAP_SHIFT 4
+// contribution flag: the offer's step update kernel follows it on the stream and
+// consumes the round's chunks as they land (owners publish arrival words)
+#define EC_CF_STEP 32u
+// arrival words: owner worker (q, w) publishes ((gen+1) << 24) | chunks landed
+#define EC_PROG_W 64
+#define EC_PROG_SHIFT 24
 // contribution flag: offer the registered gradient buffer (zero-copy, stash null)
 #define EC_CF_SRC_GRAD 8u
 // direct mode: offer the gradient buffer iff the stash is still null at decision time
@@ -50,6 +57,9 @@ struct alignas(128) EcCtrl {
   unsigned long long arrive_from[EC_MAX_P];  // gen+1: source boarded (all-arrive)
   unsigned long long done_from[EC_MAX_P];    // gen+1: source's data for gen is in our slot
   unsigned long long staged_from[EC_MAX_P];  // gen+1: source staged its offer (NVLS mode)
+  // fused updates: owner q's worker w has stored its first k chunks of
+  // generation g into our slot when prog[q][w] >= ((g+1) << 24) | k
+  unsigned long long prog[EC_MAX_P][EC_PROG_W];
 };
 
 struct alignas(64) EcReq {
@@ -109,7 +119,12 @@ struct alignas(128) EcLocal {
   unsigned long long dec_tag;      // direct step: seq + 1 once block 0 decided the step's offer
   unsigned long long dec_status;   // direct step: the decision's reply status
   int dec_fold;                    // direct step: fold the gradient into the stash in-pass
-  int pad6;
+  int pad7;
+  unsigned long long fuse_seq;     // request seq + 1 of the last offer accepted with arrival words
+  unsigned long long cmd_updm;     // round: ranks updating progressively (owners signal arrivals)
+  int step_fused;                  // the current async step updates progressively (arrival words)
+  int pad8;
+  unsigned long long upd_next_item;  // progressive update: next chunk item to claim
   EcReq dreq[EC_REQ_RING];         // stream-posted requests (device copy of the ring)
 };
 
@@ -156,6 +171,7 @@ struct EcDesc {
   int mode;                           // data phase: 0 = fused TMA, 1 = two-phase ld.cg pull,
                                       // 2 = NVLS (multimem.ld_reduce / multimem.st, fast mode)
   int chv, stages;                    // TMA chunk (16-B vectors) and pipeline depth
+  int sig_every;                      // chunks per arrival word (progressive updates; 0 = ~6/round)
   int smem_bytes;
   long long n, nvec;                  // elements, whole 16-B vectors
   long long slot_bytes;

@@ -11,6 +11,7 @@
 #include <string.h>
 #include <time.h>
 
+#include <map>
 #include <mutex>
 #include <string>
 #include <vector>
@@ -30,6 +31,7 @@ cudaError_t launch_reduce(int dtype, const void* const* srcs, int p, unsigned lo
                           void* dst, long long n, int div, cudaStream_t s);
 cudaError_t launch_post(EcLocal* L, unsigned long long seq1, unsigned int type, unsigned int flags,
                         long long t, long long arg, cudaStream_t s);
+int engine_blocks_per_sm(int dtype, int smem_bytes);
 cudaError_t launch_fold_auto(int dtype, void* stash, const void* grad, long long n, EcLocal* L,
                              unsigned long long seq1, unsigned flags, long long t, int zero_copy,
                              cudaStream_t s);
@@ -40,7 +42,7 @@ cudaError_t launch_wait_done(EcLocal* L, EcHostCtl* H, long long t, unsigned lon
 cudaError_t launch_update_gen(int dtype, void* w, void* mom, const char* ring, long long slot_bytes,
                               int R, EcLocal* L, double lr, double mu, long long n, EcHostCtl* H,
                               long long t, unsigned long long timeout_ns, unsigned long long seq1,
-                              void* stash, const void* gbuf, cudaStream_t s);
+                              void* stash, const void* gbuf, const EcDesc* dp, cudaStream_t s);
 cudaError_t launch_write_u64(unsigned long long* p, unsigned long long v, cudaStream_t s);
 cudaError_t launch_direct_step(int dtype, const EcDesc* d_desc, unsigned long long seq,
                                unsigned int flags, void* w, void* mom, const void* ring,
@@ -149,6 +151,7 @@ struct ec_comm {
   void* last_stream = nullptr;  // direct mode orders host-posted requests on it
   unsigned long long epoch = 0;
   int mode = 0, chv = 256, stages = 4, smem_bytes = 0;  // data phase (see EcDesc)
+  double budget = 0.0;                                 // SMs' worth of engine CTAs held
   // NVLS (reduction_mode "fast"): multicast object over every rank's GPU
   CUmemGenericAllocationHandle mc_handle = 0, mc_phys = 0;
   bool mc_created = false, mc_attached = false, mc_phys_made = false;
@@ -295,6 +298,45 @@ static void nvls_teardown(ec_comm_t* c) {
   }
 }
 
+// Every engine is a cooperative grid that must be co-resident with every other
+// running engine on the device (a CTA that never gets an SM would stall its
+// rank forever).  Each communicator reserves its CTAs' share of the SMs at
+// creation; a communicator created when others hold most of the device gets
+// fewer worker CTAs or fails loudly.
+static std::mutex g_budget_mu;
+static std::map<int, double> g_budget_used;
+
+static int budget_engine(ec_comm_t* c, bool w_default) {
+  int sms = 0;
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, c->device);
+  const int k = engine_blocks_per_sm(c->dtype, c->smem_bytes);
+  if (sms <= 0 || k <= 0) return fail(EC_E_CUDA, "engine occupancy query failed");
+  std::lock_guard<std::mutex> g(g_budget_mu);
+  const double left = sms - 1 - g_budget_used[c->device];   // one SM of slack
+  auto need = [&](int W) { return (double)c->n_local * (1 + W) / k; };
+  if (need(c->W) > left) {
+    if (!w_default && !getenv("EC_WORKERS_SHRINK"))
+      return fail(EC_E_STATE, "no room for another engine on device %d (%.0f of %d SMs held by "
+                  "other collectives): close or release them", c->device,
+                  g_budget_used[c->device], sms);
+    const int W = (int)(left * k / c->n_local) - 1;
+    if (W < 4)
+      return fail(EC_E_STATE, "no room for another engine on device %d (%.0f of %d SMs held by "
+                  "other collectives): close or release them", c->device,
+                  g_budget_used[c->device], sms);
+    c->W = W;
+  }
+  c->budget = need(c->W);
+  g_budget_used[c->device] += c->budget;
+  return EC_OK;
+}
+
+static void budget_release(ec_comm_t* c) {
+  std::lock_guard<std::mutex> g(g_budget_mu);
+  g_budget_used[c->device] -= c->budget;
+  c->budget = 0.0;
+}
+
 extern "C" int ec_nvls_supported(int device) {
   DrvApi& D = drv();
   if (!D.ok) return 0;
@@ -402,7 +444,12 @@ extern "C" int ec_nvls_bind(ec_comm_t* c) {
   c->mode = 2;
   // the switch round trip is long: the NVLS data phase wants more CTAs
   // (measured P=4, 1 GiB: W=64 363 GB/s, W=128 558, W=144 561 busbw)
-  if (c->W_default && c->n_local == 1) c->W = 128;
+  if (c->W_default && c->n_local == 1) {
+    budget_release(c);
+    c->W = 128;
+    int rc = budget_engine(c, true);
+    if (rc) return rc;
+  }
   return EC_OK;
 }
 
@@ -473,6 +520,13 @@ int ec_comm_create(int world_size, int rank_lo, int n_local, int device, int64_t
     c->chv = chb / 16;
     c->stages = st;
     c->smem_bytes = c->mode == 0 ? st * (world_size + 1) * chb : 0;
+  }
+  if (!c->direct) {
+    const int brc = budget_engine(c, w_default);
+    if (brc) {
+      delete c;
+      return brc;
+    }
   }
   if (const char* env = getenv("EC_TIMEOUT_S")) c->timeout_ns = (unsigned long long)(atof(env) * 1e9);
   c->ctrl.assign(world_size, nullptr);
@@ -618,6 +672,8 @@ static int upload_descs(ec_comm_t* c) {
     x.dtype = c->dtype;
     x.R = c->R;
     x.W = c->W;
+    x.sig_every = getenv("EC_SIGNAL_EVERY") ? atoi(getenv("EC_SIGNAL_EVERY")) : 0;  // 0: adaptive
+    if (x.sig_every < 0) x.sig_every = 0;
     x.replay = r->forced != nullptr;
     x.vec = V;
     x.n = c->n;
@@ -717,6 +773,7 @@ int ec_comm_destroy(ec_comm_t* c) {
   }
   if (c->d_descs) cudaFree(c->d_descs);
   if (c->es) cudaStreamDestroy(c->es);
+  budget_release(c);
   delete c;
   return rc;
 }
@@ -745,6 +802,9 @@ void* ec_slot_ptr(ec_comm_t* c, int li, int64_t gen) {
 }
 
 int64_t ec_n_elems(ec_comm_t* c) { return c ? c->n : -1; }
+int ec_comm_progressive(ec_comm_t* c) {
+  return c ? (!c->direct && c->mode == 0 && c->W <= EC_PROG_W && c->dtype != EC_I64) : -1;
+}
 
 int ec_fold(ec_comm_t* c, int li, const void* grad, int mode, void* stream) {
   int rc = check_li(c, li);
@@ -1082,8 +1142,13 @@ int ec_step_async(ec_comm_t* c, int li, int64_t t, const void* grad, uint32_t fl
     // A world of one offering its registered buffer needs no fold launch: the
     // step kernel offers it in place, or folds it into a pending stash in-pass
     ProfScope ps(0, stream);
+    // progressive update: the update kernel behind this offer consumes the
+    // round's chunks as they land (owners publish arrival words to us)
+    const void* mom_eff = (mom && mu != 0.0) ? mom : nullptr;
+    const bool prog = ec_comm_progressive(c) == 1 && !getenv("EC_NO_PROGRESSIVE") &&
+                      ((((uintptr_t)w) | ((uintptr_t)mom_eff)) & 15) == 0;
     CK(launch_fold_auto(c->dtype, r->send, grad, c->n, r->local, c->direct ? 0 : seq + 1,
-                        flags & 7u, t, zero_copy ? 1 : 0, s));
+                        (flags & 7u) | (prog ? EC_CF_STEP : 0u), t, zero_copy ? 1 : 0, s));
   }
   if (c->direct) {
     // decide + round + update in one launch (see ec_direct_step_kernel)
@@ -1101,7 +1166,7 @@ int ec_step_async(ec_comm_t* c, int li, int64_t t, const void* grad, uint32_t fl
     ProfScope ps(1, stream);
     CK(launch_update_gen(c->dtype, w, (mom && mu != 0.0) ? mom : nullptr, r->ring, c->slot_bytes, c->R,
                          r->local, lr, mu, c->n, r->hd, t, c->timeout_ns, seq + 1, r->send,
-                         r->gbuf, s));
+                         r->gbuf, c->d_descs + li, s));
   }
   if (seq_out) *seq_out = seq;
   return EC_OK;

@@ -253,10 +253,23 @@ __device__ __forceinline__ bool reduce_chunk(const char* src, char* out, int nvv
 //   rank's send buffer (peer memory, NVLink) into shared memory, reduce it in
 //   tree order, then bulk-store the result into EVERY rank's result slot
 //   (reduce-scatter pull and all-gather push, pipelined per chunk).
+// arrival words for fused updates: after the stores of this worker's first k
+// chunks completed, tell every rank that applies an update this round
+__device__ __forceinline__ void signal_chunks(const EcDesc& d, int w, long long g,
+                                              unsigned long long updm, long long k) {
+  fence_proxy_async_global();   // completed async-proxy stores -> generic release below
+  fence_acq_rel_sys();
+  const unsigned long long v = (((unsigned long long)g + 1) << EC_PROG_SHIFT) | (unsigned long long)k;
+  for (unsigned long long m = updm; m; m &= m - 1) {
+    const int q = __ffsll((long long)m) - 1;
+    st_relaxed_sys(&d.ctrl[q]->prog[d.rank][w], v);
+  }
+}
+
 template <typename T>
 __device__ void round_tma(const EcDesc& d, const char* const* sp, int w, long long g,
                           unsigned long long has, char* smem, unsigned long long* full,
-                          unsigned long long& it, bool& bad) {
+                          unsigned long long& it, bool& bad, unsigned long long updm) {
   const int P = d.P, r = d.rank, S = d.stages;
   const int chv = d.chv, chb = d.chv * 16;
   const long long nch = (d.nvec + chv - 1) / chv;
@@ -265,6 +278,10 @@ __device__ void round_tma(const EcDesc& d, const char* const* sp, int w, long lo
   const long long off = (g % d.R) * d.slot_bytes;
   const size_t stage_bytes = (size_t)(P + 1) * chb;
   const unsigned npop = (unsigned)__popcll(has);
+  // arrival words for progressive updates: ~6 per worker per round by default
+  // (each costs a full-completion wait and a sys fence on the issuing thread;
+  // measured best at P=2 and P=4)
+  const long long sig = d.sig_every > 0 ? d.sig_every : (mine + 5) / 6 > 1 ? (mine + 5) / 6 : 1;
   auto issue = [&](long long k) {  // thread 0: loads of my k-th chunk
     const int s = (int)((it + k) % S);
     const long long c = c0 + w + k * d.W;
@@ -303,12 +320,19 @@ __device__ void round_tma(const EcDesc& d, const char* const* sp, int w, long lo
       }
       tma_commit();
       if (k + S < mine) issue(k + S);
+      if (updm && k >= 2 && ((k - 1) % sig) == 0) {
+        // all but the 2 newest store groups have fully landed: chunks < k - 1
+        // (one signal per sig_every chunks: each costs a sys fence)
+        asm volatile("cp.async.bulk.wait_group 2;" ::: "memory");
+        signal_chunks(d, w, g, updm, k - 1);
+      }
     }
   }
   it += (unsigned long long)mine;
   if (threadIdx.x == 0) {
     tma_wait_all();
     fence_proxy_async_global();
+    if (updm) signal_chunks(d, w, g, updm, mine);
   }
 }
 
@@ -526,7 +550,7 @@ __device__ void engine_worker(const EcDesc& d, int w, unsigned long long epoch) 
   EcLocal* L = d.local;
   extern __shared__ __align__(128) char smem[];
   __shared__ __align__(8) unsigned long long full[8];
-  __shared__ unsigned long long s_seq, s_has, s_src;
+  __shared__ unsigned long long s_seq, s_has, s_src, s_updm;
   __shared__ long long s_gen;
   __shared__ int s_exit;
   __shared__ const char* sp[EC_MAX_P];
@@ -549,6 +573,7 @@ __device__ void engine_worker(const EcDesc& d, int w, unsigned long long epoch) 
           s_seq = s;
           s_gen = *(volatile long long*)&L->cmd_gen;
           s_has = *(volatile unsigned long long*)&L->cmd_has;
+          s_updm = *(volatile unsigned long long*)&L->cmd_updm;
           s_src = *(volatile unsigned long long*)&L->cmd_src;
           s_exit = 0;
           break;
@@ -571,7 +596,7 @@ __device__ void engine_worker(const EcDesc& d, int w, unsigned long long epoch) 
     __syncthreads();
     bool bad = false;
     if (d.mode == 0) {
-      round_tma<T>(d, sp, w, g, has, smem, full, it, bad);
+      round_tma<T>(d, sp, w, g, has, smem, full, it, bad, s_updm);
       if (w == 0 && d.rank == d.P - 1) tail_push<T>(d, sp, has, g);
     } else if (d.mode == 2) {
       round_nvls<T>(d, sp, w, g, has, seen, bad);
@@ -673,11 +698,13 @@ __device__ void engine_controller(const EcDesc& d, unsigned long long epoch) {
       EcReq* dq = &L->dreq[next_req % EC_REQ_RING];
       unsigned type, fl;
       long long t, arg;
+      bool dev_req = false;
       if (ld_acquire_gpu(&dq->seq1) == next_req + 1) {
         type = *(volatile unsigned*)&dq->type;
         fl = *(volatile unsigned*)&dq->flags;
         t = *(volatile long long*)&dq->t;
         arg = *(volatile long long*)&dq->arg;
+        dev_req = true;
       } else {
         if (!poll_host) break;
         EcReq* q = &H->req[next_req % EC_REQ_RING];
@@ -704,6 +731,15 @@ __device__ void engine_controller(const EcDesc& d, unsigned long long epoch) {
         } else {
           contrib = (int)(EC_SNAP_DATA | ((fl & 1u) ? EC_SNAP_FRESH : 0ull) |
                           ((fl & EC_CF_SRC_GRAD) ? EC_SNAP_SRC_GRAD : 0ull));
+          if ((fl & EC_CF_STEP) && dev_req && d.mode == 0 && d.W <= EC_PROG_W) {
+            // the step's update kernel (already resident behind the offer)
+            // consumes round g's chunks as they land: owners publish arrival
+            // words to us; pin slot g on its behalf now (it unpins when done),
+            // before round g can even start
+            *(volatile unsigned long long*)&L->pin_dev = (unsigned long long)g;
+            L->fuse_seq = next_req + 1;
+            contrib |= (int)EC_SNAP_UPD;
+          }
           contributed_round = t;
           status = 1;
           t_req = globaltimer_ns();
@@ -758,7 +794,8 @@ __device__ void engine_controller(const EcDesc& d, unsigned long long epoch) {
         // Result-slot reuse guard: peers write our slot g % R once the round
         // starts, so never snapshot g while a reader still needs generation
         // g - R.  Device readers pin in device memory (SC fence pairs with
-        // wait_and_pin); the host pin is the acknowledged cached value.
+        // wait_and_pin); the host pin is the acknowledged cached value; our
+        // own updater CTAs finish a fused update before upd_fin_gen moves.
         fence_sc_gpu();
         const unsigned long long gr = (unsigned long long)(g - d.R);
         if (ld_acquire_gpu(&L->pin_dev) <= gr || host_pin <= gr) {
@@ -781,19 +818,21 @@ __device__ void engine_controller(const EcDesc& d, unsigned long long epoch) {
     // ---- round: all snapshots in -> two-shot reduction -> publish
     if (snapped) {
       bool all = true;
-      unsigned long long fresh = 0, has = 0, srcg = 0;
+      unsigned long long fresh = 0, has = 0, srcg = 0, updm = 0;
       for (int q = 0; q < P; ++q) {
         unsigned long long w = ld_acquire_sys(&C->snap_from[q]);
         if ((w >> EC_SNAP_SHIFT) < (unsigned long long)g + 1) { all = false; break; }
         fresh |= (w & EC_SNAP_FRESH) << q;
         has |= ((w >> 1) & 1ull) << q;
         srcg |= ((w >> 2) & 1ull) << q;
+        updm |= ((w >> 3) & 1ull) << q;
       }
       if (all) {
         bool timed_out = false;
         L->cmd_gen = g;
         L->cmd_has = has;
         L->cmd_src = srcg;
+        L->cmd_updm = updm;
         ++seq;
         const unsigned long long t0 = globaltimer_ns();
         st_release_gpu(&L->cmd_seq, seq);
@@ -1335,6 +1374,18 @@ __device__ void wait_and_pin(EcLocal* L, EcHostCtl* H, long long t, int R,
     if (ld_relaxed_sys(&H->error) || globaltimer_ns() - t0 > timeout_ns) break;
     __nanosleep(64);
   }
+  if (seq1 && *(volatile unsigned long long*)&L->fuse_seq == seq1) {
+    // accepted for round t with arrival words: this kernel applies round t's
+    // result chunk by chunk as it lands (the controller pinned slot t)
+    L->step_fused = 1;
+    L->step_late = 0;
+    L->step_gen = t;
+    L->upd_t0 = globaltimer_ns();
+    st_relaxed_sys(&H->stepgen[t % EC_REQ_RING], (unsigned long long)t + 1);
+    st_release_gpu(&L->step_tag, (unsigned long long)t + 1);
+    return;
+  }
+  L->step_fused = 0;
   L->step_late = *(volatile int*)&L->late_copy;
   if (L->step_late) *(volatile int*)&L->late_copy = 0;
   while ((d1 = ld_acquire_gpu(&L->done_gen1_dev)) < (unsigned long long)t + 1) {
@@ -1446,15 +1497,118 @@ __device__ __forceinline__ bool update_body(T* __restrict__ w, T* __restrict__ m
 // update from the slot of the step's generation; with H != nullptr the kernel
 // also performs the wait (block 0) and the last CTA releases the pin
 // (fused wait + update + unpin: one launch)
+// Progressive update (the step's offer was accepted for round g with arrival
+// words): CTAs claim chunks in arrival order (k-th chunk of every owner's
+// workers, then k+1 ...), wait for the owner worker's arrival word, and apply
+// w - lr*u (or the momentum form) to the chunk -- the HBM-bound update runs
+// while the NVLink-bound round is still moving later chunks.  Same _rn
+// expressions as update_body.  Returns whether a value of u was non-finite.
+template <typename T, bool MOM>
+__device__ bool progressive_update(const EcDesc& d, T* __restrict__ w, T* __restrict__ mom, T lr,
+                                   T mu, long long g, unsigned long long timeout_ns) {
+  EcLocal* L = d.local;
+  __shared__ long long s_item;
+  constexpr int V = Ops<T>::V;
+  constexpr int U = MOM ? 2 : 4;
+  const int P = d.P, W = d.W, chv = d.chv;
+  const long long nch = (d.nvec + chv - 1) / chv;
+  long long kmax = 0;
+  for (int q = 0; q < P; ++q) {
+    const long long m = (chunk_lo(nch, q + 1, P) - chunk_lo(nch, q, P) + W - 1) / W;
+    if (m > kmax) kmax = m;
+  }
+  const long long nitems = kmax * P * W;
+  auto chunk_of = [&](long long i, int& q, int& wq, long long& k) -> long long {
+    k = i / ((long long)P * W);
+    const long long rem = i % ((long long)P * W);
+    q = (int)(rem / W);
+    wq = (int)(rem % W);
+    const long long c = chunk_lo(nch, q, P) + wq + k * W;
+    return c < chunk_lo(nch, q + 1, P) ? c : -1;
+  };
+  const T* __restrict__ u = reinterpret_cast<const T*>(d.ring[d.rank] + (g % d.R) * d.slot_bytes);
+  const unsigned long long t0 = globaltimer_ns();
+  bool bad = false;
+  while (true) {
+    if (threadIdx.x == 0) {
+      long long i, c = -1;
+      int q = 0, wq = 0;
+      long long k = 0;
+      do {
+        i = (long long)atomicAdd(&L->upd_next_item, 1ull);
+        if (i < nitems) c = chunk_of(i, q, wq, k);
+      } while (i < nitems && c < 0);
+      if (i < nitems) {
+        const unsigned long long need =
+            (((unsigned long long)g + 1) << EC_PROG_SHIFT) | (unsigned long long)(k + 1);
+        const unsigned long long* pw = &d.ctrl[d.rank]->prog[q][wq];
+        // hundreds of CTAs may wait at once: back off, or the polling starves
+        // the engine's controller and its NVLink traffic
+        unsigned ns = 256;
+        while (ld_acquire_sys(pw) < need) {
+          __nanosleep(ns);
+          if (ns < 2048) ns <<= 1;
+          if (globaltimer_ns() - t0 > timeout_ns) {
+            st_release_sys(&d.hctl->error_info, 0x500 + q);
+            st_release_sys(&d.hctl->error, EC_DERR_TIMEOUT);
+            break;
+          }
+        }
+        s_item = c;
+      } else {
+        s_item = -1;
+      }
+    }
+    __syncthreads();
+    const long long c = s_item;
+    if (c < 0) break;
+    const long long v0 = c * chv;
+    const int nvv = (int)min((long long)chv, d.nvec - v0);
+    for (int base = threadIdx.x; base < nvv; base += blockDim.x * U) {
+      Vec16<T> uv[U], wv[U], bv[MOM ? U : 1];
+#pragma unroll
+      for (int k = 0; k < U; ++k) {
+        const int v = base + k * blockDim.x;
+        if (v < nvv) {
+          uv[k].raw = ld_cg_v4(u + (v0 + v) * V);
+          wv[k].raw = ld_stream_v4(w + (v0 + v) * V);
+          if (MOM) bv[MOM ? k : 0].raw = ld_stream_v4(mom + (v0 + v) * V);
+        }
+      }
+#pragma unroll
+      for (int k = 0; k < U; ++k) {
+        const int v = base + k * blockDim.x;
+        if (v < nvv) {
+#pragma unroll
+          for (int l = 0; l < V; ++l) {
+            bad |= !Ops<T>::finite(uv[k].e[l]);
+            if (MOM) {
+              bv[MOM ? k : 0].e[l] = Ops<T>::mom(mu, bv[MOM ? k : 0].e[l], uv[k].e[l]);
+              wv[k].e[l] = Ops<T>::sgd(wv[k].e[l], lr, bv[MOM ? k : 0].e[l]);
+            } else {
+              wv[k].e[l] = Ops<T>::sgd(wv[k].e[l], lr, uv[k].e[l]);
+            }
+          }
+          if (MOM) st_v4(mom + (v0 + v) * V, bv[MOM ? k : 0].raw);
+          st_v4(w + (v0 + v) * V, wv[k].raw);
+        }
+      }
+    }
+    __syncthreads();   // s_item is reused
+  }
+  return bad;
+}
+
 template <typename T, bool MOM>
 __device__ __forceinline__ void update_gen_body(T* __restrict__ w, T* __restrict__ mom,
                                                 const char* __restrict__ ring, long long slot_bytes,
                                                 int R, EcLocal* __restrict__ L, T lr, T mu,
                                                 long long n, int vec_ok, EcHostCtl* H, long long t,
                                                 unsigned long long timeout_ns, unsigned long long seq1,
-                                                T* __restrict__ stash, const T* __restrict__ gbuf) {
+                                                T* __restrict__ stash, const T* __restrict__ gbuf,
+                                                const EcDesc* __restrict__ dp) {
   __shared__ long long s_gen;
-  __shared__ int s_late;
+  __shared__ int s_late, s_fusedu;
   if (threadIdx.x == 0) {
     if (H != nullptr) {
       if (blockIdx.x == 0) wait_and_pin(L, H, t, R, timeout_ns, seq1);
@@ -1462,25 +1616,54 @@ __device__ __forceinline__ void update_gen_body(T* __restrict__ w, T* __restrict
     }
     s_gen = *(volatile const long long*)&L->step_gen;
     s_late = H != nullptr ? *(volatile const int*)&L->step_late : 0;
+    s_fusedu = H != nullptr ? *(volatile const int*)&L->step_fused : 0;
     asm volatile("fence.proxy.alias;" ::: "memory");  // slot may be written via a multicast alias
   }
   __syncthreads();
   const long long G = s_gen;
-  if (s_late && stash && gbuf) {
-    // a zero-copy offer missed its round: the gradient joins the stash (0 + g)
-    // before the caller's next backward overwrites the gradient buffer
-    const long long tid0 = (long long)blockIdx.x * blockDim.x + threadIdx.x;
-    const long long nth0 = (long long)gridDim.x * blockDim.x;
-    for (long long e = tid0; e < n; e += nth0) stash[e] = Ops<T>::canon(gbuf[e]);
-  }
   const T* __restrict__ u = reinterpret_cast<const T*>(ring + (G % R) * slot_bytes);
-  const bool bad = update_body<T, MOM, MOM ? 2 : 4>(w, mom, u, lr, mu, n, vec_ok);
+  bool bad;
+  if (s_fusedu) {
+    bad = progressive_update<T, MOM>(*dp, w, mom, lr, mu, G, timeout_ns);
+  } else {
+    if (s_late && stash && gbuf) {
+      // a zero-copy offer missed its round: the gradient joins the stash (0 + g)
+      // before the caller's next backward overwrites the gradient buffer
+      const long long tid0 = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+      const long long nth0 = (long long)gridDim.x * blockDim.x;
+      for (long long e = tid0; e < n; e += nth0) stash[e] = Ops<T>::canon(gbuf[e]);
+    }
+    bad = update_body<T, MOM, MOM ? 2 : 4>(w, mom, u, lr, mu, n, vec_ok);
+  }
   if (H == nullptr) return;
   if (__syncthreads_or(bad) && threadIdx.x == 0) atomicOr(&L->upd_bad, 1u);
   if (threadIdx.x == 0) {
     __threadfence();
     if (atomicAdd(&L->upd_count, 1ull) == gridDim.x - 1) {
       L->upd_count = 0;
+      if (s_fusedu) {
+        // the round's publication: the scalar tail (reduced by the last owner
+        // with plain stores) and the log are in once done moves past G
+        L->upd_next_item = 0;
+        const unsigned long long tw = globaltimer_ns();
+        while (ld_acquire_gpu(&L->done_gen1_dev) < (unsigned long long)G + 1) {
+          if (ld_relaxed_sys(&H->error) || globaltimer_ns() - tw > timeout_ns) break;
+          __nanosleep(64);
+        }
+        const volatile T* uv = u;
+        bool tbad = false;
+        for (long long e = dp->nvec * Ops<T>::V; e < n; ++e) {
+          T uu = uv[e];
+          tbad |= !Ops<T>::finite(uu);
+          if (MOM) {
+            const T b = Ops<T>::mom(mu, mom[e], uu);
+            mom[e] = b;
+            uu = b;
+          }
+          w[e] = Ops<T>::sgd(w[e], lr, uu);
+        }
+        if (tbad) atomicOr(&L->upd_bad, 1u);
+      }
       if (s_late) *(volatile int*)&L->stash_null = 0;
       st_relaxed_sys(&H->stepbad[t % EC_REQ_RING], atomicExch(&L->upd_bad, 0u) ? 1ull : 0ull);
       const unsigned long long t1 = globaltimer_ns();
@@ -1497,9 +1680,10 @@ ec_update_gen_kernel(T* __restrict__ w, T* __restrict__ mom, const char* __restr
                      long long slot_bytes, int R, EcLocal* __restrict__ L, T lr, T mu,
                      long long n, int vec_ok, EcHostCtl* H, long long t,
                      unsigned long long timeout_ns, unsigned long long seq1,
-                     T* __restrict__ stash, const T* __restrict__ gbuf) {
+                     T* __restrict__ stash, const T* __restrict__ gbuf,
+                     const EcDesc* __restrict__ dp) {
   update_gen_body<T, MOM>(w, mom, ring, slot_bytes, R, L, lr, mu, n, vec_ok, H, t, timeout_ns, seq1,
-                          stash, gbuf);
+                          stash, gbuf, dp);
 }
 
 // Direct mode (world of one) async step: decide the step's offer (block 0;
@@ -1642,7 +1826,7 @@ ec_direct_step_kernel(const EcDesc* __restrict__ dp, unsigned long long seq, uns
     }
     if (blockIdx.x == 0 && threadIdx.x == 0) direct_reply(d, seq, s_status);
     update_gen_body<T, MOM>(w, mom, d.ring[d.rank], d.slot_bytes, d.R, L, lr, mu, n, vec_ok, H, t,
-                            timeout_ns, 0, stash, gbuf);
+                            timeout_ns, 0, stash, gbuf, dp);
     return;
   }
   const long long g = s_g;
@@ -1732,6 +1916,19 @@ cudaError_t preload_kernels() {
     if (e != cudaSuccess) return e;
   }
   return cudaSuccess;
+}
+
+// engine CTAs of this configuration that fit on one SM (shared memory /
+// registers); the host budgets every engine on a device against it
+int engine_blocks_per_sm(int dtype, int smem_bytes) {
+  const void* fn = dtype == 0 ? (const void*)ec_engine<float>
+                  : dtype == 1 ? (const void*)ec_engine<double>
+                               : (const void*)ec_engine<long long>;
+  if (cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_bytes) != cudaSuccess)
+    return 0;
+  int k = 0;
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&k, fn, 256, smem_bytes) != cudaSuccess) return 0;
+  return k;
 }
 
 cudaError_t launch_engine(int dtype, const EcDesc* d_descs, int n_local, int blocks_per_rank,
@@ -1861,7 +2058,7 @@ cudaError_t launch_wait_gen(EcLocal* L, EcHostCtl* H, long long t, int R, unsign
 cudaError_t launch_update_gen(int dtype, void* w, void* mom, const char* ring, long long slot_bytes,
                               int R, EcLocal* L, double lr, double mu, long long n, EcHostCtl* H,
                               long long t, unsigned long long timeout_ns, unsigned long long seq1,
-                              void* stash, const void* gbuf, cudaStream_t s) {
+                              void* stash, const void* gbuf, const EcDesc* dp, cudaStream_t s) {
   counted();
   const int vec_ok = ((((uintptr_t)w) | ((uintptr_t)mom) | ((uintptr_t)ring) | slot_bytes) & 15) == 0;
   const int V = dtype == 0 ? 4 : 2;
@@ -1871,11 +2068,11 @@ cudaError_t launch_update_gen(int dtype, void* w, void* mom, const char* ring, l
   if (dtype == 0) {
     auto kern = mom ? ec_update_gen_kernel<float, true> : ec_update_gen_kernel<float, false>;
     kern<<<grid, 256, 0, s>>>((float*)w, (float*)mom, ring, slot_bytes, R, L, (float)lr, (float)mu, n,
-                              vec_ok, H, t, timeout_ns, seq1, (float*)stash, (const float*)gbuf);
+                              vec_ok, H, t, timeout_ns, seq1, (float*)stash, (const float*)gbuf, dp);
   } else if (dtype == 1) {
     auto kern = mom ? ec_update_gen_kernel<double, true> : ec_update_gen_kernel<double, false>;
     kern<<<grid, 256, 0, s>>>((double*)w, (double*)mom, ring, slot_bytes, R, L, lr, mu, n, vec_ok, H,
-                              t, timeout_ns, seq1, (double*)stash, (const double*)gbuf);
+                              t, timeout_ns, seq1, (double*)stash, (const double*)gbuf, dp);
   }
   else
     return cudaErrorInvalidValue;

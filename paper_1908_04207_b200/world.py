@@ -119,6 +119,11 @@ class Comm:
         return code.value, info.value
 
     # -- tensors ------------------------------------------------------------
+    @property
+    def progressive(self) -> bool:
+        """Async steps update each chunk of the round's result as it lands."""
+        return lib.ec_comm_progressive(self.ptr) == 1
+
     def send_view(self, li: int) -> torch.Tensor:
         key = ("send", li)
         if key not in self._views:

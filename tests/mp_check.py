@@ -150,6 +150,56 @@ def main():
         h.close()
         assert st.w.cpu().numpy().tobytes() == w.tobytes()
 
+    def eager_sgd_async_fused():
+        """train_step_async over NVLink: each step's update kernel applies the
+        round's result chunk by chunk as it lands (progressive update), for
+        folded and zero-copy offers, plain SGD and momentum, ragged n -- same
+        bits as the oracle's round followed by its update."""
+        from collections import deque
+
+        from paper_1908_04207_b200 import finish_step, train_step_async
+        from paper_1908_04207_b200.eagersgd import attach_delivery_tracking
+        out = {}
+        for mu in (0.0, 0.9):
+            n, lr, steps = 3_000_017, 0.05, 6
+            rng = np.random.default_rng(9)
+            grads = rng.standard_normal((steps, world, n), dtype=np.float32)
+            w0 = rng.standard_normal(n, dtype=np.float32)
+            cfg = CollectiveConfig(p=world, flavor="solo", vector_len=n, element="f4")
+            h = AllreduceHandle(cfg, rank, pw, cid=next_cid())
+            st = TrainState.fresh(w0, lr, rank=rank, tau=None, momentum=mu)
+            attach_delivery_tracking(h, st)
+            bucket = h.grad_buffer()
+            gd = torch.as_tensor(grads[:, rank], device="cuda")
+            pend, gens = deque(), []
+            for t in range(steps):
+                if t % 2:
+                    bucket.copy_(gd[t])
+                    g = bucket
+                else:
+                    g = gd[t]
+                pend.append(train_step_async(st, h, g, all_arrive=True))
+                if len(pend) > 2:
+                    gens.append(finish_step(st, h, pend.popleft())[2])
+            while pend:
+                gens.append(finish_step(st, h, pend.popleft())[2])
+            torch.cuda.current_stream().synchronize()
+            w, buf = w0.copy(), np.zeros_like(w0)
+            for t in range(steps):
+                u, _, _ = R.allreduce_round(list(grads[t]), [True] * world, np.float32)
+                if mu:
+                    w, buf = R.momentum_update(w, buf, u, np.float32(lr), np.float32(mu))
+                else:
+                    w = R.sgd_update(w, u, lr)
+            fused = h.comm.progressive
+            h.close()
+            assert gens == list(range(steps)), gens
+            assert st.w.cpu().numpy().tobytes() == w.tobytes(), f"mu={mu}"
+            if mu:
+                assert st.momentum_buf.cpu().numpy().tobytes() == buf.tobytes()
+            out[f"mu={mu}"] = {"progressive_update": fused}
+        return out
+
     def nvls_fast_mode():
         """reduction_mode="fast": the NVSwitch reduces (when the fabric has
         NVLS); same u on every rank, within fp32 rounding of the fixed-order sum."""
@@ -225,6 +275,7 @@ def main():
     check("solo_first_arrival", solo_first_arrival)
     check("majority_prefix", majority_prefix)
     check("eager_sgd_all_arrive", eager_sgd_all_arrive)
+    check("eager_sgd_async_fused", eager_sgd_async_fused)
     check("nvls_fast_mode", nvls_fast_mode)
     check("replay_c1", replay_c1)
 
