@@ -64,11 +64,13 @@ class CpuEagerStep:
 
 
 def time_steps(p: int, n: int, budget_s: float = 15.0, min_steps: int = 2, max_steps: int = 50,
-               threads: int | None = None):
-    """Run whole steps until the budget is spent; returns dict with rank-steps/s."""
+               threads: int | None = None, warmup: int = 1):
+    """Run `warmup` untimed steps, then whole steps until the budget is spent
+    (at least min_steps, at most max_steps); returns dict with rank-steps/s."""
     b = CpuEagerStep(p, n, threads)
     try:
-        b.step()  # warm-up (page faults, pool start)
+        for _ in range(max(1, warmup)):
+            b.step()  # warm-up (page faults, pool start)
         t0 = time.perf_counter()
         k = 0
         while k < min_steps or (time.perf_counter() - t0 < budget_s and k < max_steps):
@@ -78,7 +80,7 @@ def time_steps(p: int, n: int, budget_s: float = 15.0, min_steps: int = 2, max_s
     finally:
         b.close()
     return {"steps": k, "seconds": dt, "rank_steps_per_s": p * k / dt,
-            "ms_per_step": 1e3 * dt / k, "threads": b.threads}
+            "ms_per_step": 1e3 * dt / k, "threads": b.threads, "warmup": max(1, warmup)}
 
 
 def time_local_kernels(n: int, budget_s: float = 5.0, threads: int | None = None):
