@@ -1686,169 +1686,165 @@ ec_update_gen_kernel(T* __restrict__ w, T* __restrict__ mom, const char* __restr
                           stash, gbuf, dp);
 }
 
-// Direct mode (world of one) async step: decide the step's offer (block 0;
-// the other CTAs wait for its device-state decision, dec_tag), then -- when it
-// opened round t, the common case -- ONE pass per element: u = (0 + x) / 1
-// into the slot and w -= lr*u (or the momentum form) from the register copy of
-// u, so the update never re-reads the slot.  x is the registered gradient
-// buffer (zero-copy offer, null stash), the stash (folded by ec_fold_auto), or
-// -- FOLD, a zero-copy call that met a non-null stash -- stash + g, folded in
-// this same pass.  Bit-identical to fold + decide + round + update as separate
-// launches (same expressions, same order).  Host-visible stores (reply, log,
-// step report) are all made by the last CTA behind one sys fence.  Anything
-// else (a refused offer, no activation) runs the ordinary wait + update body.
-template <typename T, bool MOM, bool FOLD>
-__device__ __forceinline__ bool direct_pass(const T* __restrict__ src, const T* __restrict__ g2,
-                                            T* __restrict__ stash, T* __restrict__ slot,
-                                            T* __restrict__ w, T* __restrict__ mom, T lr, T mu,
-                                            long long n, int vec_ok, bool has) {
+// Direct mode (world of one) async step, ONE pass per element: decide the
+// step's offer (block 0), then -- when it opened round t, the common case --
+// u = (0 + x) / 1 into the slot and w -= lr*u (or the momentum form) from the
+// register copy of u, so the update never re-reads the slot.  x is the
+// registered gradient buffer (zero-copy offer, null stash), the stash (folded
+// by ec_fold_auto), or -- FOLD, a zero-copy call that met a non-null stash --
+// stash + g, folded in this same pass.  Bit-identical to fold + decide + round
+// + update as separate launches (same expressions, same order).
+//
+// Shape (measured, profiles/): full occupancy -- one 16-byte vector of each
+// stream per thread, 8 CTAs of 256 threads per SM, one CTA per 256 vectors.
+// Block 0 decides and publishes the decision packed into ONE word
+// (dec_tag = (seq+1) << 8 | bits), so every other CTA's prologue is a single
+// acquire load; completion is the kernel boundary (ec_direct_publish_kernel,
+// launched behind it with PDL, writes every host-visible word behind one sys
+// fence), so no CTA pays a fence or a counter atomic.  The rare no-round path
+// (refused offer) runs out of line with the ordinary wait + update body.
+#define EC_DW_FUSED 1u
+#define EC_DW_FOLD 2u
+#define EC_DW_HAS 4u
+#define EC_DW_SRCG 8u
+
+template <typename T, bool MOM>
+__device__ __noinline__ void direct_step_fallback(const EcDesc& d, unsigned long long seq,
+                                                  unsigned long long status, int fold, T* w,
+                                                  T* mom, T lr, T mu, int vec_ok, long long t,
+                                                  unsigned long long timeout_ns) {
+  EcLocal* L = d.local;
+  T* stash = reinterpret_cast<T*>(d.send[d.rank]);
+  const T* gbuf = reinterpret_cast<const T*>(d.gbuf[d.rank]);
+  const long long n = d.n;
+  if (fold) {
+    const long long tid0 = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    const long long nth0 = (long long)gridDim.x * blockDim.x;
+    for (long long e = tid0; e < n; e += nth0) stash[e] = Ops<T>::add(stash[e], gbuf[e]);
+  }
+  if (blockIdx.x == 0 && threadIdx.x == 0) direct_reply(d, seq, status);
+  update_gen_body<T, MOM>(w, mom, d.ring[d.rank], d.slot_bytes, d.R, L, lr, mu, n, vec_ok, d.hctl,
+                          t, timeout_ns, 0, stash, gbuf, &d);
+}
+
+template <typename T, bool MOM>
+__global__ void __launch_bounds__(256, 8)
+ec_direct_step_kernel(const EcDesc* __restrict__ dp, unsigned long long seq,
+                           unsigned int flags, T* __restrict__ w, T* __restrict__ mom, T lr, T mu,
+                           int vec_ok, long long t, unsigned long long timeout_ns) {
+  const EcDesc& d = *dp;
+  EcLocal* L = d.local;
+  __shared__ unsigned long long s_dw;
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+  if (threadIdx.x == 0) {
+    unsigned long long dw;
+    if (blockIdx.x == 0) {
+      const unsigned long long t0 = globaltimer_ns();
+      const int fold = (flags & EC_CF_SRC_GRAD_AUTO) && !*(volatile int*)&L->stash_null;
+      const unsigned long long status = direct_decide_core(d, EC_REQ_CONTRIB, flags, t, 0);
+      const int contrib = *(volatile int*)&L->contrib;
+      const int fused = *(volatile int*)&L->snapped;
+      L->dec_status = status;
+      L->dec_fold = fold;
+      L->upd_t0 = t0;
+      dw = ((seq + 1) << 8) | (fused ? EC_DW_FUSED : 0u) | (fold ? EC_DW_FOLD : 0u) |
+           ((contrib & (int)EC_SNAP_DATA) ? EC_DW_HAS : 0u) |
+           ((contrib & (int)EC_SNAP_SRC_GRAD) ? EC_DW_SRCG : 0u);
+      __threadfence();
+      st_release_gpu(&L->dec_tag, dw);
+    } else {
+      while (((dw = ld_acquire_gpu(&L->dec_tag)) >> 8) != seq + 1) __nanosleep(32);
+    }
+    s_dw = dw;
+  }
+  __syncthreads();
+  const unsigned long long dw = s_dw;
+  if (!(dw & EC_DW_FUSED)) {
+    direct_step_fallback<T, MOM>(d, seq, *(volatile unsigned long long*)&L->dec_status,
+                                 (dw & EC_DW_FOLD) ? 1 : 0, w, mom, lr, mu, vec_ok, t, timeout_ns);
+    return;
+  }
+  // an accepted offer with activation opened round g == t (P == 1)
+  const long long g = t;
   constexpr int V = Ops<T>::V;
-  constexpr int U = (MOM || FOLD) ? 2 : 4;
-  const long long tid = (long long)blockIdx.x * blockDim.x + threadIdx.x;
-  const long long nth = (long long)gridDim.x * blockDim.x;
-  bool bad = false;
+  const bool has = (dw & EC_DW_HAS) != 0, fold = (dw & EC_DW_FOLD) != 0;
+  T* stash = reinterpret_cast<T*>(d.send[d.rank]);
+  const T* gbuf = reinterpret_cast<const T*>(d.gbuf[d.rank]);
+  const T* src = (dw & EC_DW_SRCG) ? gbuf : stash;
+  T* slot = reinterpret_cast<T*>(d.ring[d.rank] + (g % d.R) * d.slot_bytes);
+  const long long n = d.n, nv = vec_ok ? n / V : 0;
   auto reduce1 = [&](T x) -> T {   // rs_fixed<T, 1>: tree of one canonical leaf, / 1
     T c[1] = {Ops<T>::canon(x)};
     return Ops<T>::divp(tree_sum<T, 1>(c), 1, (T)1, true);
   };
-  long long done = 0;
-  if (vec_ok) {
-    const long long nv = n / V;
-    for (long long base = tid; base < nv; base += nth * U) {
-      Vec16<T> xv[U], wv[U], bv[MOM ? U : 1], gv[FOLD ? U : 1];
+  bool bad = false;
+  const long long v = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (v < nv) {
+    Vec16<T> xv, wv, bv, gv;
+    xv.raw = has ? ld_stream_v4(src + v * V) : make_uint4(0, 0, 0, 0);
+    if (fold) gv.raw = ld_stream_v4(gbuf + v * V);
+    wv.raw = ld_stream_v4(w + v * V);
+    if (MOM) bv.raw = ld_stream_v4(mom + v * V);
+    if (fold) {
 #pragma unroll
-      for (int k = 0; k < U; ++k) {
-        const long long v = base + k * nth;
-        if (v < nv) {
-          xv[k].raw = has ? ld_stream_v4(src + v * V) : make_uint4(0, 0, 0, 0);
-          if (FOLD) gv[FOLD ? k : 0].raw = ld_stream_v4(g2 + v * V);
-          wv[k].raw = ld_stream_v4(w + v * V);
-          if (MOM) bv[MOM ? k : 0].raw = ld_stream_v4(mom + v * V);
-        }
-      }
+      for (int l = 0; l < V; ++l) xv.e[l] = Ops<T>::add(xv.e[l], gv.e[l]);
+      st_v4(stash + v * V, xv.raw);
+    }
+    Vec16<T> uv;
 #pragma unroll
-      for (int k = 0; k < U; ++k) {
-        const long long v = base + k * nth;
-        if (v < nv) {
-          if (FOLD) {
-#pragma unroll
-            for (int l = 0; l < V; ++l) xv[k].e[l] = Ops<T>::add(xv[k].e[l], gv[FOLD ? k : 0].e[l]);
-            st_v4(stash + v * V, xv[k].raw);
-          }
-          Vec16<T> uv;
-#pragma unroll
-          for (int l = 0; l < V; ++l) {
-            uv.e[l] = reduce1(xv[k].e[l]);
-            bad |= !Ops<T>::finite(uv.e[l]);
-            if (MOM) {
-              bv[MOM ? k : 0].e[l] = Ops<T>::mom(mu, bv[MOM ? k : 0].e[l], uv.e[l]);
-              wv[k].e[l] = Ops<T>::sgd(wv[k].e[l], lr, bv[MOM ? k : 0].e[l]);
-            } else {
-              wv[k].e[l] = Ops<T>::sgd(wv[k].e[l], lr, uv.e[l]);
-            }
-          }
-          st_v4(slot + v * V, uv.raw);
-          if (MOM) st_v4(mom + v * V, bv[MOM ? k : 0].raw);
-          st_v4(w + v * V, wv[k].raw);
-        }
+    for (int l = 0; l < V; ++l) {
+      uv.e[l] = reduce1(xv.e[l]);
+      bad |= !Ops<T>::finite(uv.e[l]);
+      if (MOM) {
+        bv.e[l] = Ops<T>::mom(mu, bv.e[l], uv.e[l]);
+        wv.e[l] = Ops<T>::sgd(wv.e[l], lr, bv.e[l]);
+      } else {
+        wv.e[l] = Ops<T>::sgd(wv.e[l], lr, uv.e[l]);
       }
     }
-    done = nv * V;
+    st_v4(slot + v * V, uv.raw);
+    if (MOM) st_v4(mom + v * V, bv.raw);
+    st_v4(w + v * V, wv.raw);
   }
-  for (long long e = done + tid; e < n; e += nth) {
-    T x = has ? src[e] : Ops<T>::zero();
-    if (FOLD) {
-      x = Ops<T>::add(x, g2[e]);
-      stash[e] = x;
+  if (blockIdx.x == gridDim.x - 1) {
+    // elements past the whole vectors (or all of them when unaligned)
+    for (long long e = nv * V + threadIdx.x; e < n; e += blockDim.x) {
+      T x = has ? src[e] : Ops<T>::zero();
+      if (fold) {
+        x = Ops<T>::add(x, gbuf[e]);
+        stash[e] = x;
+      }
+      T uu = reduce1(x);
+      slot[e] = uu;
+      bad |= !Ops<T>::finite(uu);
+      if (MOM) {
+        const T b = Ops<T>::mom(mu, mom[e], uu);
+        mom[e] = b;
+        uu = b;
+      }
+      w[e] = Ops<T>::sgd(w[e], lr, uu);
     }
-    T uu = reduce1(x);
-    slot[e] = uu;
-    bad |= !Ops<T>::finite(uu);
-    if (MOM) {
-      T b = Ops<T>::mom(mu, mom[e], uu);
-      mom[e] = b;
-      uu = b;
-    }
-    w[e] = Ops<T>::sgd(w[e], lr, uu);
   }
-  return bad;
+  // completion is the kernel boundary: ec_direct_publish_kernel (launched
+  // right behind, PDL) reports once every CTA's stores are visible
+  if (__any_sync(0xffffffffu, bad) && (threadIdx.x & 31) == 0) atomicOr(&L->upd_bad, 1u);
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
 }
 
-template <typename T, bool MOM>
-__global__ void __launch_bounds__(256, 3)
-ec_direct_step_kernel(const EcDesc* __restrict__ dp, unsigned long long seq, unsigned int flags,
-                      T* __restrict__ w, T* __restrict__ mom, T lr, T mu, int vec_ok, long long t,
-                      unsigned long long timeout_ns) {
+__global__ void ec_direct_publish_kernel(const EcDesc* __restrict__ dp, unsigned long long seq,
+                                         long long t) {
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+  if (threadIdx.x != 0) return;
   const EcDesc& d = *dp;
   EcLocal* L = d.local;
-  EcHostCtl* H = d.hctl;
-  __shared__ int s_fused, s_contrib, s_fold;
-  __shared__ long long s_g;
-  __shared__ unsigned long long s_status, s_t0;
-  // launched with programmatic stream serialization: this grid may become
-  // resident while the previous step's grid drains; nothing it wrote may be
-  // read before this wait
-  asm volatile("griddepcontrol.wait;" ::: "memory");
-  if (threadIdx.x == 0) {
-    if (blockIdx.x == 0) {
-      const unsigned long long t0 = globaltimer_ns();
-      // a zero-copy call that meets a pending stash folds into it in this pass
-      const int fold = (flags & EC_CF_SRC_GRAD_AUTO) && !*(volatile int*)&L->stash_null;
-      const unsigned long long status = direct_decide_core(d, EC_REQ_CONTRIB, flags, t, 0);
-      L->dec_status = status;
-      L->dec_fold = fold;
-      L->upd_t0 = t0;
-      __threadfence();
-      st_release_gpu(&L->dec_tag, seq + 1);
-    } else {
-      while (ld_acquire_gpu(&L->dec_tag) != seq + 1) __nanosleep(64);
-    }
-    s_g = *(volatile long long*)&L->g;
-    s_contrib = *(volatile int*)&L->contrib;
-    // an accepted offer with activation opens round g == t (P == 1); a refused
-    // one never does, so late_copy and a fused round never meet
-    s_fused = *(volatile int*)&L->snapped;
-    s_fold = *(volatile int*)&L->dec_fold;
-    s_status = *(volatile unsigned long long*)&L->dec_status;
-    s_t0 = *(volatile unsigned long long*)&L->upd_t0;
-  }
-  __syncthreads();
-  T* stash = reinterpret_cast<T*>(d.send[d.rank]);
-  const T* gbuf = reinterpret_cast<const T*>(d.gbuf[d.rank]);
-  const long long n = d.n;
-  if (!s_fused) {
-    // rare: no round this step.  Keep a folded gradient, reply, then the
-    // ordinary wait + update (refused zero-copy offers are copied late)
-    if (s_fold) {
-      const long long tid0 = (long long)blockIdx.x * blockDim.x + threadIdx.x;
-      const long long nth0 = (long long)gridDim.x * blockDim.x;
-      for (long long e = tid0; e < n; e += nth0) stash[e] = Ops<T>::add(stash[e], gbuf[e]);
-    }
-    if (blockIdx.x == 0 && threadIdx.x == 0) direct_reply(d, seq, s_status);
-    update_gen_body<T, MOM>(w, mom, d.ring[d.rank], d.slot_bytes, d.R, L, lr, mu, n, vec_ok, H, t,
-                            timeout_ns, 0, stash, gbuf, dp);
-    return;
-  }
-  const long long g = s_g;
-  const int contrib = s_contrib;
-  const bool has = (contrib & (int)EC_SNAP_DATA) != 0;
-  const T* src = (contrib & (int)EC_SNAP_SRC_GRAD) ? gbuf : stash;
-  T* slot = reinterpret_cast<T*>(d.ring[d.rank] + (g % d.R) * d.slot_bytes);
-  bool bad;
-  if (s_fold) bad = direct_pass<T, MOM, true>(stash, gbuf, stash, slot, w, mom, lr, mu, n, vec_ok, has);
-  else bad = direct_pass<T, MOM, false>(src, nullptr, stash, slot, w, mom, lr, mu, n, vec_ok, has);
-  // the next step's grid may start launching (it waits for our completion)
-  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
-  if (__syncthreads_or(bad) && threadIdx.x == 0) atomicOr(&L->upd_bad, 1u);
-  if (threadIdx.x == 0) {
-    __threadfence();
-    if (atomicAdd(&L->upd_count, 1ull) == gridDim.x - 1) {
-      L->upd_count = 0;
-      L->step_gen = g;
-      DirectStepReport rep{seq, s_status, s_t0, t, atomicExch(&L->upd_bad, 0u) != 0u};
-      direct_publish(d, g, contrib, has ? 1ull : 0ull, &rep);
-    }
-  }
+  const unsigned long long dw = *(volatile unsigned long long*)&L->dec_tag;
+  if ((dw >> 8) != seq + 1 || !(dw & EC_DW_FUSED)) return;   // the fallback reported itself
+  L->step_gen = t;
+  const int contrib = *(volatile int*)&L->contrib;
+  DirectStepReport rep{seq, *(volatile unsigned long long*)&L->dec_status,
+                       *(volatile unsigned long long*)&L->upd_t0, t,
+                       atomicExch(&L->upd_bad, 0u) != 0u};
+  direct_publish(d, t, contrib, (dw & EC_DW_HAS) ? 1ull : 0ull, &rep);
 }
 
 __global__ void ec_post_kernel(EcLocal* L, unsigned long long seq1, unsigned int type,
@@ -1908,6 +1904,7 @@ cudaError_t preload_kernels() {
       (const void*)ec_update_gen_kernel<float, false>, (const void*)ec_update_gen_kernel<double, false>,
       (const void*)ec_direct_step_kernel<float, false>, (const void*)ec_direct_step_kernel<double, false>,
       (const void*)ec_direct_step_kernel<float, true>, (const void*)ec_direct_step_kernel<double, true>,
+      (const void*)ec_direct_publish_kernel,
       (const void*)ec_update_gen_kernel<float, true>, (const void*)ec_update_gen_kernel<double, true>,
   };
   for (const void* f : fns) {
@@ -2088,13 +2085,9 @@ cudaError_t launch_direct_step(int dtype, const EcDesc* d_desc, unsigned long lo
   const int vec_ok = ((((uintptr_t)w) | ((uintptr_t)mom) | ((uintptr_t)ring) | slot_bytes |
                        ((uintptr_t)src0) | ((uintptr_t)src1)) & 15) == 0;
   const int V = dtype == 0 ? 4 : 2;
-  // __launch_bounds__(256, 3): one wave is SMs x 3 blocks
-  long long gb = ((n / V + 1) / 4 + 255) / 256 + 1;
-  const int grid = (int)(gb < (long long)sms() * 3 ? gb : (long long)sms() * 3);
   // programmatic dependent launch: the grid is scheduled while the previous
   // kernel on the stream drains (the kernel's griddepcontrol.wait orders its reads)
   cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = dim3(grid);
   cfg.blockDim = dim3(256);
   cfg.stream = s;
   cudaLaunchAttribute attr[1];
@@ -2102,16 +2095,24 @@ cudaError_t launch_direct_step(int dtype, const EcDesc* d_desc, unsigned long lo
   attr[0].val.programmaticStreamSerializationAllowed = getenv("EC_NO_PDL") ? 0 : 1;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
+  // full-occupancy shape: one CTA per 256 vectors (>= 1 CTA for the tail)
+  const long long nvv = vec_ok ? n / V : 0;
+  cfg.gridDim = dim3((unsigned)((nvv + 255) / 256 > 0 ? (nvv + 255) / 256 : 1));
+  cudaError_t e = cudaErrorInvalidValue;
   if (dtype == 0) {
     auto kern = mom ? ec_direct_step_kernel<float, true> : ec_direct_step_kernel<float, false>;
-    return cudaLaunchKernelEx(&cfg, kern, d_desc, seq, flags, (float*)w, (float*)mom, (float)lr,
-                              (float)mu, vec_ok, t, timeout_ns);
+    e = cudaLaunchKernelEx(&cfg, kern, d_desc, seq, flags, (float*)w, (float*)mom, (float)lr,
+                           (float)mu, vec_ok, t, timeout_ns);
   } else if (dtype == 1) {
     auto kern = mom ? ec_direct_step_kernel<double, true> : ec_direct_step_kernel<double, false>;
-    return cudaLaunchKernelEx(&cfg, kern, d_desc, seq, flags, (double*)w, (double*)mom, lr, mu,
-                              vec_ok, t, timeout_ns);
+    e = cudaLaunchKernelEx(&cfg, kern, d_desc, seq, flags, (double*)w, (double*)mom, lr, mu,
+                           vec_ok, t, timeout_ns);
   }
-  return cudaErrorInvalidValue;
+  if (e != cudaSuccess) return e;
+  counted();
+  cfg.gridDim = dim3(1);
+  cfg.blockDim = dim3(32);
+  return cudaLaunchKernelEx(&cfg, ec_direct_publish_kernel, d_desc, seq, t);
 }
 
 cudaError_t launch_write_u64(unsigned long long* p, unsigned long long v, cudaStream_t s) {
