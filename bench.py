@@ -233,6 +233,14 @@ def main():
         pw.resume()
         barrier()
 
+    def settle():
+        # the bracket of a timed region: the engines are resident by design (a
+        # device-wide synchronize would wait for them forever), so every rank
+        # drains its own streams -- nothing of the warm-up is left in flight
+        barrier()
+        torch.cuda.current_stream().synchronize()
+        barrier()
+
     gen = torch.Generator(device=dev)
     gen.manual_seed(1234 + rank)
     w0 = torch.randn(n, device=dev, generator=gen) * 0.01
@@ -286,6 +294,9 @@ def main():
     host_t = [0.0, 0.0]       # host seconds in train_step_async (issue) / finish_step
     run_steps(args.warmup, lambda t: grads[t % 2])
     quiesce()
+    # the engines were relaunched by quiesce(): their first rounds stay untimed
+    run_steps(2, lambda t: grads[t % 2])
+    settle()
     host_t = [0.0, 0.0]
     launches0 = _lib.lib.ec_launch_count()
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -336,8 +347,9 @@ def main():
     host_grad = torch.randn(n, generator=torch.Generator().manual_seed(7 + rank)).pin_memory()
     dgrad = gbuf                          # the H2D copy lands in the registered bucket
     h2d = lambda i: dgrad.copy_(host_grad, non_blocking=True)  # noqa: E731
-    run_steps(2, lambda t: dgrad, pre=h2d)
     quiesce()
+    run_steps(2, lambda t: dgrad, pre=h2d)
+    settle()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e2e_steps = max(5, args.steps // 2)
     e0.record()
@@ -456,16 +468,16 @@ def bench_allreduce(args, pw, rank, world, dev, barrier, max_over_ranks, quiesce
 
         from paper_1908_04207_b200.harness import _round as rnd
 
-        for t in range(3):
-            rnd(h, t)
         quiesce()
-        t_next = 3
+        for t in range(3):        # warm-up with the (re)launched engines, untimed
+            rnd(h, t)
+        barrier()
         from paper_1908_04207_b200.harness import rounds_back_to_back
         # back-to-back rounds on the stream (device-side waits, no host round
         # trip), all-arrive so nap = P: like nccl-tests' busbw
         ms = max_over_ranks(rounds_back_to_back(h, 3, rounds)) / rounds
         busbw = 2 * (world - 1) / world * 4 * n / (ms / 1e3) / 1e9
-        quiesce()
+        barrier()
         # the same through the blocking call_round-style API (host waits each round)
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record()
@@ -506,9 +518,12 @@ def bench_imbalance(args, pw, rank, world, dev, barrier, max_over_ranks, quiesce
         attach_delivery_tracking(h, st)
         naps = []
         quiesce()
+        drive(train_step(st, None, h, grad=g))   # step 0 with the relaunched engine, untimed
+        barrier()
+        torch.cuda.current_stream().synchronize()
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record()
-        for t in range(args.imb_steps):
+        for t in range(1, args.imb_steps + 1):
             device_delay(inject_delay(rank, t, model, world))
             _, res, _g = drive(train_step(st, None, h, grad=g))
             naps.append(res.nap)

@@ -743,7 +743,13 @@ __device__ void engine_controller(const EcDesc& d, unsigned long long epoch) {
           contributed_round = t;
           status = 1;
           t_req = globaltimer_ns();
-          if (fl & 4u) {  // all-arrive
+          if ((fl & 4u) && (fl & 2u) && d.flavor != 2 && !d.replay) {
+            // all-arrive, solo/sync: every rank boards with its own activation,
+            // so each snapshots its own fresh offer without broadcasting one;
+            // the round still starts only when every rank's snapshot is in
+            // (nap = P), one NVLink exchange sooner than the arrival barrier
+            internal_act = 1;
+          } else if (fl & 4u) {  // all-arrive (majority: the initiator activates)
             push_all(2, (unsigned long long)g + 1);
             arrive_pending = 1;
             arrive_activate = (fl & 2u) ? 1 : 0;
@@ -1303,6 +1309,7 @@ __global__ void __launch_bounds__(256, 6)
 ec_fold_auto_kernel(T* __restrict__ stash, const T* __restrict__ grad, long long n,
                     EcLocal* __restrict__ L, int vec_ok, unsigned long long seq1, unsigned flags,
                     long long t, int zero_copy) {
+  asm volatile("griddepcontrol.wait;" ::: "memory");   // PDL-launched behind the previous step
   const int add = *(volatile int*)&L->stash_null ? 0 : 1;
   if (zero_copy && !add) {
     // null stash and the gradient sits in the registered buffer: offer it in
@@ -1635,6 +1642,8 @@ __device__ __forceinline__ void update_gen_body(T* __restrict__ w, T* __restrict
     }
     bad = update_body<T, MOM, MOM ? 2 : 4>(w, mom, u, lr, mu, n, vec_ok);
   }
+  // the next step's offer kernel may be scheduled now (it waits for our completion)
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
   if (H == nullptr) return;
   if (__syncthreads_or(bad) && threadIdx.x == 0) atomicOr(&L->upd_bad, 1u);
   if (threadIdx.x == 0) {
@@ -2029,13 +2038,25 @@ cudaError_t launch_fold_auto(int dtype, void* stash, const void* grad, long long
   const int vec_ok = ((((uintptr_t)stash) | ((uintptr_t)grad)) & 15) == 0;
   const int V = dtype == 0 ? 4 : 2;
   const int grid = grid_for((n / V + 1) / 2 + 1, 256);
+  // programmatic dependent launch: scheduled while the previous step's update
+  // kernel drains (griddepcontrol.wait in the kernel orders every read)
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(256);
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = getenv("EC_NO_PDL") ? 0 : 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
   if (dtype == 0)
-    ec_fold_auto_kernel<float><<<grid, 256, 0, s>>>((float*)stash, (const float*)grad, n, L, vec_ok, seq1, flags, t, zero_copy);
-  else if (dtype == 1)
-    ec_fold_auto_kernel<double><<<grid, 256, 0, s>>>((double*)stash, (const double*)grad, n, L, vec_ok, seq1, flags, t, zero_copy);
-  else
-    ec_fold_auto_kernel<long long><<<grid, 256, 0, s>>>((long long*)stash, (const long long*)grad, n, L, vec_ok, seq1, flags, t, zero_copy);
-  return cudaGetLastError();
+    return cudaLaunchKernelEx(&cfg, ec_fold_auto_kernel<float>, (float*)stash, (const float*)grad, n, L,
+                              vec_ok, seq1, flags, t, zero_copy);
+  if (dtype == 1)
+    return cudaLaunchKernelEx(&cfg, ec_fold_auto_kernel<double>, (double*)stash, (const double*)grad, n,
+                              L, vec_ok, seq1, flags, t, zero_copy);
+  return cudaLaunchKernelEx(&cfg, ec_fold_auto_kernel<long long>, (long long*)stash,
+                            (const long long*)grad, n, L, vec_ok, seq1, flags, t, zero_copy);
 }
 
 cudaError_t launch_wait_done(EcLocal* L, EcHostCtl* H, long long t, unsigned long long timeout_ns,
