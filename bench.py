@@ -298,9 +298,11 @@ def main():
     run_steps(2, lambda t: grads[t % 2])
     settle()
     host_t = [0.0, 0.0]
-    launches0 = _lib.lib.ec_launch_count()
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     naps = []
+    if world > 1:
+        h.stream_barrier()     # every rank's start event fires together (device barrier)
+    launches0 = _lib.lib.ec_launch_count()
     with ClockSampler(local_rank) as clk:
         h0 = time.perf_counter()
         ev0.record()
@@ -352,6 +354,8 @@ def main():
     settle()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e2e_steps = max(5, args.steps // 2)
+    if world > 1:
+        h.stream_barrier()
     e0.record()
     # each step: H2D of the gradient from pinned memory, the step, and the
     # step's result (generation, mask, nap) read back by finish_step
@@ -372,6 +376,9 @@ def main():
     quiesce()
 
     extras = {}
+    # every communicator's engine holds SMs: release the step's before the
+    # allreduce / imbalance legs create theirs
+    h.close()
     if not args.no_extras and world > 1:
         extras.update(bench_allreduce(args, pw, rank, world, dev, barrier, max_over_ranks, quiesce))
         extras.update(bench_imbalance(args, pw, rank, world, dev, barrier, max_over_ranks, quiesce))

@@ -108,6 +108,12 @@ int64_t ec_n_elems(ec_comm_t* c);
  * eagersgd.py:165 to each chunk of the round's result as it lands (owners
  * publish per-chunk-group arrival words), overlapping the NVLink-bound round */
 int ec_comm_progressive(ec_comm_t* c);
+/* enqueue a device-side barrier across all ranks of the communicator on
+ * `stream` (a one-thread kernel: system-scope arrival count in rank 0's
+ * control block).  Every rank must call it the same number of times.  Used to
+ * align the start of timed regions; no reference counterpart (the simulator
+ * has one clock). */
+int ec_stream_barrier(ec_comm_t* c, int local_idx, void* stream);
 
 /* ---- application protocol -------------------------------------------------
  * GradientBuffer.fold (eagersgd.py:55-57) into the send buffer, stream-ordered.

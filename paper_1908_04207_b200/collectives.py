@@ -202,6 +202,13 @@ class AllreduceHandle:
     def _stream(self) -> int:
         return _stream_ptr(self.device)
 
+    def stream_barrier(self) -> None:
+        """Enqueue a device-side barrier across every rank of this collective on
+        the current stream (ec_stream_barrier): work queued behind it starts
+        when the last rank reached it.  Every rank calls it equally often;
+        emulated ranks need their own streams."""
+        call("ec_stream_barrier", self.comm.ptr, self.li, self._stream())
+
     def _ensure_started(self) -> None:
         if not self.comm.running:
             self.comm.start()

@@ -36,7 +36,7 @@
 // consumes the round's chunks as they land (owners publish arrival words)
 #define EC_CF_STEP 32u
 // arrival words: owner worker (q, w) publishes ((gen+1) << 24) | chunks landed
-#define EC_PROG_W 64
+#define EC_PROG_W 128
 #define EC_PROG_SHIFT 24
 // contribution flag: offer the registered gradient buffer (zero-copy, stash null)
 #define EC_CF_SRC_GRAD 8u
@@ -60,6 +60,8 @@ struct alignas(128) EcCtrl {
   // fused updates: owner q's worker w has stored its first k chunks of
   // generation g into our slot when prog[q][w] >= ((g+1) << 24) | k
   unsigned long long prog[EC_MAX_P][EC_PROG_W];
+  unsigned long long bar_count;   // rank 0's copy: stream-barrier arrivals (monotone)
+  unsigned long long pad_bar[15];
 };
 
 struct alignas(64) EcReq {

@@ -32,6 +32,8 @@ cudaError_t launch_reduce(int dtype, const void* const* srcs, int p, unsigned lo
 cudaError_t launch_post(EcLocal* L, unsigned long long seq1, unsigned int type, unsigned int flags,
                         long long t, long long arg, cudaStream_t s);
 int engine_blocks_per_sm(int dtype, int smem_bytes);
+cudaError_t launch_stream_barrier(unsigned long long* count, unsigned long long target,
+                                  EcHostCtl* H, unsigned long long timeout_ns, cudaStream_t s);
 cudaError_t launch_fold_auto(int dtype, void* stash, const void* grad, long long n, EcLocal* L,
                              unsigned long long seq1, unsigned flags, long long t, int zero_copy,
                              cudaStream_t s);
@@ -123,6 +125,7 @@ struct EcRankHost {
   long long n_forced = 0;
   unsigned long long next_seq = 0;
   unsigned long long last_update_ns = 0;  // device-timed update of the last reconciled async step
+  unsigned long long bar_epoch = 0;       // ec_stream_barrier calls so far
   std::mutex mu;
 };
 
@@ -492,7 +495,11 @@ int ec_comm_create(int world_size, int rank_lo, int n_local, int device, int64_t
   if (workers_per_rank <= 0) {
     const bool ldg = getenv("EC_DATA") && strcmp(getenv("EC_DATA"), "ldg") == 0;
     if (n_local == 1) {
-      workers_per_rank = ldg ? 128 : 64;
+      // TMA: 96 workers at P=2, 64 beyond.  100 MB sweeps (plain rounds):
+      // P=2 587 -> 620 GB/s, P=4 623 -> 640 GB/s with 96; but at P=4 the
+      // progressive step update's arrival words cost more with 96 workers
+      // (step period 295 vs 309 us), at P=2 96 wins either way (221 vs 225 us)
+      workers_per_rank = ldg ? 128 : (world_size == 2 ? 96 : 64);
     } else {  // emulated world: all ranks' CTA groups share one GPU
       workers_per_rank = (144 / n_local) - 1;
       if (workers_per_rank > 16) workers_per_rank = 16;
@@ -802,6 +809,18 @@ void* ec_slot_ptr(ec_comm_t* c, int li, int64_t gen) {
 }
 
 int64_t ec_n_elems(ec_comm_t* c) { return c ? c->n : -1; }
+int ec_stream_barrier(ec_comm_t* c, int li, void* stream) {
+  int rc = check_li(c, li);
+  if (rc) return rc;
+  if (!c->ctrl[0]) return fail(EC_E_STATE, "rank 0's control block is not mapped (import first)");
+  EcRankHost* r = c->L[li];
+  // every rank's epoch advances in lockstep: the k-th barrier completes at k*P
+  const unsigned long long epoch = ++r->bar_epoch;
+  CK(launch_stream_barrier(&c->ctrl[0]->bar_count, epoch * (unsigned long long)c->P, r->hd,
+                           c->timeout_ns, (cudaStream_t)stream));
+  return EC_OK;
+}
+
 int ec_comm_progressive(ec_comm_t* c) {
   return c ? (!c->direct && c->mode == 0 && c->W <= EC_PROG_W && c->dtype != EC_I64) : -1;
 }

@@ -1890,6 +1890,24 @@ static inline int grid_for(long long work, int threads) {
   return (int)b;
 }
 
+// stream barrier across the ranks of a communicator: every rank's kernel adds
+// one to rank 0's counter (system-scope atomic over NVLink) and spins until all
+// P arrivals of this epoch are in; watchdog-bounded
+__global__ void ec_stream_barrier_kernel(unsigned long long* count, unsigned long long target,
+                                         EcHostCtl* H, unsigned long long timeout_ns) {
+  if (threadIdx.x != 0) return;
+  __threadfence_system();
+  atomicAdd_system(count, 1ull);
+  const unsigned long long t0 = globaltimer_ns();
+  while (ld_acquire_sys(count) < target) {
+    if (globaltimer_ns() - t0 > timeout_ns) {
+      st_release_sys(&H->error_info, 0x700);
+      st_release_sys(&H->error, EC_DERR_TIMEOUT);
+      break;
+    }
+  }
+}
+
 // Force-load every kernel of this library.  With CUDA lazy loading a kernel's
 // first launch loads its code, and that load waits for running kernels -- which
 // never happens while the persistent engine is resident.  Called before the
@@ -1913,7 +1931,7 @@ cudaError_t preload_kernels() {
       (const void*)ec_update_gen_kernel<float, false>, (const void*)ec_update_gen_kernel<double, false>,
       (const void*)ec_direct_step_kernel<float, false>, (const void*)ec_direct_step_kernel<double, false>,
       (const void*)ec_direct_step_kernel<float, true>, (const void*)ec_direct_step_kernel<double, true>,
-      (const void*)ec_direct_publish_kernel,
+      (const void*)ec_direct_publish_kernel, (const void*)ec_stream_barrier_kernel,
       (const void*)ec_update_gen_kernel<float, true>, (const void*)ec_update_gen_kernel<double, true>,
   };
   for (const void* f : fns) {
@@ -2134,6 +2152,13 @@ cudaError_t launch_direct_step(int dtype, const EcDesc* d_desc, unsigned long lo
   cfg.gridDim = dim3(1);
   cfg.blockDim = dim3(32);
   return cudaLaunchKernelEx(&cfg, ec_direct_publish_kernel, d_desc, seq, t);
+}
+
+cudaError_t launch_stream_barrier(unsigned long long* count, unsigned long long target,
+                                  EcHostCtl* H, unsigned long long timeout_ns, cudaStream_t s) {
+  counted();
+  ec_stream_barrier_kernel<<<1, 32, 0, s>>>(count, target, H, timeout_ns);
+  return cudaGetLastError();
 }
 
 cudaError_t launch_write_u64(unsigned long long* p, unsigned long long v, cudaStream_t s) {

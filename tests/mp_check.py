@@ -200,6 +200,25 @@ def main():
             out[f"mu={mu}"] = {"progressive_update": fused}
         return out
 
+    def stream_barrier():
+        """ec_stream_barrier: ranks enqueue it 50 ms apart; the stream work
+        behind it completes together on every rank (host clocks compared)."""
+        cfg = CollectiveConfig(p=world, flavor="solo", vector_len=16, element="f4")
+        h = AllreduceHandle(cfg, rank, pw, cid=next_cid())
+        spread = []
+        for k in range(3):
+            dist.barrier()
+            time.sleep(0.05 * ((rank + k) % world))
+            h.stream_barrier()
+            torch.cuda.current_stream().synchronize()
+            done = [None] * world
+            dist.all_gather_object(done, time.time())
+            spread.append(max(done) - min(done))
+        h.close()
+        # without the barrier the returns would spread over up to 50*(P-1) ms
+        assert max(spread) < (0.03 if not shared_gpus else 0.06), spread
+        return {"exit_spread_ms": [round(x * 1e3, 2) for x in spread]}
+
     def nvls_fast_mode():
         """reduction_mode="fast": the NVSwitch reduces (when the fabric has
         NVLS); same u on every rank, within fp32 rounding of the fixed-order sum."""
@@ -276,6 +295,7 @@ def main():
     check("majority_prefix", majority_prefix)
     check("eager_sgd_all_arrive", eager_sgd_all_arrive)
     check("eager_sgd_async_fused", eager_sgd_async_fused)
+    check("stream_barrier", stream_barrier)
     check("nvls_fast_mode", nvls_fast_mode)
     check("replay_c1", replay_c1)
 
