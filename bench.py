@@ -296,6 +296,8 @@ def main():
     quiesce()
     # the engines were relaunched by quiesce(): their first rounds stay untimed
     run_steps(2, lambda t: grads[t % 2])
+    clk = ClockSampler(local_rank)       # NVML init and thread start stay outside the region
+    clk.__enter__()
     settle()
     host_t = [0.0, 0.0]
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -303,12 +305,12 @@ def main():
     if world > 1:
         h.stream_barrier()     # every rank's start event fires together (device barrier)
     launches0 = _lib.lib.ec_launch_count()
-    with ClockSampler(local_rank) as clk:
-        h0 = time.perf_counter()
-        ev0.record()
-        upd_ns = run_steps(args.steps, lambda t: grads[t % 2], ev_end=ev1, naps=naps)
-        host_ms = (time.perf_counter() - h0) * 1e3
-        ev1.synchronize()
+    h0 = time.perf_counter()
+    ev0.record()
+    upd_ns = run_steps(args.steps, lambda t: grads[t % 2], ev_end=ev1, naps=naps)
+    host_ms = (time.perf_counter() - h0) * 1e3
+    ev1.synchronize()
+    clk.__exit__(None, None, None)
     launches = _lib.lib.ec_launch_count() - launches0
     host_issue_us, host_finish_us = (x / args.steps * 1e6 for x in host_t)
     ms = ev0.elapsed_time(ev1)
@@ -392,6 +394,25 @@ def main():
                "sample": f"{r['steps']} whole P=1 steps of {n} fp32 ({r['seconds']:.1f} s, "
                          f"oracle restatement, numpy over {r['threads']} threads)"}
 
+    if direct:
+        roofline = {"bound": "hbm", "kernel": upd_kernel, "achieved": upd_gbs, "peak": peak,
+                    "unit": "GB/s", "frac": upd_gbs / peak, "traffic": _traffic("direct_step"),
+                    "bytes_per_launch": upd_bytes, "avg_launch_ms": upd_ms,
+                    "peak_source": peak_kind}
+    else:
+        # with peers the dominant cost is the round's data phase, bound by NVLink
+        # (the HBM-bound update overlaps it chunk by chunk): bus bytes
+        # 2(P-1)/P * 4N per round over the engine's device-timed data phase, vs
+        # the measured B200 peer copy per direction (B200_PROFILING.md)
+        bus = 2 * (world - 1) / world * 4 * n
+        data_us = timeline["data_phase"]
+        roofline = {"bound": "nvlink", "kernel": "ec_engine<float> data phase (round_tma)",
+                    "achieved": bus / (data_us * 1e-6) / 1e9, "peak": 770.0, "unit": "GB/s",
+                    "frac": bus / (data_us * 1e-6) / 1e9 / 770.0, "traffic": None,
+                    "bytes_per_launch": bus, "avg_launch_ms": data_us / 1e3,
+                    "peak_source": "measured peer copy per direction (B200_PROFILING.md)",
+                    "hbm_update": {"kernel": upd_kernel, "bytes_per_launch": upd_bytes,
+                                   "note": "progressive: spans the round, overlapped"}}
     if rank == 0:
         line = {
             "metric": "eager-SGD steps/s (fold + solo partial allreduce + SGD update), "
@@ -408,12 +429,7 @@ def main():
             "e2e": {"value": e2e_value, "unit": "steps/s", "h2d_bytes_per_step": 4 * n,
                     "h2d_copy_gbs": h2d_gbs,
                     "d2h_bytes_per_step": 16},
-            "roofline": {"bound": "hbm", "kernel": upd_kernel,
-                         "achieved": upd_gbs, "peak": peak, "unit": "GB/s",
-                         "frac": upd_gbs / peak,
-                         "traffic": _traffic("direct_step" if direct else "update"),
-                         "bytes_per_launch": upd_bytes, "avg_launch_ms": upd_ms,
-                         "peak_source": peak_kind},
+            "roofline": roofline,
             "local_kernels": {
                 "fold": {"zero_copy": True,
                          "note": ("world of one: no fold launch -- the step kernel offers the "
