@@ -278,10 +278,12 @@ __device__ void round_tma(const EcDesc& d, const char* const* sp, int w, long lo
   const long long off = (g % d.R) * d.slot_bytes;
   const size_t stage_bytes = (size_t)(P + 1) * chb;
   const unsigned npop = (unsigned)__popcll(has);
-  // arrival words for progressive updates: ~6 per worker per round by default
-  // (each costs a full-completion wait and a sys fence on the issuing thread;
-  // measured best at P=2 and P=4)
-  const long long sig = d.sig_every > 0 ? d.sig_every : (mine + 5) / 6 > 1 ? (mine + 5) / 6 : 1;
+  // arrival words for progressive updates: ~4 per worker per round by default.
+  // Each costs a full-completion wait and proxy + sys fences on the issuing
+  // thread (P=4, 100 MB step: data phase 248.7 us without, 253.9 with one
+  // final word, 260.9 with one per 8 chunks, 266.2 per 4); fewer words leave
+  // more of the update after the round (done->offer 46 us with one)
+  const long long sig = d.sig_every > 0 ? d.sig_every : (mine + 3) / 4 > 1 ? (mine + 3) / 4 : 1;
   auto issue = [&](long long k) {  // thread 0: loads of my k-th chunk
     const int s = (int)((it + k) % S);
     const long long c = c0 + w + k * d.W;
