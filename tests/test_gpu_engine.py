@@ -634,3 +634,34 @@ def test_live_rounds_satisfy_lemma1_contracts(flavor):
         gens = [res[(r, t)].rnd for t in range(rounds)]
         assert all(g >= t for t, g in enumerate(gens)) and gens == sorted(gens)
     world.close()
+
+
+def test_engine_budget_refuses_a_communicator_that_cannot_be_resident():
+    """Every engine is a cooperative grid that must be co-resident with the
+    running ones.  Eight emulated ranks fill the device (8 x 17 CTAs of 144 KB
+    shared memory); a second collective gets an error, not a deadlock; after
+    the first is released the same collective fits."""
+    from paper_1908_04207_b200 import _lib
+    world = EmulatedWorld(8)
+    cfg = CollectiveConfig(p=8, flavor="sync", vector_len=1000, element="f4")
+    h0 = [AllreduceHandle(cfg, r, world, cid=0) for r in range(8)]
+    vec = np.arange(1000, dtype=np.float32)
+
+    def sync_round(hs, t):
+        out = [None] * len(hs)
+
+        def body(r):
+            out[r] = drive(hs[r].call_round(t, vec))
+
+        th = [threading.Thread(target=body, args=(r,)) for r in range(len(hs))]
+        [x.start() for x in th]
+        [x.join() for x in th]
+        return out
+
+    assert all(o.nap == 8 for o in sync_round(h0, 0))
+    with pytest.raises(_lib.EcError, match="no room for another engine"):
+        AllreduceHandle(cfg, 0, world, cid=1)
+    world.release(0)
+    h1 = [AllreduceHandle(cfg, r, world, cid=1) for r in range(8)]
+    assert all(o.nap == 8 for o in sync_round(h1, 0))
+    world.close()
