@@ -163,6 +163,12 @@ def warm_device_libraries(device: int) -> None:
         (a @ a).sum().item()
         (a @ a[:, 0]).sum().item()
         torch.cuda.current_blas_handle()
+        # torch's stream pool is created on the first torch.cuda.Stream(); that
+        # first creation was seen to block behind a resident engine
+        for _ in range(2):
+            s = torch.cuda.Stream(device)
+            e = torch.cuda.Event()
+            e.record(s)
         torch.cuda.synchronize(device)
 
 

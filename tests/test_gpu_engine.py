@@ -665,3 +665,15 @@ def test_engine_budget_refuses_a_communicator_that_cannot_be_resident():
     h1 = [AllreduceHandle(cfg, r, world, cid=1) for r in range(8)]
     assert all(o.nap == 8 for o in sync_round(h1, 0))
     world.close()
+
+
+def test_torch_stream_creation_with_resident_engine():
+    """Creating a torch stream while a persistent engine runs must not block
+    (torch's stream pool is initialised when the world is built).  Run in a
+    subprocess with a deadline: a regression fails instead of hanging."""
+    import subprocess
+    import sys
+    script = os.path.join(os.path.dirname(__file__), "stream_late_check.py")
+    res = subprocess.run([sys.executable, script], capture_output=True, text=True, timeout=180)
+    assert res.returncode == 0, res.stdout[-2000:] + res.stderr[-2000:]
+    assert "stream created while the engine runs: True" in res.stdout
