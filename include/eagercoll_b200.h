@@ -114,6 +114,12 @@ int ec_comm_progressive(ec_comm_t* c);
  * align the start of timed regions; no reference counterpart (the simulator
  * has one clock). */
 int ec_stream_barrier(ec_comm_t* c, int local_idx, void* stream);
+/* resume from a checkpoint (extending eagersgd.py:281-299's
+ * EGW1): re-base a parked rank so its next round is `gen`, with its stash
+ * holding an offer (`stash_pending`) or null, and `contributed_round` as the
+ * staleness guard's last contribution.  Every rank resumes at the same gen. */
+int ec_comm_set_generation(ec_comm_t* c, int local_idx, int64_t gen, int stash_pending,
+                           int64_t contributed_round);
 
 /* ---- application protocol -------------------------------------------------
  * GradientBuffer.fold (eagersgd.py:55-57) into the send buffer, stream-ordered.

@@ -30,7 +30,8 @@ from .collectives import (  # noqa: E402,F401
 )
 from .eagersgd import (  # noqa: E402,F401
     DivergenceError, GradientBuffer, TrainState, attach_delivery_tracking, finish_step,
-    resync_models, resync_step, staleness_guard, train_step, train_step_async, training_process,
+    load_state, resync_models, resync_step, save_state, staleness_guard, train_step,
+    train_step_async, training_process,
 )
 from .trace import TraceRecorder  # noqa: E402,F401
 from .transport import DelayModel, Sleep, delayed_ranks, inject_delay  # noqa: E402,F401

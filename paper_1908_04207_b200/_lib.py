@@ -52,6 +52,7 @@ _SIGS = {
     "ec_n_elems": (_i64, [_vp]),
     "ec_comm_progressive": (_i32, [_vp]),
     "ec_stream_barrier": (_i32, [_vp, _i32, _vp]),
+    "ec_comm_set_generation": (_i32, [_vp, _i32, _i64, _i32, _i64]),
     "ec_fold": (_i32, [_vp, _i32, _vp, _i32, _vp]),
     "ec_copy_in": (_i32, [_vp, _i32, _vp, _vp]),
     "ec_post_contribute": (_i32, [_vp, _i32, _i64, _u32, _vp, _P(_u64)]),

@@ -32,6 +32,8 @@ cudaError_t launch_reduce(int dtype, const void* const* srcs, int p, unsigned lo
 cudaError_t launch_post(EcLocal* L, unsigned long long seq1, unsigned int type, unsigned int flags,
                         long long t, long long arg, cudaStream_t s);
 int engine_blocks_per_sm(int dtype, int smem_bytes);
+cudaError_t launch_set_generation(EcLocal* L, EcHostCtl* H, long long gen, int stash_pending,
+                                  long long contributed_round, cudaStream_t s);
 cudaError_t launch_stream_barrier(unsigned long long* count, unsigned long long target,
                                   EcHostCtl* H, unsigned long long timeout_ns, cudaStream_t s);
 cudaError_t launch_fold_auto(int dtype, void* stash, const void* grad, long long n, EcLocal* L,
@@ -809,6 +811,22 @@ void* ec_slot_ptr(ec_comm_t* c, int li, int64_t gen) {
 }
 
 int64_t ec_n_elems(ec_comm_t* c) { return c ? c->n : -1; }
+int ec_comm_set_generation(ec_comm_t* c, int li, int64_t gen, int stash_pending,
+                           int64_t contributed_round) {
+  int rc = check_li(c, li);
+  if (rc) return rc;
+  if (c->running) return fail(EC_E_STATE, "pause the engine before re-basing its generation");
+  if (gen < 0) return fail(EC_E_ARG, "generation must be >= 0");
+  EcRankHost* r = c->L[li];
+  CK(cudaSetDevice(c->device));
+  // the engine's own stream is idle while it is parked
+  cudaError_t e = launch_set_generation(r->local, r->hd, gen, stash_pending ? 1 : 0,
+                                        contributed_round, c->es);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(c->es);
+  if (e != cudaSuccess) return fail(EC_E_CUDA, "set generation: %s", cudaGetErrorString(e));
+  return EC_OK;
+}
+
 int ec_stream_barrier(ec_comm_t* c, int li, void* stream) {
   int rc = check_li(c, li);
   if (rc) return rc;

@@ -1892,6 +1892,34 @@ static inline int grid_for(long long work, int threads) {
   return (int)b;
 }
 
+// resume (checkpoint): re-base a parked rank at generation `gen`
+__global__ void ec_set_generation_kernel(EcLocal* L, EcHostCtl* H, long long gen, int stash_pending,
+                                         long long contributed_round) {
+  if (threadIdx.x != 0) return;
+  L->g = gen;
+  L->hold_from = EC_INF_GEN;
+  L->contributed_round = contributed_round;
+  L->snapped = 0;
+  L->contrib = 0;
+  L->internal_act = 0;
+  L->arrive_pending = 0;
+  L->arrive_activate = 0;
+  L->stash_null = stash_pending ? 0 : 1;
+  L->poison = 0u;
+  L->late_copy = 0;
+  L->pin_dev = ~0ull;
+  __threadfence();
+  st_release_gpu(&L->done_gen1_dev, (unsigned long long)gen);
+  st_release_sys(&H->snap_gen1, (unsigned long long)gen);
+  st_release_sys(&H->done_gen1, (unsigned long long)gen);
+}
+
+cudaError_t launch_set_generation(EcLocal* L, EcHostCtl* H, long long gen, int stash_pending,
+                                  long long contributed_round, cudaStream_t s) {
+  ec_set_generation_kernel<<<1, 32, 0, s>>>(L, H, gen, stash_pending, contributed_round);
+  return cudaGetLastError();
+}
+
 // stream barrier across the ranks of a communicator: every rank's kernel adds
 // one to rank 0's counter (system-scope atomic over NVLink) and spins until all
 // P arrivals of this epoch are in; watchdog-bounded
@@ -1934,6 +1962,7 @@ cudaError_t preload_kernels() {
       (const void*)ec_direct_step_kernel<float, false>, (const void*)ec_direct_step_kernel<double, false>,
       (const void*)ec_direct_step_kernel<float, true>, (const void*)ec_direct_step_kernel<double, true>,
       (const void*)ec_direct_publish_kernel, (const void*)ec_stream_barrier_kernel,
+      (const void*)ec_set_generation_kernel,
       (const void*)ec_update_gen_kernel<float, true>, (const void*)ec_update_gen_kernel<double, true>,
   };
   for (const void* f : fns) {

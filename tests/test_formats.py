@@ -71,3 +71,33 @@ def test_egw1_checkpoint_roundtrip(tmp_path):
     p.write_bytes(raw[:40])
     with pytest.raises(ValueError):
         load_weights(str(p))
+
+
+def test_egs1_state_roundtrip(tmp_path):
+    """Resumable eager-SGD state: weights, stash, momentum,
+    pending rounds, ledger, step and generation survive bit for bit."""
+    from paper_1908_04207_b200.eagersgd import read_state_file, write_state_file
+    rng = np.random.default_rng(3)
+    for dt in (np.float32, np.float64):
+        rec = {"w": rng.standard_normal(1001).astype(dt), "t": 17, "generation": 17,
+               "contributed_round": 15, "rank": 3, "resync_period": 8, "tau": None, "lr": 0.05,
+               "mu": 0.9, "pending": [15, 16], "ledger": {3: 4, 7: 9},
+               "stash": rng.standard_normal(1001).astype(dt),
+               "momentum": rng.standard_normal(1001).astype(dt)}
+        p = tmp_path / f"s{dt.__name__}.egs"
+        write_state_file(str(p), rec)
+        out = read_state_file(str(p))
+        for k in ("w", "stash", "momentum"):
+            assert out[k].dtype == dt and out[k].tobytes() == rec[k].tobytes()
+        assert out["pending"] == [15, 16] and out["ledger"] == {3: 4, 7: 9}
+        assert (out["t"], out["generation"], out["contributed_round"], out["tau"]) == (17, 17, 15, None)
+        raw = p.read_bytes()
+        assert raw[:4] == b"EGS1"
+        p.write_bytes(raw[:-8])
+        with pytest.raises(ValueError):
+            read_state_file(str(p))
+    rec["stash"] = rec["momentum"] = None
+    rec["pending"], rec["tau"] = [], 4
+    write_state_file(str(tmp_path / "n.egs"), rec)
+    out = read_state_file(str(tmp_path / "n.egs"))
+    assert out["stash"] is None and out["momentum"] is None and out["tau"] == 4
