@@ -46,7 +46,8 @@ cudaError_t launch_wait_done(EcLocal* L, EcHostCtl* H, long long t, unsigned lon
 cudaError_t launch_update_gen(int dtype, void* w, void* mom, const char* ring, long long slot_bytes,
                               int R, EcLocal* L, double lr, double mu, long long n, EcHostCtl* H,
                               long long t, unsigned long long timeout_ns, unsigned long long seq1,
-                              void* stash, const void* gbuf, const EcDesc* dp, cudaStream_t s);
+                              void* stash, const void* gbuf, const EcDesc* dp, int progressive,
+                              cudaStream_t s);
 cudaError_t launch_write_u64(unsigned long long* p, unsigned long long v, cudaStream_t s);
 cudaError_t launch_direct_step(int dtype, const EcDesc* d_desc, unsigned long long seq,
                                unsigned int flags, void* w, void* mom, const void* ring,
@@ -1174,16 +1175,16 @@ int ec_step_async(ec_comm_t* c, int li, int64_t t, const void* grad, uint32_t fl
     if ((rc = reserve_seq(c, r, &seq))) return rc;
   }
   const bool zero_copy = grad == r->gbuf;
+  // progressive update: the update kernel behind this offer consumes the
+  // round's chunks as they land (owners publish arrival words to us)
+  const void* mom_eff = (mom && mu != 0.0) ? mom : nullptr;
+  const bool prog = !c->direct && ec_comm_progressive(c) == 1 && !getenv("EC_NO_PROGRESSIVE") &&
+                    ((((uintptr_t)w) | ((uintptr_t)mom_eff)) & 15) == 0;
   if (!(c->direct && zero_copy)) {
     // fold (+ the offer's post, fused into the fold's last CTA, engine mode).
     // A world of one offering its registered buffer needs no fold launch: the
     // step kernel offers it in place, or folds it into a pending stash in-pass
     ProfScope ps(0, stream);
-    // progressive update: the update kernel behind this offer consumes the
-    // round's chunks as they land (owners publish arrival words to us)
-    const void* mom_eff = (mom && mu != 0.0) ? mom : nullptr;
-    const bool prog = ec_comm_progressive(c) == 1 && !getenv("EC_NO_PROGRESSIVE") &&
-                      ((((uintptr_t)w) | ((uintptr_t)mom_eff)) & 15) == 0;
     CK(launch_fold_auto(c->dtype, r->send, grad, c->n, r->local, c->direct ? 0 : seq + 1,
                         (flags & 7u) | (prog ? EC_CF_STEP : 0u), t, zero_copy ? 1 : 0, s));
   }
@@ -1203,7 +1204,7 @@ int ec_step_async(ec_comm_t* c, int li, int64_t t, const void* grad, uint32_t fl
     ProfScope ps(1, stream);
     CK(launch_update_gen(c->dtype, w, (mom && mu != 0.0) ? mom : nullptr, r->ring, c->slot_bytes, c->R,
                          r->local, lr, mu, c->n, r->hd, t, c->timeout_ns, seq + 1, r->send,
-                         r->gbuf, c->d_descs + li, s));
+                         r->gbuf, c->d_descs + li, prog ? 1 : 0, s));
   }
   if (seq_out) *seq_out = seq;
   return EC_OK;
