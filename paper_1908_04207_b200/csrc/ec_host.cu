@@ -498,11 +498,11 @@ int ec_comm_create(int world_size, int rank_lo, int n_local, int device, int64_t
   if (workers_per_rank <= 0) {
     const bool ldg = getenv("EC_DATA") && strcmp(getenv("EC_DATA"), "ldg") == 0;
     if (n_local == 1) {
-      // TMA: 96 workers at P=2, 64 beyond.  100 MB sweeps (plain rounds):
-      // P=2 587 -> 620 GB/s, P=4 623 -> 640 GB/s with 96; but at P=4 the
-      // progressive step update's arrival words cost more with 96 workers
-      // (step period 295 vs 309 us), at P=2 96 wins either way (221 vs 225 us)
-      workers_per_rank = ldg ? 128 : (world_size == 2 ? 96 : 64);
+      // TMA: 96 workers at P=2, 80 beyond.  100 MB sweeps (plain rounds):
+      // P=2 587 -> 620 GB/s, P=4 623 -> 640 GB/s with 96 vs 64; in the P=4
+      // step (progressive update beside the round) 80 is best (period 285-287
+      // vs 290 us for 64 and 96), at P=2 96 wins (209 vs 211 us)
+      workers_per_rank = ldg ? 128 : (world_size == 2 ? 96 : 80);
     } else {  // emulated world: all ranks' CTA groups share one GPU
       workers_per_rank = (144 / n_local) - 1;
       if (workers_per_rank > 16) workers_per_rank = 16;
