@@ -173,7 +173,7 @@ struct EcDesc {
   int mode;                           // data phase: 0 = fused TMA, 1 = two-phase ld.cg pull,
                                       // 2 = NVLS (multimem.ld_reduce / multimem.st, fast mode)
   int chv, stages;                    // TMA chunk (16-B vectors) and pipeline depth
-  int sig_every;                      // chunks per arrival word (progressive updates; 0 = ~6/round)
+  int sig_every;                      // chunks per arrival word (progressive updates; 0 = ~4/round)
   int smem_bytes;
   long long n, nvec;                  // elements, whole 16-B vectors
   long long slot_bytes;
