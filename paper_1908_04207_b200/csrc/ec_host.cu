@@ -969,8 +969,22 @@ int ec_gen_info(ec_comm_t* c, int li, int64_t gen, uint64_t* mask, uint64_t* has
   unsigned long long g1 = aload(&lg->gen1);
   unsigned long long m = aload(&lg->mask), hm = aload(&lg->has), np = aload(&lg->nap);
   __atomic_thread_fence(__ATOMIC_ACQUIRE);
-  if (aload(&lg->gen1) != g1 || g1 != (unsigned long long)gen + 1)
-    return fail(EC_E_STATE, "generation %lld fell out of the %d-entry log", (long long)gen, EC_LOG_RING);
+  if (aload(&lg->gen1) != g1 || g1 != (unsigned long long)gen + 1) {
+    if (g1 > (unsigned long long)gen + 1 || (long long)aload(&r->h->done_gen1) > gen + EC_LOG_RING)
+      return fail(EC_E_STATE, "generation %lld fell out of the %d-entry log", (long long)gen, EC_LOG_RING);
+    // done says the entry exists: its stores are in flight (never observed
+    // since the tag moved before the publisher's fence; kept as a guard)
+    Backoff bo;
+    while (aload(&lg->gen1) != (unsigned long long)gen + 1) {
+      if (bo.expired(1000))
+        return fail(EC_E_STATE, "generation %lld: log entry not published", (long long)gen);
+      bo.pause();
+    }
+    __atomic_thread_fence(__ATOMIC_ACQUIRE);
+    m = aload(&lg->mask);
+    hm = aload(&lg->has);
+    np = aload(&lg->nap);
+  }
   if (mask) *mask = m;
   if (has) *has = hm;
   if (nap) *nap = (int)np;
@@ -984,6 +998,11 @@ int ec_gen_times(ec_comm_t* c, int li, int64_t gen, uint64_t* t5) {
   if (gen < 0 || (long long)aload(&r->h->done_gen1) <= gen)
     return fail(EC_E_STATE, "generation %lld has not completed", (long long)gen);
   EcLog* lg = &r->h->log[gen % EC_LOG_RING];
+  {
+    // done says the entry exists; wait out stores still in flight (guard)
+    Backoff bo;
+    while (aload(&lg->gen1) < (unsigned long long)gen + 1 && !bo.expired(1000)) bo.pause();
+  }
   unsigned long long g1 = aload(&lg->gen1);
   t5[0] = aload(&lg->t_snap);
   t5[1] = aload(&lg->t_cmd);

@@ -873,10 +873,12 @@ __device__ void engine_controller(const EcDesc& d, unsigned long long epoch) {
         st_relaxed_sys(&lg->t_done, t_done);
         st_relaxed_sys(&lg->t_req, t_req);
         st_relaxed_sys(&lg->poison, poison ? 1ull : 0ull);
+        // the entry's own generation tag is record data (ring-overwrite check):
+        // it must be visible before done_gen1, so it goes before the fence
+        st_relaxed_sys(&lg->gen1, (unsigned long long)g + 1);
         t_req = 0;
         st_release_gpu(&L->done_gen1_dev, (unsigned long long)g + 1);  // device waiters first
         fence_acq_rel_sys();                     // log entry before the host-visible flags
-        st_relaxed_sys(&lg->gen1, (unsigned long long)g + 1);
         st_relaxed_sys(&H->done_gen1, (unsigned long long)g + 1);
         ++g;
         snapped = 0;
@@ -1062,8 +1064,8 @@ __device__ void direct_publish(const EcDesc& d, long long g, int contrib, unsign
     st_relaxed_sys(&H->stepbad[ts], step->bad ? 1ull : 0ull);
     st_relaxed_sys(&H->stepns[ts], tn - step->t0);
   }
+  st_relaxed_sys(&lg->gen1, (unsigned long long)g + 1);   // record data: before the fence
   fence_acq_rel_sys();
-  st_relaxed_sys(&lg->gen1, (unsigned long long)g + 1);
   st_relaxed_sys(&H->snap_gen1, (unsigned long long)g + 1);
   st_relaxed_sys(&H->done_gen1, (unsigned long long)g + 1);
   st_relaxed_gpu(&L->done_gen1_dev, (unsigned long long)g + 1);
