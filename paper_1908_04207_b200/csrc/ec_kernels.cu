@@ -725,8 +725,8 @@ __device__ void engine_controller(const EcDesc& d, unsigned long long epoch) {
           if (fl & EC_CF_SRC_GRAD) *(volatile int*)&L->late_copy = 1;  // keep the gradient
         } else if (t > g) {
           status = 5;
+          st_release_sys(&H->error_info, (unsigned long long)t);   // info before the code
           st_release_sys(&H->error, EC_DERR_ORDER);
-          st_release_sys(&H->error_info, (unsigned long long)t);
         } else if (d.replay && forced_bit(g) != 1) {
           status = 2;
           if (fl & EC_CF_SRC_GRAD) *(volatile int*)&L->late_copy = 1;
