@@ -503,6 +503,18 @@ def main():
             "gpu_launches": int(launches),
         }
         line.update(extras)
+        # BASELINE.json's metric is a pair: solo/majority allreduce bus GB/s at
+        # 100 MB, and eager-SGD steps/s under imbalance.  `value` is the config-2
+        # step rate (defined at every N, including N=1 where neither half
+        # exists); both halves sit here at N > 1 (details in allreduce / imbalance)
+        line["baseline_metric"] = ("solo/majority allreduce bus GB/s at 100MB; "
+                                   "eager-SGD steps/s under imbalance")
+        if "allreduce" in extras:
+            line["bus_gbs_100mb"] = {f: v["busbw_gbs"] for f, v in extras["allreduce"].items()}
+        if "imbalance" in extras:
+            line["steps_per_s_under_imbalance"] = {
+                f: v["steps_per_s"] for f, v in extras["imbalance"].items()
+                if isinstance(v, dict) and "steps_per_s" in v}
         print(json.dumps(line), flush=True)
     pw.close()
     if world > 1:
