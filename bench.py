@@ -562,21 +562,29 @@ def bench_allreduce(args, pw, rank, world, dev, barrier, max_over_ranks, quiesce
             rnd(h, t)
         barrier()
         from paper_1908_04207_b200.harness import rounds_back_to_back
-        # back-to-back rounds on the stream (device-side waits, no host round
-        # trip), all-arrive so nap = P: like nccl-tests' busbw
-        ms = max_over_ranks(rounds_back_to_back(h, 3, rounds)) / rounds
+        # back-to-back rounds on the stream, all-arrive so nap = P, like
+        # nccl-tests' busbw: posted with no wait between them (the engine takes
+        # each next offer the moment the previous round completes), and -- for
+        # comparison -- each behind a device-side wait for the previous one
+        from paper_1908_04207_b200.harness import rounds_pipelined
+        ms = max_over_ranks(rounds_pipelined(h, 3, rounds)) / rounds
         busbw = 2 * (world - 1) / world * 4 * n / (ms / 1e3) / 1e9
+        barrier()
+        ms_ser = max_over_ranks(rounds_back_to_back(h, 3 + rounds, rounds)) / rounds
         barrier()
         # the same through the blocking call_round-style API (host waits each round)
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record()
-        for t in range(3 + rounds, 3 + 2 * rounds):
+        for t in range(3 + 2 * rounds, 3 + 3 * rounds):
             rnd(h, t)
         e1.record()
         e1.synchronize()
         ms_sync = max_over_ranks(e0.elapsed_time(e1)) / rounds
         out[flavor] = {"busbw_gbs": busbw, "us_per_round": ms * 1e3, "bytes": 4 * n,
                        "frac_of_900": busbw / 900.0, "frac_of_770_measured_peer": busbw / 770.0,
+                       "serialized": {"us_per_round": ms_ser * 1e3,
+                                      "busbw_gbs": 2 * (world - 1) / world * 4 * n
+                                      / (ms_ser / 1e3) / 1e9},
                        "blocking_api": {"us_per_round": ms_sync * 1e3,
                                         "busbw_gbs": busbw * ms / ms_sync}}
         h.close()

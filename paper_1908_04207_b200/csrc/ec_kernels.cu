@@ -717,6 +717,15 @@ __device__ void engine_controller(const EcDesc& d, unsigned long long epoch) {
         arg = (long long)ld_relaxed_sys((const unsigned long long*)&q->arg);
       }
       unsigned long long status = 3;  // OK
+      // An offer for the NEXT generation while this rank has already done its
+      // part for round g (contributed or snapshotted): keep it at the head of
+      // the queue until g completes, then take it at once -- back-to-back
+      // rounds posted without host waits pay no post latency between them.
+      // (The application API never posts early; a buffer re-offered early must
+      // not change while round g still reads it.)
+      if (type == EC_REQ_CONTRIB && !(fl & EC_CF_POISON) && t == g + 1 &&
+          (snapped || contributed_round == g))
+        break;
       if (type == EC_REQ_CONTRIB) {
         if (fl & EC_CF_POISON) {
           status = 4;

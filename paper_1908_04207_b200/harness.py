@@ -89,6 +89,35 @@ def rounds_back_to_back(h, t0, k, all_arrive=True):
     return e0.elapsed_time(e1)
 
 
+def rounds_pipelined(h, t0, k, all_arrive=True):
+    """k rounds t0..t0+k-1 posted back to back on the current stream with no
+    wait between them (the nccl-tests pattern: the same buffer every round);
+    the engine defers each next-generation offer until the previous round
+    completes, then takes it at once.  One device-side wait behind the last.
+    Returns device ms between the first offer and the last completion."""
+    import torch
+
+    from . import _lib
+    from ._lib import call
+    h._ensure_started()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    seqs = []
+    e0.record()
+    for t in range(t0, t0 + k):
+        flags = _lib.EC_CF_FRESH | (_lib.EC_CF_ALL_ARRIVE if all_arrive else 0) | \
+            (_lib.EC_CF_ACTIVATE if h._may_activate(t) else 0)
+        seq = C.c_uint64()
+        fn = "ec_round_async" if t == t0 + k - 1 else "ec_post_contribute"
+        call(fn, h.comm.ptr, h.li, t, flags, h._stream(), C.byref(seq))
+        seqs.append(seq.value)
+    e1.record()
+    e1.synchronize()
+    for s in seqs:
+        h._reply(s)
+    h._wait(t0 + k - 1, 60.0, pin=False)
+    return e0.elapsed_time(e1)
+
+
 def allreduce_sweep(world, rank, p, sizes_bytes, flavor="solo", rounds_cap=50, workers=None,
                     max_over_ranks=lambda x: x, barrier=lambda: None, reduction_mode="fixed_order"):
     """Bus bandwidth of the partial allreduce per payload size (fp32)."""
@@ -117,6 +146,9 @@ def allreduce_sweep(world, rank, p, sizes_bytes, flavor="solo", rounds_cap=50, w
         barrier()
         b2b_ms = rounds_back_to_back(h, 3 + rounds, rounds)
         b2b_us = max_over_ranks(b2b_ms * 1e3 / rounds)
+        barrier()
+        pipe_ms = rounds_pipelined(h, 3 + 2 * rounds, rounds)
+        pipe_us = max_over_ranks(pipe_ms * 1e3 / rounds)
         phases = [_gen_times(h, g) for g in range(2, 3 + rounds)]
         prev, phases = phases[0], phases[1:]
         data_us = sum((x[3] - x[1]) for x in phases) / rounds / 1e3
@@ -131,6 +163,8 @@ def allreduce_sweep(world, rank, p, sizes_bytes, flavor="solo", rounds_cap=50, w
                     "busbw_gbs": bus / (round_us * 1e-6) / 1e9,
                     "us_per_round_b2b": b2b_us,
                     "busbw_b2b_gbs": bus / (b2b_us * 1e-6) / 1e9,
+                    "us_per_round_pipelined": pipe_us,
+                    "busbw_pipelined_gbs": bus / (pipe_us * 1e-6) / 1e9,
                     "device_data_us": data_us, "device_rs_us": max_over_ranks(rs_us),
                     "busbw_device_gbs": bus / (data_us * 1e-6) / 1e9 if data_us > 0 else None,
                     "snap_to_start_us": max_over_ranks(snap_wait_us),
