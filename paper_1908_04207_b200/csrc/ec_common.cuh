@@ -35,6 +35,8 @@
 // contribution flag: the offer's step update kernel follows it on the stream and
 // consumes the round's chunks as they land (owners publish arrival words)
 #define EC_CF_STEP 32u
+// internal: a host-posted request the engine's poller copied into the device ring
+#define EC_CF_HOSTPOSTED 0x200u
 // arrival words: owner worker (q, w) publishes ((gen+1) << 24) | chunks landed
 #define EC_PROG_W 128
 #define EC_PROG_SHIFT 24
@@ -127,6 +129,12 @@ struct alignas(128) EcLocal {
   int step_fused;                  // the current async step updates progressively (arrival words)
   int pad8;
   unsigned long long upd_next_item;  // progressive update: next chunk item to claim
+  // host poller (engine thread 32): mirrors of host-mapped words, so the
+  // controller thread never stalls on a PCIe read
+  unsigned long long hp_seq;       // changes of the mirrored host pin (monotone)
+  unsigned long long hp_lo;        // mirrored host pin (EcHostCtl::pin_lo)
+  unsigned long long hp_ps;        // the pin_seq it was read with (acknowledged)
+  unsigned long long hp_stop;      // epoch whose stop request the poller saw
   EcReq dreq[EC_REQ_RING];         // stream-posted requests (device copy of the ring)
 };
 

@@ -673,23 +673,25 @@ __device__ void engine_controller(const EcDesc& d, unsigned long long epoch) {
     return (int)((d.forced[gen] >> r) & 1ull);
   };
 
-  unsigned long long last_host_poll = 0;
-  // host pin, refreshed with every host poll and acknowledged (ec_wait's pin
-  // waits for the ack, so the per-round check never reads host memory)
+  // host pin, mirrored into device memory by the host poller (engine thread
+  // 32) and acknowledged HERE after this thread read it, so every later
+  // snapshot check sees it (ec_wait's pin waits for the ack)
   unsigned long long host_pin = ld_relaxed_sys(&H->pin_lo);
+  unsigned long long last_hs = ld_acquire_gpu(&L->hp_seq);
   while (true) {
     bool progress = false;
-    // Host-mapped words cost a PCIe round trip: read them only every ~8 us
-    // (host-posted requests, stop); stream-posted requests arrive through the
-    // device ring and doorbell.
-    const unsigned long long now = globaltimer_ns();
-    const bool poll_host = now - last_host_poll > 8000ull;
-    if (poll_host) last_host_poll = now;
-    if (poll_host) {
-      const unsigned long long ps = ld_acquire_sys(&H->pin_seq);
-      host_pin = ld_relaxed_sys(&H->pin_lo);
-      st_release_sys(&H->pin_ack, ps);  // release: orders the pin_lo read before the ack
-      if (!stopping && ld_relaxed_sys(&H->stop)) {
+    // Host-mapped words cost a PCIe round trip; the poller mirrors them (and
+    // copies host-posted requests into the device ring), so this thread only
+    // reads device memory.
+    {
+      const unsigned long long hs = ld_acquire_gpu(&L->hp_seq);
+      if (hs != last_hs) {
+        host_pin = *(volatile unsigned long long*)&L->hp_lo;
+        // release: orders the pin read before the ack
+        st_release_sys(&H->pin_ack, *(volatile unsigned long long*)&L->hp_ps);
+        last_hs = hs;
+      }
+      if (!stopping && ld_acquire_gpu(&L->hp_stop) == epoch) {
         stopping = true;
         stop_t0 = globaltimer_ns();
       }
@@ -701,21 +703,14 @@ __device__ void engine_controller(const EcDesc& d, unsigned long long epoch) {
       unsigned type, fl;
       long long t, arg;
       bool dev_req = false;
-      if (ld_acquire_gpu(&dq->seq1) == next_req + 1) {
-        type = *(volatile unsigned*)&dq->type;
-        fl = *(volatile unsigned*)&dq->flags;
-        t = *(volatile long long*)&dq->t;
-        arg = *(volatile long long*)&dq->arg;
-        dev_req = true;
-      } else {
-        if (!poll_host) break;
-        EcReq* q = &H->req[next_req % EC_REQ_RING];
-        if (ld_acquire_sys(&q->seq1) != next_req + 1) break;
-        type = ld_relaxed_sys_u32(&q->type);
-        fl = ld_relaxed_sys_u32(&q->flags);
-        t = (long long)ld_relaxed_sys((const unsigned long long*)&q->t);
-        arg = (long long)ld_relaxed_sys((const unsigned long long*)&q->arg);
-      }
+      // stream-posted requests and (copied by the poller) host-posted ones
+      if (ld_acquire_gpu(&dq->seq1) != next_req + 1) break;
+      type = *(volatile unsigned*)&dq->type;
+      fl = *(volatile unsigned*)&dq->flags;
+      t = *(volatile long long*)&dq->t;
+      arg = *(volatile long long*)&dq->arg;
+      dev_req = !(fl & EC_CF_HOSTPOSTED);
+      fl &= ~EC_CF_HOSTPOSTED;
       unsigned long long status = 3;  // OK
       // An offer for the NEXT generation while this rank has already done its
       // part for round g (contributed or snapshotted): keep it at the head of
@@ -815,10 +810,7 @@ __device__ void engine_controller(const EcDesc& d, unsigned long long epoch) {
         // own updater CTAs finish a fused update before upd_fin_gen moves.
         fence_sc_gpu();
         const unsigned long long gr = (unsigned long long)(g - d.R);
-        if (ld_acquire_gpu(&L->pin_dev) <= gr || host_pin <= gr) {
-          go = false;
-          if (host_pin <= gr) last_host_poll = 0;  // re-read the host pin promptly
-        }
+        if (ld_acquire_gpu(&L->pin_dev) <= gr || host_pin <= gr) go = false;
       }
       if (go) {
         push_all(1, (((unsigned long long)g + 1) << EC_SNAP_SHIFT) | (unsigned long long)contrib);
@@ -926,6 +918,51 @@ __device__ void engine_controller(const EcDesc& d, unsigned long long epoch) {
   st_release_sys(&H->exited, epoch);
 }
 
+// engine: host poller (thread 32 of the controller's CTA).  Mirrors the host
+// pin and stop words into EcLocal and copies host-posted requests into the
+// device request ring in sequence order (stream-posted sequence numbers are
+// skipped once their kernel posted them), so the controller thread never
+// stalls on a PCIe read.  Runs until the controller parks.
+__device__ void engine_host_poller(const EcDesc& d, unsigned long long epoch) {
+  EcLocal* L = d.local;
+  EcHostCtl* H = d.hctl;
+  unsigned long long pn = *(volatile unsigned long long*)&L->next_req;   // parked cursor
+  unsigned long long last_ps = ~0ull, last_lo = ~0ull, changes = *(volatile unsigned long long*)&L->hp_seq;
+  while (ld_acquire_gpu(&L->exit_epoch) != epoch) {
+    // the pin moves either through the acknowledged host handshake (pin_seq)
+    // or through a stream-ordered kernel store (ec_set_pin ordered): mirror
+    // both, the latter without an acknowledgement
+    const unsigned long long ps = ld_acquire_sys(&H->pin_seq);
+    const unsigned long long lo = ld_relaxed_sys(&H->pin_lo);
+    if (ps != last_ps || lo != last_lo) {
+      st_relaxed_gpu(&L->hp_lo, lo);
+      st_relaxed_gpu(&L->hp_ps, ps);
+      st_release_gpu(&L->hp_seq, ++changes);
+      last_ps = ps;
+      last_lo = lo;
+    }
+    if (ld_relaxed_sys(&H->stop)) st_release_gpu(&L->hp_stop, epoch);
+    while (true) {
+      EcReq* dq = &L->dreq[pn % EC_REQ_RING];
+      if (ld_acquire_gpu(&dq->seq1) == pn + 1) {   // stream-posted: nothing to copy
+        ++pn;
+        continue;
+      }
+      EcReq* q = &H->req[pn % EC_REQ_RING];
+      if (ld_acquire_sys(&q->seq1) != pn + 1) break;
+      volatile EcReq* v = dq;
+      v->type = ld_relaxed_sys_u32(&q->type);
+      v->flags = ld_relaxed_sys_u32(&q->flags) | EC_CF_HOSTPOSTED;
+      v->t = (long long)ld_relaxed_sys((const unsigned long long*)&q->t);
+      v->arg = (long long)ld_relaxed_sys((const unsigned long long*)&q->arg);
+      __threadfence();
+      st_release_gpu(&dq->seq1, pn + 1);
+      ++pn;
+    }
+    __nanosleep(1000);
+  }
+}
+
 template <typename T>
 __global__ void __launch_bounds__(256, 2)
 ec_engine(const EcDesc* __restrict__ descs, int blocks_per_rank, unsigned long long epoch) {
@@ -934,6 +971,7 @@ ec_engine(const EcDesc* __restrict__ descs, int blocks_per_rank, unsigned long l
   const EcDesc& d = descs[lr];
   if (role == 0) {
     if (threadIdx.x == 0) engine_controller(d, epoch);
+    else if (threadIdx.x == 32) engine_host_poller(d, epoch);
     return;
   }
   engine_worker<T>(d, role - 1, epoch);
