@@ -745,3 +745,51 @@ def test_checkpoint_resume_is_bit_exact(tmp_path):
     for r in range(p):
         assert (st[r].w.cpu().numpy().tobytes(), st[r].momentum_buf.cpu().numpy().tobytes()) == want[r]
     world.close()
+
+
+def test_zero_skew_trajectories_identical_across_flavors():
+    """test_acceptance.py:168-185: with zero skew (every rank boards every
+    round) sync, solo and majority produce the same trajectory, bit for bit,
+    on every rank -- here through the async step path (progressive updates)."""
+    from collections import deque
+
+    from paper_1908_04207_b200 import finish_step, train_step_async
+    p, n, lr, steps = 4, 50_003, 0.05, 4
+    rng = np.random.default_rng(8)
+    grads = torch.as_tensor(rng.standard_normal((steps, p, n), dtype=np.float32), device="cuda")
+    w0 = rng.standard_normal(n, dtype=np.float32)
+    streams = [torch.cuda.Stream() for _ in range(p)]
+    finals = {}
+    for flavor in ("sync", "solo", "majority"):
+        world = EmulatedWorld(p)
+        cfg = CollectiveConfig(p=p, flavor=flavor, vector_len=n, element="f4", seed=1234)
+        hs = [AllreduceHandle(cfg, r, world) for r in range(p)]
+        st = [TrainState.fresh(w0, lr, rank=r, tau=None) for r in range(p)]
+        naps = {}
+
+        def body(r):
+            torch.cuda.set_device(0)
+            torch.cuda.set_stream(streams[r])
+            attach_delivery_tracking(hs[r], st[r])
+            pend, out = deque(), []
+            for t in range(steps):
+                pend.append(train_step_async(st[r], hs[r], grads[t, r], all_arrive=True))
+                if len(pend) > 1:
+                    out.append(finish_step(st[r], hs[r], pend.popleft())[1].nap)
+            while pend:
+                out.append(finish_step(st[r], hs[r], pend.popleft())[1].nap)
+            torch.cuda.current_stream().synchronize()
+            naps[r] = out
+
+        th = [threading.Thread(target=body, args=(r,)) for r in range(p)]
+        [x.start() for x in th]
+        [x.join() for x in th]
+        assert all(naps[r] == [p] * steps for r in range(p)), (flavor, naps)
+        finals[flavor] = [s.w.cpu().numpy().tobytes() for s in st]
+        world.close()
+    w = w0.copy()
+    for t in range(steps):
+        u, _, _ = R.allreduce_round(list(grads[t].cpu().numpy()), [True] * p, np.float32)
+        w = R.sgd_update(w, u, lr)
+    for flavor, ws in finals.items():
+        assert all(x == w.tobytes() for x in ws), flavor
