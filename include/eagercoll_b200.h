@@ -54,10 +54,13 @@ enum {
 
 typedef struct ec_comm ec_comm_t;
 
-/* Library identity. */
+/* Library identity and the thread-local message of the last failing call
+ * (no reference counterpart: the reference raises Python exceptions,
+ * collectives.py:51-59, schedule.py:38-55). */
 int ec_version(void);
 const char* ec_last_error(void);
-/* Number of kernels this library has launched in the process (instrumentation). */
+/* Number of kernels this library has launched in the process (instrumentation;
+ * no reference counterpart). */
 uint64_t ec_launch_count(void);
 
 /* ---- communicator lifecycle ------------------------------------------------
@@ -73,11 +76,15 @@ int ec_comm_create(int world_size, int rank_lo, int n_local, int device,
 /* CUDA IPC handles of local rank `local_idx`'s buffers, for exchange over the
  * process group at init (replaces transport.register_engine, transport.py:205-214). */
 int ec_comm_export(ec_comm_t* c, int local_idx, void* blob, size_t cap, size_t* len);
-/* Map a remote rank's buffers from its exported blob. */
+/* Map a remote rank's buffers from its exported blob (the peer side of
+ * transport.register_engine, transport.py:205-214). */
 int ec_comm_import(ec_comm_t* c, int peer_rank, const void* blob, size_t len);
-/* Replay mode: force generation g's inclusion mask to masks[g] (g < n). */
+/* Replay mode: force generation g's inclusion mask to masks[g] (g < n) --
+ * participation recorded from a reference run, so the
+ * snapshot decisions of collectives.py:146-153 are reproduced exactly. */
 int ec_comm_set_replay(ec_comm_t* c, int local_idx, const uint64_t* masks, int64_t n);
-/* NVLS ("fast" reduction mode, fp32, one rank per GPU): the NVSwitch reduces.
+/* NVLS ("fast" reduction mode, fp32, one rank per GPU; no reference
+ * counterpart -- CollectiveConfig.reduction_mode is an extension): the NVSwitch reduces.
  * One rank ec_nvls_create()s the multicast object and shares the fabric-handle
  * blob; every rank ec_nvls_attach()es it (the creator passes NULL); after all
  * ranks attached, every rank ec_nvls_bind()s its memory, which also switches the
@@ -87,19 +94,26 @@ int ec_nvls_supported(int device);
 int ec_nvls_create(ec_comm_t* c, void* blob, size_t cap, size_t* len);
 int ec_nvls_attach(ec_comm_t* c, const void* blob, size_t len);
 int ec_nvls_bind(ec_comm_t* c);
-/* Start (or resume) the persistent engine kernel on the comm's own stream. */
+/* Start (or resume) the persistent engine kernel on the comm's own stream: the
+ * device form of the engine's pump (schedule.py:346-465, driven by
+ * transport.py:233-317 in the reference). */
 int ec_comm_start(ec_comm_t* c);
 /* Drain and stop the engine at a round boundary so device-wide syncs return;
  * ec_comm_start resumes it with all protocol state preserved. */
 int ec_comm_pause(ec_comm_t* c, int timeout_ms);
 int ec_comm_destroy(ec_comm_t* c);
+/* Device error word (watchdog timeout, out-of-order round): the reference's
+ * TimeoutError / AssertionError (collectives.py:298,331). */
 int ec_comm_error(ec_comm_t* c, int local_idx, uint64_t* code, uint64_t* info);
-/* Diagnostics snapshot of a local rank's engine (16 int64 words, see ec_host.cu). */
+/* Diagnostics snapshot of a local rank's engine (16 int64 words, see ec_host.cu;
+ * no reference counterpart). */
 int ec_debug_state(ec_comm_t* c, int local_idx, int64_t* out16);
 
-/* device addresses of the local rank's send buffer, its registered gradient
- * buffer (write the gradient here and pass it to ec_step_async: while the stash
- * is null the reduction reads it in place, no fold) and result slot `gen % R` */
+/* device addresses of the local rank's send buffer (the stash / send buffer,
+ * eagersgd.py:68, collectives.py:301-303), its registered gradient buffer
+ * (write the gradient here and pass it to ec_step_async: while the stash is
+ * null the reduction reads it in place, no fold) and result slot `gen % R`
+ * (the recv buffer, schedule.py:382-390) */
 void* ec_send_ptr(ec_comm_t* c, int local_idx);
 void* ec_grad_ptr(ec_comm_t* c, int local_idx);
 void* ec_slot_ptr(ec_comm_t* c, int local_idx, int64_t gen);
@@ -137,7 +151,8 @@ int ec_post_activate(ec_comm_t* c, int local_idx, int64_t t, uint64_t* seq);
 /* staleness guard (eagersgd.py:89-110): generations >= hold_from are held
  * until this rank contributes; INT64_MAX disables. */
 int ec_post_hold(ec_comm_t* c, int local_idx, int64_t hold_from, uint64_t* seq);
-/* Reply to request `seq` (EC_R_*), waiting up to timeout_ms (0 = poll once). */
+/* Reply to request `seq` (EC_R_*), waiting up to timeout_ms (0 = poll once):
+ * try_contribute's bool (collectives.py:291-309). */
 int ec_reply(ec_comm_t* c, int local_idx, uint64_t seq, int timeout_ms, int* status);
 /* done_generation (collectives.py:278-289); -1 before the first round. */
 int ec_done_gen(ec_comm_t* c, int local_idx, int64_t* gen);
@@ -150,8 +165,9 @@ int ec_wait(ec_comm_t* c, int local_idx, int64_t t, int timeout_ms, int pin,
  * + ec_reply + ec_wait(t, unpinned).  *status is the offer's reply. */
 int ec_round(ec_comm_t* c, int local_idx, int64_t t, uint32_t flags, void* stream,
              int timeout_ms, int* status, int64_t* gen, uint64_t* mask, int* nap);
-/* A round offered in stream order with a stream-ordered wait for its completion
- * behind it: back-to-back rounds with no host round trip (bandwidth sweeps). */
+/* call_round (collectives.py:334-345) offered in stream order with a
+ * stream-ordered wait for its completion behind it: back-to-back rounds with no
+ * host round trip (bandwidth sweeps). */
 int ec_round_async(ec_comm_t* c, int local_idx, int64_t t, uint32_t flags, void* stream,
                    uint64_t* seq);
 /* One eager-SGD step of the hot path in one call (eagersgd.py:129-167):
@@ -170,9 +186,12 @@ int ec_step(ec_comm_t* c, int local_idx, int64_t t, const void* grad, int fold_m
  * wait occupies `stream`: ranks sharing one GPU need distinct streams. */
 int ec_step_async(ec_comm_t* c, int local_idx, int64_t t, const void* grad, uint32_t flags,
                   void* w, void* mom, double lr, double mu, void* stream, uint64_t* seq);
+/* The outcome of an ec_step_async step: what train_step returns
+ * (eagersgd.py:166-167: the offer's reply, the generation applied, its mask
+ * and nap). */
 int ec_step_result(ec_comm_t* c, int local_idx, uint64_t seq, int64_t t, int timeout_ms,
                    int* status, int64_t* gen, uint64_t* mask, int* nap);
-/* Instrumentation: with profiling on, ec_step brackets its fold and update
+/* Instrumentation (no reference counterpart): with profiling on, ec_step brackets its fold and update
  * launches with CUDA events; ec_profile_read sums the durations
  * (ms_sum[0]/counts[0] = fold, [1] = update) and clears the record. */
 int ec_profile_enable(int on);
@@ -180,14 +199,19 @@ int ec_profile_enable(int on);
  * ec_step_result (from the device wait's release to the last CTA). */
 int ec_step_update_ns(ec_comm_t* c, int local_idx, uint64_t* ns);
 int ec_profile_read(double* ms_sum2, int64_t* counts2);
-/* Mask / nap of an earlier generation from the device log (RoundRecord source). */
+/* Mask / nap of an earlier generation from the device log: CollectiveResult's
+ * included / nap (collectives.py:70-75, 254-274), the RoundRecord source
+ * (trace.py:15-45). */
 int ec_gen_info(ec_comm_t* c, int local_idx, int64_t gen, uint64_t* mask,
                 uint64_t* has_data, int* nap);
-/* Device timestamps (%globaltimer ns) of a completed generation at this rank:
+/* Device timestamps (%globaltimer ns) of a completed generation at this rank
+ * (the timing behind LatencyRecord, trace.py:38-45):
  * t5 = {snapshot taken, reduction issued (all snapshots in), own data phase
  * done, published, own offer processed (0 if none)}. */
 int ec_gen_times(ec_comm_t* c, int local_idx, int64_t gen, uint64_t* t5);
-/* Lowest generation the host may still read: the engine never overwrites the
+/* Result-slot pin (no reference counterpart: the reference copies u out,
+ * collectives.py:260; here slots are read in place).
+ * Lowest generation the host may still read: the engine never overwrites the
  * slot of generation h unless h < pin_lo.  ordered != 0 performs the store in
  * `stream` order (release after the update kernel read the slot); ordered == 0
  * stores from the host immediately. */
@@ -199,7 +223,8 @@ int ec_fold_raw(void* stash, const void* grad, int64_t n, int dtype, int mode,
                 uint32_t* nonfinite_flag, void* stream);
 /* w = w - lr*u, two roundings, no FMA (eagersgd.py:165). */
 int ec_sgd_update(void* w, const void* u, double lr, int64_t n, int dtype, void* stream);
-/* buf = mu*buf + u ; w = w - lr*buf (opt-in momentum; mu == 0 is plain SGD). */
+/* buf = mu*buf + u ; w = w - lr*buf: the opt-in momentum form of
+ * eagersgd.py:165 (the reference is plain SGD; mu == 0 is it). */
 int ec_momentum_update(void* w, void* buf, const void* u, double lr, double mu,
                        int64_t n, int dtype, void* stream);
 /* tree_order_sum (collectives.py:385-403) of p device vectors in the engine's
