@@ -151,6 +151,13 @@ int ec_post_activate(ec_comm_t* c, int local_idx, int64_t t, uint64_t* seq);
 /* staleness guard (eagersgd.py:89-110): generations >= hold_from are held
  * until this rank contributes; INT64_MAX disables. */
 int ec_post_hold(ec_comm_t* c, int local_idx, int64_t hold_from, uint64_t* seq);
+/* staleness_guard (eagersgd.py:89-110) with the ages tracked on the device,
+ * so every step path -- including the stream-ordered ec_step_async -- is
+ * guarded without a host round trip: generation g is held until this rank
+ * contributes when g >= min(oldest round still pending in the stash, the
+ * round after the last offer) + tau (eagersgd.py:102-108).  tau < 0 turns it
+ * off; pending_lo >= 0 seeds the oldest pending round (e.g. after a resume). */
+int ec_post_guard(ec_comm_t* c, int local_idx, int64_t tau, int64_t pending_lo, uint64_t* seq);
 /* Reply to request `seq` (EC_R_*), waiting up to timeout_ms (0 = poll once):
  * try_contribute's bool (collectives.py:291-309). */
 int ec_reply(ec_comm_t* c, int local_idx, uint64_t seq, int timeout_ms, int* status);

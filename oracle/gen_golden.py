@@ -21,6 +21,11 @@ Fixtures written:
                      flavor: per-generation masks, per-(rank, step) accepted
                      offers, observed generations, gradients, weights and the
                      delivery ledger (SURVEY.md Appendix A.4 recipe).
+  c2c3_bench.npz     BASELINE configs 2/3 schedules at the bench cadence
+                     (harness.py:206-241): solo under linear_skew 1 ms and
+                     random_subset k=1 0.2 ms seed 11 at P=2/4/8, majority
+                     seed 1234 and sync at P=8, 64 rounds each -- masks,
+                     accepted offers, observed generations, latencies.
 """
 
 from __future__ import annotations
@@ -253,6 +258,76 @@ def gen_c1_traces(C, E, H, T):
               "obs-lag hist", np.bincount((observed - np.arange(steps)).ravel()).tolist())
 
 
+# BASELINE configs 2/3 at the bench cadence: the reference's
+# own bench_flavor (harness.py:206-241) with the configs' injected delays.
+# Participation is data-independent, so a small
+# vector_len records the schedule that the GPU replays at ResNet-50 size.
+BENCH_TRACES = {
+    # name: (flavor, p, delay kind, unit_ms, k, delay seed)
+    "solo_linear_p2": ("solo", 2, "linear_skew", 1.0, 1, 0),
+    "solo_linear_p4": ("solo", 4, "linear_skew", 1.0, 1, 0),
+    "solo_linear_p8": ("solo", 8, "linear_skew", 1.0, 1, 0),
+    "solo_subset_p2": ("solo", 2, "random_subset", 0.2, 1, 11),
+    "solo_subset_p4": ("solo", 4, "random_subset", 0.2, 1, 11),
+    "solo_subset_p8": ("solo", 8, "random_subset", 0.2, 1, 11),
+    "majority_linear_p8": ("majority", 8, "linear_skew", 1.0, 1, 0),
+    "majority_subset_p8": ("majority", 8, "random_subset", 0.2, 1, 11),
+    "sync_linear_p8": ("sync", 8, "linear_skew", 1.0, 1, 0),
+}
+
+
+def gen_bench_traces(C, H, T, rounds: int = 64):
+    """Per trace: per-generation inclusion masks, per-(rank, round) accepted
+    offers (a fresh snapshot of that round) and the generation each rank's
+    call_round observed (collectives.py:334-345), from the reference run."""
+    out = {}
+    orig = C.AllreduceHandle.call_round
+    for name, (flavor, p, kind, unit, k, dseed) in BENCH_TRACES.items():
+        cfg = H.RunConfig(mode="bench", flavors=(flavor,), p=p, rounds=rounds, vector_len=8,
+                          delay=T.DelayModel(kind, unit_ms=unit, k=k, seed=dseed),
+                          link_latency_us=10, seed=1234)
+        observed = np.full((p, rounds), -1, dtype=np.int64)
+
+        def wrapped(self, t, vec, _orig=orig, _obs=observed):
+            res = yield from _orig(self, t, vec)
+            _obs[self.rank, t] = res.rnd
+            return res
+
+        C.AllreduceHandle.call_round = wrapped
+        try:
+            records, rec, _ = H.bench_flavor(cfg, flavor)
+        finally:
+            C.AllreduceHandle.call_round = orig
+        masks = np.zeros(rounds, dtype=np.int64)
+        naps = np.zeros(rounds, dtype=np.int64)
+        for r in rec.rounds:
+            masks[r.rnd] = r.included
+            naps[r.rnd] = r.nap
+        acc = np.zeros((p, rounds), dtype=np.int8)
+        for sn in rec.snapshots:
+            if sn.fresh:
+                acc[sn.rank, sn.rnd] = 1
+        assert (observed >= 0).all(), name
+        for t in range(rounds):
+            for r in range(p):
+                assert bool(acc[r, t]) == bool((masks[t] >> r) & 1), (name, r, t)
+        inits = np.array([C.initiator_for_round(cfg.seed, t, p) if flavor == "majority" else -1
+                          for t in range(rounds)], dtype=np.int64)
+        lat = np.zeros((p, rounds), dtype=np.int64)
+        for b in records:
+            lat[b.rank, b.round] = b.latency_us
+        out[f"{name}/masks"] = masks
+        out[f"{name}/naps"] = naps
+        out[f"{name}/accepted"] = acc
+        out[f"{name}/observed"] = observed
+        out[f"{name}/initiator"] = inits
+        out[f"{name}/latency_us"] = lat
+        out[f"{name}/meta"] = np.array([p, rounds, cfg.seed], dtype=np.int64)
+        print(f"bench {name}: nap hist {np.bincount(naps).tolist()}, "
+              f"max obs lag {int((observed - np.arange(rounds)).max())}")
+    np.savez_compressed(os.path.join(OUT, "c2c3_bench.npz"), **out)
+
+
 def main():
     C, E, H, T, V = _import_reference()
     os.makedirs(OUT, exist_ok=True)
@@ -260,6 +335,7 @@ def main():
     gen_known_answers(C, E, T, V)
     gen_protocol_tables(C, T)
     gen_c1_traces(C, E, H, T)
+    gen_bench_traces(C, H, T)
     print("golden fixtures written to", os.path.normpath(OUT))
 
 

@@ -166,6 +166,39 @@ def bench_period_us(delays: np.ndarray, p: int, link_latency_us: int) -> int:
     return int(delays.max()) + (3 * hops + 4) * link_latency_us + 1000
 
 
+def bench_delays(model: DelayModel, p: int, rounds: int) -> np.ndarray:
+    """harness.py:198-203: [p, rounds] injected microseconds."""
+    d = np.zeros((p, rounds), dtype=np.int64)
+    for t in range(rounds):
+        for r in range(p):
+            d[r, t] = inject_delay(r, t, model, p)
+    return d
+
+
+def bench_masks(flavor: str, delays: np.ndarray, seed: int) -> np.ndarray:
+    """Inclusion mask of every bench round (harness.py:206-241 with the
+    activation rules of collectives.py:146-153, 311-317).
+
+    The bench cadence gives every round its own slot, so rank r arrives at
+    offset delays[r, t] and the round starts when its activator arrives: the
+    first arrival (solo), the designated initiator (majority) or the last
+    arrival (sync).  A rank is fresh iff it arrived no later than that moment
+    (the injected offsets differ by >= 200 us, far above the few link hops the
+    activation takes); everyone else's slot is snapshotted null."""
+    p, rounds = delays.shape
+    out = np.zeros(rounds, dtype=np.int64)
+    for t in range(rounds):
+        arr = delays[:, t]
+        if flavor == SOLO:
+            a = arr.min()
+        elif flavor == MAJORITY:
+            a = arr[initiator_for_round(seed, t, p)]
+        else:
+            a = arr.max()
+        out[t] = sum(1 << r for r in range(p) if arr[r] <= a)
+    return out
+
+
 # ---------------------------------------------------------------------------
 # eager-SGD (eagersgd.py)
 

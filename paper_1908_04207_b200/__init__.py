@@ -26,7 +26,8 @@ if _os.environ.get("CUDA_MODULE_LOADING") != "EAGER":
 
 from .collectives import (  # noqa: E402,F401
     FLAVORS, MAJORITY, SOLO, SYNC, AllreduceHandle, CollectiveConfig, CollectiveResult,
-    ceil_log2, drive, floor_pow2, initiator_for_round, run_allreduce, tree_order_sum,
+    allreduce_majority, allreduce_solo, allreduce_sync, ceil_log2, drive, floor_pow2,
+    initiator_for_round, run_allreduce, tree_order_sum,
 )
 from .eagersgd import (  # noqa: E402,F401
     DivergenceError, GradientBuffer, TrainState, attach_delivery_tracking, finish_step,

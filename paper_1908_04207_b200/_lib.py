@@ -58,6 +58,7 @@ _SIGS = {
     "ec_post_contribute": (_i32, [_vp, _i32, _i64, _u32, _vp, _P(_u64)]),
     "ec_post_activate": (_i32, [_vp, _i32, _i64, _P(_u64)]),
     "ec_post_hold": (_i32, [_vp, _i32, _i64, _P(_u64)]),
+    "ec_post_guard": (_i32, [_vp, _i32, _i64, _i64, _P(_u64)]),
     "ec_reply": (_i32, [_vp, _i32, _u64, _i32, _P(_i32)]),
     "ec_done_gen": (_i32, [_vp, _i32, _P(_i64)]),
     "ec_wait": (_i32, [_vp, _i32, _i64, _i32, _i32, _P(_i64), _P(_u64), _P(_i32)]),

@@ -178,6 +178,12 @@ class AllreduceHandle:
         self._guard_state = None
         self._hold_posted = _lib.INT64_MAX
         self._pinned = False
+        # one pinned read at a time per rank: the slot pin is a single word
+        self._read_lock = threading.Lock()
+        # generations whose snapshot took an offer issued by train_step_async:
+        # by the time the host dispatches the callback the device may already
+        # have reused the buffer the round read, so those get data=None
+        self._async_gens: set = set()
 
     def close(self) -> None:
         """Destroy this collective instance on every rank of the world (the
@@ -312,7 +318,13 @@ class AllreduceHandle:
             g = self._dispatched + 1
             fresh = g in self._fresh_gens
             self._fresh_gens.discard(g)
-            data = self.send_buffer() if fresh else None
+            stale = g in self._async_gens
+            self._async_gens.discard(g)
+            # the buffer the round consumed: the send buffer still holds it on
+            # the synchronous paths (dispatch runs before the next fold); an
+            # async step's offer may have been the gradient bucket or already
+            # overwritten, so no data is passed
+            data = self.send_buffer() if fresh and not stale else None
             if self.recorder is not None:
                 self.recorder.snapshot(SnapshotRecord(
                     self.rank, g, None if data is None else data.clone(), fresh,
@@ -322,9 +334,10 @@ class AllreduceHandle:
             self._dispatched = g
 
     def _read_result(self, t: int, timeout: float = 60.0, clone: bool = True):
-        gen, mask, nap = self._wait(t, timeout, pin=True)
-        u = self._slot(gen).clone() if clone else None
-        self._unpin()
+        with self._read_lock:
+            gen, mask, nap = self._wait(t, timeout, pin=True)
+            u = self._slot(gen).clone() if clone else None
+            self._unpin()
         res = CollectiveResult(u=u, included=mask, nap=nap, rnd=gen)
         self._last = (gen, res)
         if self.recorder is not None:
@@ -433,9 +446,115 @@ def run_allreduce(cfg: CollectiveConfig, contributions, *, rounds: int = 1, dela
     return results, handles, world
 
 
-def tree_order_sum(vectors) -> torch.Tensor:
+def _spec_round(h: "AllreduceHandle", t: int, x, timeout: float, all_arrive: bool):
+    """One rank's SPEC-level call: offer x (fresh) or the null payload (zeros,
+    empty flag mask, SPEC.md ContributionPayload), activate per the flavor's
+    rule, block for the result of round t (the latest generation >= t)."""
+    if x is None:
+        vec = torch.zeros(h.cfg.vector_len, dtype=h.cfg.torch_dtype, device=f"cuda:{h.device}")
+        fresh = False
+    else:
+        vec = _as_device(x, h.cfg.torch_dtype, h.device, h.cfg.vector_len)
+        fresh = True
+    if not h.round_done(t):
+        h._contribute(t, vec, fresh, activate=True, all_arrive=all_arrive)
+    _, res = h.wait_blocking(t, timeout)
+    h._spec_next = t + 1
+    return res
+
+
+def _spec_allreduce(flavor: str, cfg: CollectiveConfig, contribution_or_null, handle, t,
+                    timeout: float) -> CollectiveResult:
+    if cfg.flavor != flavor:
+        import dataclasses
+        cfg = dataclasses.replace(cfg, flavor=flavor)
+    if handle is not None:
+        # per-rank form (one call per rank and round, any world)
+        if handle.cfg.flavor != flavor or handle.cfg.vector_len != cfg.vector_len:
+            raise ValueError(f"handle is bound to {handle.cfg}, not a {flavor} collective of "
+                             f"length {cfg.vector_len}")
+        rnd = getattr(handle, "_spec_next", 0) if t is None else t
+        return _spec_round(handle, rnd, contribution_or_null, timeout, all_arrive=False)
+    # all-ranks form: one row (vector or None) per rank, zero skew, on one GPU
+    rows = contribution_or_null
+    if cfg.p == 1 and (rows is None or (not isinstance(rows, (list, tuple))
+                                        and np.asarray(rows if not isinstance(rows, torch.Tensor)
+                                                       else rows.cpu()).ndim == 1)):
+        rows = [rows]
+    rows = list(rows)
+    if len(rows) != cfg.p:
+        raise ValueError(f"expected {cfg.p} contributions (one per rank), got {len(rows)}")
+    for x in rows:
+        if x is not None and int(np.prod(np.shape(x))) != cfg.vector_len:
+            raise ValueError(f"length mismatch: contribution of {int(np.prod(np.shape(x)))} "
+                             f"elements vs vector_len {cfg.vector_len}")
+    world = EmulatedWorld(cfg.p, torch.cuda.current_device())
+    try:
+        hs = [AllreduceHandle(cfg, r, world) for r in range(cfg.p)]
+        out: dict = {}
+        errors: list = []
+
+        def body(r: int):
+            try:
+                torch.cuda.set_device(world.device)
+                # every rank boards before activation: zero skew, as SPEC's examples
+                out[r] = _spec_round(hs[r], 0, rows[r], timeout, all_arrive=True)
+            except BaseException as e:  # surfaced below
+                errors.append(e)
+
+        threads = [threading.Thread(target=body, args=(r,), daemon=True) for r in range(cfg.p)]
+        for th in threads:
+            th.start()
+        for th in threads:
+            th.join()
+        if errors:
+            raise errors[0]
+        res0 = out[0]
+        for r in range(1, cfg.p):   # Lemma 1 safety: identical result at every rank
+            if out[r].included != res0.included or not torch.equal(out[r].u, res0.u):
+                raise AssertionError(f"rank {r} observed a different result than rank 0")
+        return res0
+    finally:
+        world.close()
+
+
+def allreduce_sync(cfg: CollectiveConfig, contribution_or_null, *, handle=None, t=None,
+                   timeout: float = 30.0) -> CollectiveResult:
+    """SPEC.md:188-196 `allreduce_sync(cfg, contribution) -> CollectiveResult`:
+    completes after every rank joined; u = sum/P, included = all fresh ranks.
+
+    Two call forms (both thin wrappers over AllreduceHandle):
+    * `handle=` a rank's AllreduceHandle: this rank's contribution (a vector,
+      or None for the null payload) to round `t` (default: the round after the
+      previous call); every rank of the world makes the matching call.
+    * no handle: `contribution_or_null` holds all P ranks' rows (P=1 also
+      accepts a single vector); the P ranks run on the current GPU and the
+      common result is returned.
+    Raises ValueError on a length mismatch (SPEC: errors: length-mismatch)."""
+    return _spec_allreduce(SYNC, cfg, contribution_or_null, handle, t, timeout)
+
+
+def allreduce_solo(cfg: CollectiveConfig, contribution_or_null, *, handle=None, t=None,
+                   timeout: float = 30.0) -> CollectiveResult:
+    """SPEC.md:197-205 `allreduce_solo(cfg, contribution_or_null)`: the first
+    arriving rank starts the round for everyone; later ranks contribute what
+    their send buffer holds (null if nothing).  Call forms as allreduce_sync."""
+    return _spec_allreduce(SOLO, cfg, contribution_or_null, handle, t, timeout)
+
+
+def allreduce_majority(cfg: CollectiveConfig, contribution_or_null, *, handle=None, t=None,
+                       timeout: float = 30.0) -> CollectiveResult:
+    """SPEC.md:206-214 `allreduce_majority(cfg, contribution_or_null)`: only
+    initiator_for_round(cfg.seed, t, P)'s arrival starts the round.  Call forms
+    as allreduce_sync."""
+    return _spec_allreduce(MAJORITY, cfg, contribution_or_null, handle, t, timeout)
+
+
+def tree_order_sum(vectors, divide: bool = False) -> torch.Tensor:
     """collectives.py:385-403 on the device: the fixed association the engine
-    uses, dtype-preserving.  Accepts torch tensors (one device) or arrays."""
+    uses, dtype-preserving.  Accepts torch tensors (one device) or arrays.
+    divide=True also divides by the vector count exactly as a round does
+    (collectives.py:254-260; eagersgd.py:170-174's resync average)."""
     vs = list(vectors)
     p = len(vs)
     if p == 0:
@@ -454,12 +573,13 @@ def tree_order_sum(vectors) -> torch.Tensor:
     srcs = (C.c_void_p * p)(*[t.data_ptr() for t in ts])
     with torch.cuda.device(device):
         call("ec_local_reduce", srcs, p, (1 << p) - 1 if p < 64 else _lib.UINT64_MAX,
-             out.data_ptr(), n, code, 0, _stream_ptr(device))
+             out.data_ptr(), n, code, int(divide), _stream_ptr(device))
     return out
 
 
 __all__ = [
     "SOLO", "MAJORITY", "SYNC", "FLAVORS", "CollectiveConfig", "CollectiveResult",
     "AllreduceHandle", "initiator_for_round", "ceil_log2", "floor_pow2", "run_allreduce",
-    "tree_order_sum", "drive", "EmulatedWorld", "ProcessWorld",
+    "tree_order_sum", "drive", "EmulatedWorld", "ProcessWorld", "allreduce_sync",
+    "allreduce_solo", "allreduce_majority",
 ]

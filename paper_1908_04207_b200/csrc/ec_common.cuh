@@ -23,6 +23,9 @@
 #define EC_REQ_CONTRIB 1
 #define EC_REQ_ACTIVATE 2
 #define EC_REQ_HOLD 3
+// staleness guard with device-tracked ages (eagersgd.py:89-110): arg = tau
+// (< 0 disables), t = the lowest pending round to seed (< 0: none)
+#define EC_REQ_GUARD 4
 // internal contribution flag (set by the post kernel from the fold's poison word)
 #define EC_CF_POISON 0x100
 
@@ -135,6 +138,14 @@ struct alignas(128) EcLocal {
   unsigned long long hp_lo;        // mirrored host pin (EcHostCtl::pin_lo)
   unsigned long long hp_ps;        // the pin_seq it was read with (acknowledged)
   unsigned long long hp_stop;      // epoch whose stop request the poller saw
+  // staleness guard (controller-owned, persisted across pause/resume): a
+  // generation g is held until this rank contributes when
+  // g >= min(pend_lo, last_off + 1) + guard_tau -- the oldest gradient not yet
+  // delivered (a pending stash round, or the step in progress after the last
+  // offer), eagersgd.py:102-108
+  long long guard_tau;             // EC_INF_GEN: guard off
+  long long pend_lo;               // oldest offered round still in the stash (EC_INF_GEN: none)
+  long long last_off;              // round of the last offer processed (-1: none yet)
   EcReq dreq[EC_REQ_RING];         // stream-posted requests (device copy of the ring)
 };
 

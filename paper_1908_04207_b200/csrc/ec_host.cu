@@ -129,7 +129,12 @@ struct EcRankHost {
   unsigned long long next_seq = 0;
   unsigned long long last_update_ns = 0;  // device-timed update of the last reconciled async step
   unsigned long long bar_epoch = 0;       // ec_stream_barrier calls so far
+  // the last stream-ordered pin release (ec_set_pin ordered): a new host pin
+  // waits for it, so an older queued unpin can never clear a newer pin
+  cudaEvent_t unpin_ev = nullptr;
+  bool unpin_pending = false;
   std::mutex mu;
+  std::mutex pin_mu;
 };
 
 struct BlobV1 {
@@ -574,6 +579,9 @@ int ec_comm_create(int world_size, int rank_lo, int n_local, int device, int64_t
     init.contributed_round = -1;
     init.stash_null = 1;
     init.pin_dev = ~0ull;
+    init.guard_tau = EC_INF_GEN;
+    init.pend_lo = EC_INF_GEN;
+    init.last_off = -1;
     if ((e = cudaMemcpy(r->local, &init, sizeof(init), cudaMemcpyHostToDevice)) != cudaSuccess) {
       ec_comm_destroy(c);
       return fail(EC_E_CUDA, "init local: %s", cudaGetErrorString(e));
@@ -778,6 +786,7 @@ int ec_comm_destroy(ec_comm_t* c) {
     if (r->gbuf) cudaFree(r->gbuf);
     if (r->local) cudaFree(r->local);
     if (r->forced) cudaFree(r->forced);
+    if (r->unpin_ev) cudaEventDestroy(r->unpin_ev);
     if (r->h) cudaFreeHost(r->h);
     delete r;
   }
@@ -929,6 +938,10 @@ int ec_post_hold(ec_comm_t* c, int li, int64_t hold_from, uint64_t* seq) {
   return host_post(c, li, EC_REQ_HOLD, 0, 0, hold_from, seq);
 }
 
+int ec_post_guard(ec_comm_t* c, int li, int64_t tau, int64_t pending_lo, uint64_t* seq) {
+  return host_post(c, li, EC_REQ_GUARD, 0, pending_lo, tau, seq);
+}
+
 int ec_reply(ec_comm_t* c, int li, uint64_t seq, int timeout_ms, int* status) {
   int rc = check_li(c, li);
   if (rc) return rc;
@@ -1029,7 +1042,16 @@ int ec_wait(ec_comm_t* c, int li, int64_t t, int timeout_ms, int pin, int64_t* g
     bo.pause();
   }
   long long G = (long long)d1 - 1;
+  std::unique_lock<std::mutex> pin_lock(r->pin_mu, std::defer_lock);
   if (pin && !c->direct) {
+    // A stream-ordered unpin of an earlier read may still be queued (e.g.
+    // behind that read's clone): let it land first, or it would clear this pin
+    // after the handshake below and the engine could reuse the slot under us.
+    pin_lock.lock();
+    if (r->unpin_pending) {
+      CK(cudaEventSynchronize(r->unpin_ev));
+      r->unpin_pending = false;
+    }
     // Pin handshake with the controller's pre-snapshot check (ec_kernels.cu):
     // publish the pin, wait until the controller has acknowledged seeing it
     // (it refreshes the host pin every few us), then make sure the engine had
@@ -1268,8 +1290,14 @@ int ec_set_pin(ec_comm_t* c, int li, uint64_t pin_lo, int ordered, void* stream)
   if (rc) return rc;
   EcRankHost* r = c->L[li];
   if (ordered) {
+    std::lock_guard<std::mutex> g(r->pin_mu);
+    CK(cudaSetDevice(c->device));
     CK(launch_write_u64(&r->hd->pin_lo, pin_lo, (cudaStream_t)stream));
+    if (!r->unpin_ev) CK(cudaEventCreateWithFlags(&r->unpin_ev, cudaEventDisableTiming));
+    CK(cudaEventRecord(r->unpin_ev, (cudaStream_t)stream));
+    r->unpin_pending = true;
   } else {
+    std::lock_guard<std::mutex> g(r->pin_mu);
     __atomic_store_n(&r->h->pin_lo, (unsigned long long)pin_lo, __ATOMIC_SEQ_CST);
   }
   return EC_OK;

@@ -641,6 +641,7 @@ __device__ void engine_controller(const EcDesc& d, unsigned long long epoch) {
   EcCtrl* C = d.ctrl[d.rank];
   const int r = d.rank, P = d.P;
   long long g = L->g, hold_from = L->hold_from, contributed_round = L->contributed_round;
+  long long guard_tau = L->guard_tau, pend_lo = L->pend_lo, last_off = L->last_off;
   unsigned long long next_req = L->next_req;
   int snapped = L->snapped, contrib = L->contrib, internal_act = L->internal_act;
   int arrive_pending = L->arrive_pending, arrive_activate = L->arrive_activate;
@@ -721,6 +722,12 @@ __device__ void engine_controller(const EcDesc& d, unsigned long long epoch) {
       if (type == EC_REQ_CONTRIB && !(fl & EC_CF_POISON) && t == g + 1 &&
           (snapped || contributed_round == g))
         break;
+      if (type == EC_REQ_CONTRIB && !(fl & EC_CF_POISON) && t <= g) {
+        // guard ages: the offered stash now holds round t's gradient until a
+        // fresh snapshot delivers it (eagersgd.py:117-124)
+        if (t < pend_lo) pend_lo = t;
+        if (t > last_off) last_off = t;
+      }
       if (type == EC_REQ_CONTRIB) {
         if (fl & EC_CF_POISON) {
           status = 4;
@@ -767,6 +774,9 @@ __device__ void engine_controller(const EcDesc& d, unsigned long long epoch) {
         if (t == g) activate();
       } else if (type == EC_REQ_HOLD) {
         hold_from = arg;
+      } else if (type == EC_REQ_GUARD) {
+        guard_tau = arg < 0 ? EC_INF_GEN : arg;
+        if (t >= 0 && t < pend_lo) pend_lo = t;
       }
       st_relaxed_sys(&H->reply[next_req % EC_REQ_RING], ((next_req + 1) << 8) | status);
       ++next_req;
@@ -798,7 +808,11 @@ __device__ void engine_controller(const EcDesc& d, unsigned long long epoch) {
         bool ext = false;
         for (int q = 0; q < P && !ext; ++q) ext = ld_acquire_sys(&C->act_from[q]) >= (unsigned long long)g + 1;
         if (ext) {
-          const bool held = !stopping && g >= hold_from && contributed_round < g;
+          // staleness guard: an explicit threshold (ec_post_hold) or the
+          // device-tracked ages (ec_post_guard), eagersgd.py:102-108
+          const long long lo = pend_lo < last_off + 1 ? pend_lo : last_off + 1;
+          const bool aged = guard_tau != EC_INF_GEN && g >= lo + guard_tau;
+          const bool held = !stopping && contributed_round < g && (g >= hold_from || aged);
           go = !held;
         }
       }
@@ -818,6 +832,7 @@ __device__ void engine_controller(const EcDesc& d, unsigned long long epoch) {
         st_relaxed_sys(&H->snap_gen1, (unsigned long long)g + 1);
         if (contrib & (int)EC_SNAP_FRESH) {
           hold_from = EC_INF_GEN;  // stash delivered (eagersgd.py:117-124)
+          pend_lo = EC_INF_GEN;
           *(volatile int*)&L->stash_null = 1;
         }
         snapped = 1;
@@ -913,6 +928,9 @@ __device__ void engine_controller(const EcDesc& d, unsigned long long epoch) {
   L->arrive_pending = arrive_pending;
   L->arrive_activate = arrive_activate;
   L->t_snap = t_snap;
+  L->guard_tau = guard_tau;
+  L->pend_lo = pend_lo;
+  L->last_off = last_off;
   __threadfence();
   st_release_gpu(&L->exit_epoch, epoch);
   st_release_sys(&H->exited, epoch);
@@ -1954,6 +1972,10 @@ __global__ void ec_set_generation_kernel(EcLocal* L, EcHostCtl* H, long long gen
   L->arrive_pending = 0;
   L->arrive_activate = 0;
   L->stash_null = stash_pending ? 0 : 1;
+  // guard ages restart at the resume point; the host re-seeds the pending
+  // stash's oldest round with its next ec_post_guard (staleness_guard)
+  L->pend_lo = EC_INF_GEN;
+  L->last_off = gen - 1;
   L->poison = 0u;
   L->late_copy = 0;
   L->pin_dev = ~0ull;
@@ -2119,9 +2141,10 @@ cudaError_t launch_post(EcLocal* L, unsigned long long seq1, unsigned int type, 
 cudaError_t launch_direct(int dtype, const EcDesc* d_desc, long long nvec, unsigned long long seq,
                           unsigned int type, unsigned int flags, long long t, long long arg,
                           cudaStream_t s) {
-  counted(type == EC_REQ_HOLD ? 1 : 2);
+  const bool no_round = type == EC_REQ_HOLD || type == EC_REQ_GUARD;
+  counted(no_round ? 1 : 2);
   ec_direct_decide<<<1, 32, 0, s>>>(d_desc, seq, type, flags, t, arg);
-  if (type == EC_REQ_HOLD) return cudaGetLastError();
+  if (no_round) return cudaGetLastError();
   const int grid = grid_for((nvec + 3) / 4 + 1, 256);
   if (dtype == 0) ec_direct_round<float><<<grid, 256, 0, s>>>(d_desc);
   else if (dtype == 1) ec_direct_round<double><<<grid, 256, 0, s>>>(d_desc);

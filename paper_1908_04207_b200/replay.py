@@ -137,3 +137,76 @@ def _gen_mask(h: AllreduceHandle, g: int) -> int:
     m, hm, nap = C.c_uint64(), C.c_uint64(), C.c_int()
     call("ec_gen_info", h.comm.ptr, h.li, g, C.byref(m), C.byref(hm), C.byref(nap))
     return m.value
+
+
+def replay_bench_rank(h: AllreduceHandle, vec: torch.Tensor, masks, accepted_r, observed_r,
+                      verify=None) -> dict:
+    """One rank of a replayed bench schedule (BASELINE configs 2/3 at the
+    reference's bench cadence, harness.py:206-241): per round t, call_round's
+    contribute-if-not-done (collectives.py:334-345) with the rank's constant
+    vector, under the engine's forced inclusion masks; then the generation the
+    reference observed is read from its result slot (pinned ahead, so later
+    rounds cannot reuse it) and handed to `verify(g, mask, slot) -> bool`.
+
+    Returns {"accepted": [...], "masks_seen": [...], "verified": [...]} per round;
+    every entry must equal the recorded schedule (masks[g], accepted_r[t])."""
+    rounds = len(observed_r)
+    stream = torch.cuda.current_stream(h.device).cuda_stream
+    acc, seen, ok = [], [], []
+    call("ec_set_pin", h.comm.ptr, h.li, int(observed_r[0]), 0, None)
+    for t in range(rounds):
+        a = False
+        if not h.round_done(t):
+            a = h._contribute(t, vec, fresh=True, activate=True, copy=(t == 0))
+        acc.append(bool(a))
+        g = int(observed_r[t])
+        h._wait(g, 60.0, pin=False)
+        m = _gen_mask(h, g)
+        seen.append(m)
+        ok.append(True if verify is None else bool(verify(g, m, h._slot(g))))
+        nxt = int(observed_r[t + 1]) if t + 1 < rounds else _lib.UINT64_MAX
+        call("ec_set_pin", h.comm.ptr, h.li, nxt, 1, stream)
+    torch.cuda.current_stream(h.device).synchronize()
+    return {"accepted": acc, "masks_seen": seen, "verified": ok}
+
+
+def replay_bench(flavor: str, masks, accepted, observed, vectors, *, element: str = "f4",
+                 seed: int = 1234, device: int = 0, world=None, ring_slots: int = 4,
+                 verify=None) -> dict:
+    """Replay a recorded bench schedule on an emulated world of P ranks (one
+    GPU, P host threads) at the size of `vectors` ([P] device tensors, rank r's
+    constant contribution, as bench_flavor's np.full(vector_len, r+1)).
+    verify(rank, g, mask, slot) checks a result slot; returns per-rank dicts."""
+    p = len(vectors)
+    n = int(vectors[0].numel())
+    cfg = CollectiveConfig(p=p, flavor=flavor, vector_len=n, element=element, seed=seed)
+    own = world is None
+    world = world or EmulatedWorld(p, device, ring_slots=ring_slots)
+    try:
+        hs = [AllreduceHandle(cfg, r, world, cid=0) for r in range(p)]
+        for r in range(p):
+            hs[r].comm.set_replay(r, [int(m) for m in masks])
+        out: dict = {}
+        errors: list = []
+        go = threading.Barrier(p)
+
+        def body(r: int):
+            try:
+                torch.cuda.set_device(device)
+                go.wait()
+                vf = None if verify is None else (lambda g, m, s, _r=r: verify(_r, g, m, s))
+                out[r] = replay_bench_rank(hs[r], vectors[r], masks, accepted[r], observed[r], vf)
+            except BaseException as ex:  # surfaced below
+                errors.append(ex)
+
+        threads = [threading.Thread(target=body, args=(r,), daemon=True) for r in range(p)]
+        for th in threads:
+            th.start()
+        for th in threads:
+            th.join()
+        if errors:
+            raise errors[0]
+        return out
+    finally:
+        if own:
+            world.close()

@@ -352,13 +352,16 @@ class ProcessWorld(_WorldBase):
         process group); see ec_nvls_create/attach/bind.  Any rank failing before
         the bind leaves every rank on the fixed-order engine (a valid "fast")."""
         import os
+        import secrets
         import socket
         import struct
-        import tempfile
         import warnings
         fabric = os.environ.get("EC_NVLS_HANDLE") == "fabric"
-        path = os.path.join(tempfile.gettempdir(), f"ec_nvls_{os.getppid()}_{id(comm)}")
-        path = self._all_gather(path)[0]
+        # Linux abstract-namespace socket (no file to squat on) with a random
+        # name; rank 0 hands the descriptor only to the world's own processes
+        # (SO_PEERCRED pid and uid checked against the all-gathered pids)
+        path = "\0ec_nvls_" + self._all_gather(secrets.token_hex(16))[0]
+        pids = self._all_gather(os.getpid())
         msg = (True, b"")
         srv = None
         if self.rank == 0:
@@ -368,8 +371,6 @@ class ProcessWorld(_WorldBase):
                 call("ec_nvls_create", comm.ptr, buf, 256, C.byref(n))
                 msg = (True, bytes(buf[: n.value]))
                 if not fabric:     # the descriptor travels over a Unix socket (SCM_RIGHTS)
-                    if os.path.exists(path):
-                        os.unlink(path)
                     srv = socket.socket(socket.AF_UNIX, socket.SOCK_STREAM)
                     srv.bind(path)
                     srv.listen(self.p)
@@ -382,9 +383,16 @@ class ProcessWorld(_WorldBase):
         if not fabric:
             if self.rank == 0:
                 fd = struct.unpack("i", blob[:4])[0]
-                for _ in range(self.p - 1):
+                want = set(pids[1:])
+                srv.settimeout(60.0)
+                while want:
                     conn, _ = srv.accept()
-                    socket.send_fds(conn, [b"x"], [fd])
+                    cred = conn.getsockopt(socket.SOL_SOCKET, socket.SO_PEERCRED,
+                                           struct.calcsize("3i"))
+                    pid, uid, _gid = struct.unpack("3i", cred)
+                    if pid in want and uid == os.getuid():
+                        socket.send_fds(conn, [b"x"], [fd])
+                        want.discard(pid)
                     conn.close()
             else:
                 cli = socket.socket(socket.AF_UNIX, socket.SOCK_STREAM)
@@ -401,7 +409,6 @@ class ProcessWorld(_WorldBase):
             self.barrier()
             if srv is not None:
                 srv.close()
-                os.unlink(path)
         err = ""
         try:
             call("ec_nvls_attach", comm.ptr, blob, len(blob))

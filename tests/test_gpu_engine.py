@@ -793,3 +793,61 @@ def test_zero_skew_trajectories_identical_across_flavors():
         w = R.sgd_update(w, u, lr)
     for flavor, ws in finals.items():
         assert all(x == w.tobytes() for x in ws), flavor
+
+
+def test_back_to_back_pinned_reads_and_concurrent_readers():
+    """A host pin released in stream order (after the read's clone) must never
+    clear a newer pin (advisor r1): a reader thread alternates latest_result()
+    and wait_blocking() -- two pinned reads with no post between them -- on
+    the handle its rank's driver also reads, while 300 sync rounds run on a
+    3-slot ring.  Every u read must be its own generation's value (u = g)."""
+    n = 1 << 16
+    world = EmulatedWorld(2, ring_slots=3)
+    cfg = CollectiveConfig(p=2, flavor="sync", vector_len=n, element="f4")
+    hs = [AllreduceHandle(cfg, r, world) for r in range(2)]
+    rounds = 300
+    stop = threading.Event()
+    bad: list = []
+    errors: list = []
+
+    def driver(r):
+        try:
+            torch.cuda.set_device(0)
+            s = torch.cuda.Stream()
+            with torch.cuda.stream(s):
+                for t in range(rounds):
+                    hs[r]._contribute(t, torch.full((n,), float(t), device="cuda"), True, True)
+                    g, res = hs[r].wait_blocking(t)
+                    if not bool((res.u == float(g)).all()):
+                        bad.append(("driver", r, g))
+        except BaseException as e:  # surfaced below
+            errors.append(e)
+
+    def reader():
+        try:
+            torch.cuda.set_device(0)
+            s = torch.cuda.Stream()
+            with torch.cuda.stream(s):
+                while not stop.is_set():
+                    g, res = hs[0].latest_result()
+                    if g < 0:
+                        continue
+                    g2, res2 = hs[0].wait_blocking(g)
+                    for gg, rr in ((g, res), (g2, res2)):
+                        if not bool((rr.u == float(gg)).all()):
+                            bad.append(("reader", gg))
+        except BaseException as e:  # surfaced below
+            errors.append(e)
+
+    th = [threading.Thread(target=driver, args=(r,), daemon=True) for r in range(2)]
+    rd = threading.Thread(target=reader, daemon=True)
+    rd.start()
+    for x in th:
+        x.start()
+    for x in th:
+        x.join()
+    stop.set()
+    rd.join()
+    world.close()
+    assert not errors, errors[0]
+    assert not bad, bad[:5]

@@ -128,3 +128,34 @@ def test_replay_masks_are_consistent(golden_dir):
         assert (tr["observed"] >= np.arange(steps)).all()
         if flavor == "sync":
             assert (tr["masks"] == (1 << p) - 1).all()
+
+
+BENCH_DELAYS = {"linear": ("linear_skew", 1.0, 1, 0), "subset": ("random_subset", 0.2, 1, 11)}
+
+
+def test_bench_schedules_match_the_restated_activation_rules(golden_dir):
+    """The config-2/3 schedules recorded from the reference's bench_flavor
+    (oracle/gen_golden.py) equal the restated activation rules: per round the
+    fresh set is every rank that arrived by its activator's arrival, nap is its
+    popcount, accepted offers are exactly the mask bits, and every rank saw its
+    own round's result (the cadence leaves no lag)."""
+    z = np.load(os.path.join(golden_dir, "c2c3_bench.npz"))
+    names = sorted({k.split("/")[0] for k in z.files})
+    assert len(names) == 9
+    for name in names:
+        flavor, kind, pp = name.split("_")
+        p, rounds, seed = (int(x) for x in z[f"{name}/meta"])
+        assert pp == f"p{p}"
+        k, unit, kk, dseed = BENCH_DELAYS[kind]
+        delays = R.bench_delays(R.DelayModel(k, unit, kk, dseed), p, rounds)
+        masks = z[f"{name}/masks"]
+        assert masks.tolist() == R.bench_masks(flavor, delays, seed).tolist(), name
+        assert z[f"{name}/naps"].tolist() == [int(m).bit_count() for m in masks]
+        acc = z[f"{name}/accepted"]
+        for t in range(rounds):
+            assert [bool(a) for a in acc[:, t]] == [bool((int(masks[t]) >> r) & 1)
+                                                  for r in range(p)]
+        assert (z[f"{name}/observed"] == np.arange(rounds)).all()
+        if flavor == "majority":
+            inits = z[f"{name}/initiator"]
+            assert all((int(masks[t]) >> int(inits[t])) & 1 for t in range(rounds))
