@@ -326,9 +326,17 @@ class AllreduceHandle:
             # overwritten, so no data is passed
             data = self.send_buffer() if fresh and not stale else None
             if self.recorder is not None:
-                self.recorder.snapshot(SnapshotRecord(
-                    self.rank, g, None if data is None else data.clone(), fresh,
-                    _now_us()))
+                # a null snapshot consumed the zeroed send buffer: record the
+                # zero vector, as the reference does (trace.py:92-96,
+                # schedule.py:373-380); a stale async offer records None
+                if data is not None:
+                    rec = data.clone()
+                elif not fresh:
+                    rec = torch.zeros(self.cfg.vector_len, dtype=self.cfg.torch_dtype,
+                                      device=f"cuda:{self.device}")
+                else:
+                    rec = None
+                self.recorder.snapshot(SnapshotRecord(self.rank, g, rec, fresh, _now_us()))
             if self.user_snapshot_cb is not None:
                 self.user_snapshot_cb(g, data, fresh)
             self._dispatched = g

@@ -29,7 +29,13 @@ from dataclasses import dataclass
 os.environ.setdefault("CUDA_MODULE_LOADING", "EAGER")
 
 BENCH_SCHEMA = "eagercoll-bench-v1"
+TRAIN_SCHEMA = "eagercoll-train-v1"
 _BENCH_FIELDS = ("flavor", "round", "rank", "latency_us", "nap", "initiator")
+_TRAIN_FIELDS = ("flavor", "round", "epoch", "rank", "loss", "nap", "staleness_max", "t_us")
+
+
+class ConfigError(ValueError):
+    """harness.py:50 of the reference (bad config / unreadable CSV)."""
 
 
 @dataclass
@@ -41,6 +47,12 @@ class BenchRecord:
     latency_us: int
     nap: int
     initiator: int = -1
+
+    def __post_init__(self):
+        if self.latency_us < 0:
+            raise ValueError("negative latency")
+        if self.nap < 1:
+            raise ValueError("nap < 1")
 
 
 def _gen_times(h, g):
@@ -320,13 +332,76 @@ def summarize(records):
     return out
 
 
+def _fmt(v) -> str:
+    """harness.py:379-382: floats as repr (round-trippable), the rest as str."""
+    if isinstance(v, float):
+        return repr(v)
+    return str(v)
+
+
 def write_bench_csv(records, path: str) -> None:
-    """harness.py:373-378 (same schema line and columns)."""
+    """harness.py:385-390 (same schema line and columns)."""
     with open(path, "w") as f:
         f.write(f"# {BENCH_SCHEMA}\n")
         f.write(",".join(_BENCH_FIELDS) + "\n")
         for b in records:
-            f.write(",".join(str(getattr(b, k)) for k in _BENCH_FIELDS) + "\n")
+            f.write(",".join(_fmt(getattr(b, k)) for k in _BENCH_FIELDS) + "\n")
+
+
+def train_row(flavor: str, m: dict) -> dict:
+    """One eagercoll-train-v1 row from a training_process metrics dict
+    (eagersgd.py:214-219: round, epoch, rank, loss, nap, staleness_max,
+    wall_or_sim_time)."""
+    return {"flavor": flavor, "round": int(m["round"]), "epoch": int(m["epoch"]),
+            "rank": int(m["rank"]), "loss": float(m["loss"]), "nap": int(m["nap"]),
+            "staleness_max": int(m["staleness_max"]), "t_us": int(m["wall_or_sim_time"])}
+
+
+def write_train_csv(rows, path: str) -> None:
+    """harness.py:393-398: `# eagercoll-train-v1`, then the columns."""
+    with open(path, "w") as f:
+        f.write(f"# {TRAIN_SCHEMA}\n")
+        f.write(",".join(_TRAIN_FIELDS) + "\n")
+        for row in rows:
+            f.write(",".join(_fmt(row[k]) for k in _TRAIN_FIELDS) + "\n")
+
+
+def write_jsonl(path: str, schema: str, dicts) -> None:
+    """harness.py:401-407: JSON-lines mirror of a CSV -- one header object,
+    then one object per row with identical fields and values."""
+    with open(path, "w") as f:
+        f.write(json.dumps({"schema": schema}, sort_keys=True) + "\n")
+        for d in dicts:
+            f.write(json.dumps(d, sort_keys=True) + "\n")
+
+
+def read_bench_csv(path: str) -> list:
+    """harness.py:410-424: parse an eagercoll-bench-v1 CSV back into records."""
+    with open(path) as f:
+        header = f.readline().strip()
+        if header != f"# {BENCH_SCHEMA}":
+            raise ConfigError(f"{path}: unknown schema {header!r}")
+        names = f.readline().strip().split(",")
+        if tuple(names) != _BENCH_FIELDS:
+            raise ConfigError(f"{path}: unexpected columns {names}")
+        out = []
+        for line in f:
+            vals = line.strip().split(",")
+            out.append(BenchRecord(vals[0], int(vals[1]), int(vals[2]), int(vals[3]),
+                                   int(vals[4]), int(vals[5])))
+    return out
+
+
+def emit_bench(records, stem: str) -> None:
+    """harness.py:427-431: <stem>.csv and its JSONL mirror."""
+    import dataclasses
+    write_bench_csv(records, stem + ".csv")
+    write_jsonl(stem + ".jsonl", BENCH_SCHEMA, [dataclasses.asdict(b) for b in records])
+
+
+def emit_train(rows, stem: str) -> None:
+    write_train_csv(rows, stem + ".csv")
+    write_jsonl(stem + ".jsonl", TRAIN_SCHEMA, rows)
 
 
 def _main(argv=None):
@@ -406,6 +481,7 @@ def _main(argv=None):
             kind, unit = args.delay.split(":")
             model = DelayModel(kind, unit_ms=float(unit), k=1, seed=11)
         out = {}
+        train_rows: list = []
         flavors = [f for f in args.flavors.split(",") if f] if args.flavors != "solo,majority" \
             else ["sync", "solo", "majority"]
         for i, f in enumerate(flavors):
@@ -419,6 +495,7 @@ def _main(argv=None):
                 dist.all_gather_object(allr, {k: r[k] for k in ("rows", "val", "wall_s")})
             else:
                 allr[0] = {k: r[k] for k in ("rows", "val", "wall_s")}
+            train_rows += [train_row(f, m) for x in allr for m in x["rows"]]
             wall = max(x["wall_s"] for x in allr)
             steps = sum(len(x["rows"]) for x in allr)
             last = max(e for x in allr for (_, e) in x["val"])
@@ -430,6 +507,9 @@ def _main(argv=None):
             for f in out:
                 out[f]["speedup_vs_sync"] = out[f]["steps_per_s"] / out["sync"]["steps_per_s"]
         result["train"] = out
+        if rank == 0 and args.out:
+            emit_train(sorted(train_rows, key=lambda d: (d["flavor"], d["round"], d["rank"])),
+                       args.out)
     else:
         kind, unit = args.delay.split(":")
         model = DelayModel(kind, unit_ms=float(unit), k=1, seed=11)
@@ -441,7 +521,7 @@ def _main(argv=None):
         flat = sorted((r for rr in allr for r in rr), key=lambda b: (b.flavor, b.round, b.rank))
         result["summary"] = summarize(flat)
         if rank == 0 and args.out:
-            write_bench_csv(flat, args.out + ".csv")
+            emit_bench(flat, args.out)
     if rank == 0:
         s = json.dumps(result)
         print(s, flush=True)

@@ -26,9 +26,14 @@ from .world import EmulatedWorld
 
 
 def replay_rank(r: int, h: AllreduceHandle, resync_h: AllreduceHandle, st: TrainState, trace,
-                grads_r: torch.Tensor, ledger, acc: np.ndarray, seen_masks: np.ndarray) -> None:
+                grads_r: torch.Tensor, ledger, acc: np.ndarray, seen_masks: np.ndarray,
+                rows: list | None = None, loss_fn=None, flavor: str = "") -> None:
     """One rank's replayed training loop (training_process, eagersgd.py:187-226,
-    with the offers' outcomes and the observed generations forced by `trace`)."""
+    with the offers' outcomes and the observed generations forced by `trace`).
+    With `rows`, appends one eagercoll-train-v1 row per step (harness.py:393):
+    loss = loss_fn(rank, t, w) of the weights the step started from, nap of the
+    generation applied, the stash's staleness and -- a replay has no clock --
+    the observed generation as t_us."""
     steps = int(trace["steps"])
     epochs = int(trace["epochs"])
     spe = int(trace["steps_per_epoch"])
@@ -40,6 +45,7 @@ def replay_rank(r: int, h: AllreduceHandle, resync_h: AllreduceHandle, st: Train
         for s in range(spe):
             t = e * spe + s
             ledger.generated(r, t)
+            loss = float(loss_fn(r, t, st.w)) if loss_fn is not None else 0.0
             with h.engine.lock:
                 st.send_buf.bind(h)
                 st.send_buf.fold(grads_r[t], t)
@@ -57,6 +63,10 @@ def replay_rank(r: int, h: AllreduceHandle, resync_h: AllreduceHandle, st: Train
                 raise AssertionError(f"generation {g}: rank {r} saw mask {m:#x}, "
                                      f"another rank {int(seen_masks[g]):#x}")
             apply_update(st, h._slot(g))
+            if rows is not None:
+                rows.append({"flavor": flavor, "round": t, "epoch": e, "rank": r, "loss": loss,
+                             "nap": int(m).bit_count(), "staleness_max": st.staleness_max(),
+                             "t_us": g})
             nxt = int(observed[r, t + 1]) if t + 1 < steps else _lib.UINT64_MAX
             call("ec_set_pin", h.comm.ptr, h.li, nxt, 1,
                  torch.cuda.current_stream(h.device).cuda_stream)
@@ -74,14 +84,16 @@ def replay_configs(trace, element: str):
             CollectiveConfig(p=p, flavor="sync", vector_len=dim, element=element))
 
 
-def replay_training(trace, element: str = "f4", device: int = 0, world=None, ring_slots: int = 4):
+def replay_training(trace, element: str = "f4", device: int = 0, world=None, ring_slots: int = 4,
+                    loss_fn=None, flavor: str = "replay"):
     """Replay a c1_<flavor> trace (tests/golden) on an emulated world (P ranks,
     P host threads, one GPU).
 
     trace: mapping with p, steps, epochs, steps_per_epoch, lr, resync_period,
     masks[g], accepted[r, t], observed[r, t], grads[r, t, :], w0.
     Returns dict(w=[p, dim] final weights (numpy), accepted=[p, steps],
-    ledger=dict, masks=[steps] device masks).
+    ledger=dict, masks=[steps] device masks, rows=eagercoll-train-v1 rows
+    sorted by (round, rank); see replay_rank for loss_fn).
     """
     p = int(trace["p"])
     steps = int(trace["steps"])
@@ -105,6 +117,7 @@ def replay_training(trace, element: str = "f4", device: int = 0, world=None, rin
               for r in range(p)]
     acc = np.zeros((p, steps), dtype=np.int8)
     seen_masks = np.zeros(steps, dtype=np.int64)
+    rows: list = [[] for _ in range(p)]
     errors: list = []
     go = threading.Barrier(p)
 
@@ -113,7 +126,7 @@ def replay_training(trace, element: str = "f4", device: int = 0, world=None, rin
             torch.cuda.set_device(device)
             go.wait()
             replay_rank(r, handles[r], resync[r], states[r], trace, grads[r], ledger, acc,
-                        seen_masks)
+                        seen_masks, rows[r], loss_fn, flavor)
         except BaseException as ex:  # surfaced below
             errors.append(ex)
 
@@ -126,7 +139,9 @@ def replay_training(trace, element: str = "f4", device: int = 0, world=None, rin
         if errors:
             raise errors[0]
         w = np.stack([st.w.detach().cpu().numpy() for st in states])
-        return {"w": w, "accepted": acc, "ledger": ledger.as_dict(), "masks": seen_masks}
+        flat = sorted((x for rr in rows for x in rr), key=lambda d: (d["round"], d["rank"]))
+        return {"w": w, "accepted": acc, "ledger": ledger.as_dict(), "masks": seen_masks,
+                "rows": flat}
     finally:
         if own:
             world.close()

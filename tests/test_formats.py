@@ -101,3 +101,88 @@ def test_egs1_state_roundtrip(tmp_path):
     write_state_file(str(tmp_path / "n.egs"), rec)
     out = read_state_file(str(tmp_path / "n.egs"))
     assert out["stash"] is None and out["momentum"] is None and out["tau"] == 4
+
+
+def test_train_csv_and_jsonl_mirror(tmp_path):
+    """harness.py:393-407: eagercoll-train-v1 CSV (floats as repr) and its
+    JSON-lines mirror with a schema header, identical fields and values."""
+    from paper_1908_04207_b200.harness import emit_train, train_row
+    rows = [train_row("solo", {"round": t, "epoch": t // 4, "rank": r, "loss": 0.1 * (t + r) + 1e-17,
+                               "nap": 1 + r, "staleness_max": t % 2, "wall_or_sim_time": 10 * t})
+            for t in range(3) for r in range(2)]
+    emit_train(rows, str(tmp_path / "tr"))
+    lines = (tmp_path / "tr.csv").read_text().splitlines()
+    assert lines[0] == "# eagercoll-train-v1"
+    assert lines[1] == "flavor,round,epoch,rank,loss,nap,staleness_max,t_us"
+    assert lines[3] == f"solo,0,0,1,{rows[1]['loss']!r},2,0,0"
+    js = [json.loads(x) for x in (tmp_path / "tr.jsonl").read_text().splitlines()]
+    assert js[0] == {"schema": "eagercoll-train-v1"}
+    assert js[1:] == rows
+    for line, row in zip(lines[2:], rows):
+        assert float(line.split(",")[4]) == row["loss"]      # repr round-trips
+
+
+def test_read_bench_csv_roundtrip_and_schema_errors(tmp_path):
+    """harness.py:410-424 read_bench_csv, harness.py:427-431 JSONL mirror."""
+    from paper_1908_04207_b200.harness import ConfigError, emit_bench, read_bench_csv
+    recs = [BenchRecord("majority", t, r, 7 * t + r, 1 + (t + r) % 3, (t * 5) % 4)
+            for t in range(4) for r in range(4)]
+    emit_bench(recs, str(tmp_path / "b"))
+    assert read_bench_csv(str(tmp_path / "b.csv")) == recs
+    js = [json.loads(x) for x in (tmp_path / "b.jsonl").read_text().splitlines()]
+    assert js[0] == {"schema": "eagercoll-bench-v1"} and len(js) == 17
+    assert js[5] == {"flavor": "majority", "round": 1, "rank": 0, "latency_us": 7, "nap": 2,
+                     "initiator": 1}
+    bad = tmp_path / "bad.csv"
+    bad.write_text("# eagercoll-bench-v0\nflavor\n")
+    with pytest.raises(ConfigError):
+        read_bench_csv(str(bad))
+    bad.write_text("# eagercoll-bench-v1\nflavor,round\n")
+    with pytest.raises(ConfigError):
+        read_bench_csv(str(bad))
+    with pytest.raises(ValueError):
+        BenchRecord("solo", 0, 0, -1, 1)
+    with pytest.raises(ValueError):
+        BenchRecord("solo", 0, 0, 1, 0)
+
+
+def test_hyperplane_model_pinned_to_reference():
+    """models.py:62-71 known answer (test_models.py:18-22), central
+    differences (acceptance criterion 10) and -- against the reference's own
+    config-1 run (tests/golden/c1_solo.npz) -- the dataset, the per-(rank, step)
+    minibatch and the gradient at every epoch start, on CPU torch in f64."""
+    import os
+
+    import torch
+
+    from paper_1908_04207_b200.models import gen_dataset, loss_and_grad, mse, sample_batch
+    loss, grad = loss_and_grad(torch.tensor([2.0], dtype=torch.float64),
+                               torch.tensor([[1.0]], dtype=torch.float64),
+                               torch.tensor([0.0], dtype=torch.float64))
+    assert float(loss) == 4.0 and grad.tolist() == [4.0]
+    rng = np.random.default_rng(31337)
+    worst = 0.0
+    for _ in range(50):
+        dim, b = int(rng.integers(1, 17)), int(rng.integers(1, 33))
+        x = torch.as_tensor(rng.standard_normal((b, dim)))
+        y = torch.as_tensor(rng.standard_normal(b))
+        w = torch.as_tensor(rng.standard_normal(dim))
+        _, g = loss_and_grad(w, x, y)
+        for j in range(dim):
+            e = torch.zeros(dim, dtype=torch.float64)
+            e[j] = 1e-6
+            fd = (mse(w + e, x, y) - mse(w - e, x, y)) / 2e-6
+            worst = max(worst, abs(float(g[j]) - fd) / max(1.0, abs(fd)))
+    assert worst <= 1e-6
+    golden = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden")
+    tr = np.load(os.path.join(golden, "c1_solo.npz"))
+    ds = gen_dataset(64, 4096, seed=99, device=torch.device("cpu"), dtype=torch.float64)
+    spe = int(tr["steps_per_epoch"])
+    for r in range(int(tr["p"])):
+        for e in range(0, int(tr["epochs"]), 7):
+            t = e * spe
+            x, y = sample_batch(ds, 99, r, t, 128)
+            loss, g = loss_and_grad(torch.as_tensor(tr["w_epoch"][r, e]), x, y)
+            ref = tr["grads"][r, t]
+            assert np.max(np.abs(g.numpy() - ref)) <= 1e-12 * max(1.0, np.max(np.abs(ref)))
+            assert abs(float(loss) - tr["losses"][r, t]) <= 1e-12 * max(1.0, tr["losses"][r, t])
