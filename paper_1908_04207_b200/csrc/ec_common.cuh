@@ -78,17 +78,28 @@ struct alignas(64) EcReq {
   unsigned long long pad[4];
 };
 
+// one round command (controller -> workers); command s (s = 1, 2, ...) sits in
+// EcLocal::cmd[(s - 1) & 3] -- up to EcDesc::lead rounds are in flight
+struct EcCmd {
+  long long gen;
+  unsigned long long has;          // has-data mask of the round
+  unsigned long long src;          // ranks whose offer is their gradient buffer
+  unsigned long long updm;         // ranks updating progressively (owners signal arrivals)
+};
+
 struct alignas(128) EcLocal {
-  // round command: controller -> workers
-  unsigned long long cmd_seq;      // incremented per round; ~0ull = exit
-  long long cmd_gen;
-  unsigned long long cmd_has;      // has-data mask of the round
+  // round commands: controller -> workers
+  unsigned long long cmd_seq;      // commands issued (monotone)
   unsigned long long exit_epoch;   // workers of launch `epoch` exit when this equals it
-  unsigned long long pad0[4];
+  unsigned long long pad0[6];
+  EcCmd cmd[4];
   unsigned long long rs_count;     // worker CTAs finished reduce-scatter (monotone)
   unsigned long long pad1[7];
-  unsigned long long ag_count;     // worker CTAs finished all-gather (monotone)
-  unsigned long long pad2[7];
+  // worker CTAs finished command s, counted in ag_cnt[(s - 1) & 3] (monotone)
+  unsigned long long ag_cnt[4];
+  unsigned long long t_rs4[4];     // globaltimer when command s's last worker finished
+  unsigned int rpoison[4];         // command s's CTAs saw a non-finite reduced value
+  unsigned long long pad2[2];
   unsigned long long round_done;   // last cmd_seq fully done
   unsigned long long pad3[7];
   // controller state (persisted across pause/resume)
@@ -115,11 +126,10 @@ struct alignas(128) EcLocal {
   unsigned long long upd_count;    // CTAs of the fused wait+update kernel done (last one unpins)
   unsigned long long step_tag;     // t + 1 once step_gen holds step t's generation
   unsigned long long upd_t0;       // globaltimer when the fused update's compute began
-  unsigned long long cmd_src;      // round: ranks whose offer is their gradient buffer
   unsigned long long req_done_dev; // requests the controller has processed (device mirror)
   int late_copy;                   // a zero-copy offer was refused: copy gbuf -> stash
   int step_late;                   // latched late_copy for the current async step's update
-  unsigned int round_poison;       // this rank's CTAs saw a non-finite reduced value
+  unsigned int pad_rp;
   unsigned int upd_bad;            // the async step's update read a non-finite u
   unsigned long long pin_dev;      // device-side pin (async steps): lowest gen still read
   unsigned long long stage_count;  // NVLS: CTAs that staged this round (monotone)
@@ -128,7 +138,6 @@ struct alignas(128) EcLocal {
   int dec_fold;                    // direct step: fold the gradient into the stash in-pass
   int pad7;
   unsigned long long fuse_seq;     // request seq + 1 of the last offer accepted with arrival words
-  unsigned long long cmd_updm;     // round: ranks updating progressively (owners signal arrivals)
   int step_fused;                  // the current async step updates progressively (arrival words)
   int pad8;
   unsigned long long upd_next_item;  // progressive update: next chunk item to claim
@@ -189,6 +198,8 @@ struct alignas(128) EcHostCtl {
 struct EcDesc {
   int rank, P, flavor, dtype;
   int R, W, replay, vec;              // ring slots, worker CTAs, replay flag, elems / 16 B
+  int lead;                           // rounds the engine may have in flight (1, or 2: the
+                                      // next round's snapshot overlaps the current data phase)
   int mode;                           // data phase: 0 = fused TMA, 1 = two-phase ld.cg pull,
                                       // 2 = NVLS (multimem.ld_reduce / multimem.st, fast mode)
   int chv, stages;                    // TMA chunk (16-B vectors) and pipeline depth

@@ -39,15 +39,15 @@ cudaError_t launch_stream_barrier(unsigned long long* count, unsigned long long 
 cudaError_t launch_fold_auto(int dtype, void* stash, const void* grad, long long n, EcLocal* L,
                              unsigned long long seq1, unsigned flags, long long t, int zero_copy,
                              cudaStream_t s);
-cudaError_t launch_wait_gen(EcLocal* L, EcHostCtl* H, long long t, int R, unsigned long long timeout_ns,
-                            cudaStream_t s);
+cudaError_t launch_wait_gen(EcLocal* L, EcHostCtl* H, long long t, int R, int lead,
+                            unsigned long long timeout_ns, cudaStream_t s);
 cudaError_t launch_wait_done(EcLocal* L, EcHostCtl* H, long long t, unsigned long long timeout_ns,
                              cudaStream_t s);
 cudaError_t launch_update_gen(int dtype, void* w, void* mom, const char* ring, long long slot_bytes,
                               int R, EcLocal* L, double lr, double mu, long long n, EcHostCtl* H,
                               long long t, unsigned long long timeout_ns, unsigned long long seq1,
                               void* stash, const void* gbuf, const EcDesc* dp, int progressive,
-                              cudaStream_t s);
+                              int share, cudaStream_t s);
 cudaError_t launch_write_u64(unsigned long long* p, unsigned long long v, cudaStream_t s);
 cudaError_t launch_direct_step(int dtype, const EcDesc* d_desc, unsigned long long seq,
                                unsigned int flags, void* w, void* mom, const void* ring,
@@ -162,6 +162,7 @@ struct ec_comm {
   void* last_stream = nullptr;  // direct mode orders host-posted requests on it
   unsigned long long epoch = 0;
   int mode = 0, chv = 256, stages = 4, smem_bytes = 0;  // data phase (see EcDesc)
+  int lead = 1;                                        // rounds in flight (EcDesc::lead)
   double budget = 0.0;                                 // SMs' worth of engine CTAs held
   // NVLS (reduction_mode "fast"): multicast object over every rank's GPU
   CUmemGenericAllocationHandle mc_handle = 0, mc_phys = 0;
@@ -703,6 +704,10 @@ static int upload_descs(ec_comm_t* c) {
     x.chv = c->chv;
     x.stages = c->stages;
     x.smem_bytes = c->smem_bytes;
+    // two rounds in flight (the next one's snapshot overlaps this one's data
+    // phase) need the fused TMA pipeline and a third result slot for readers
+    c->lead = (c->mode == 0 && c->R >= 3 && !getenv("EC_NO_LEAD")) ? 2 : 1;
+    x.lead = c->lead;
     for (int q = 0; q < c->P; ++q) {
       x.ctrl[q] = c->ctrl[q];
       x.send[q] = c->send[q];
@@ -1067,7 +1072,7 @@ int ec_wait(ec_comm_t* c, int li, int64_t t, int timeout_ms, int pin, int64_t* g
         ab.pause();
       }
       long long D = (long long)aload(&r->h->done_gen1) - 1;
-      if (D < G + c->R - 1) break;
+      if (D < G + c->R - c->lead) break;   // no snapshot of G + R yet (see wait_and_pin)
       G = D;
     }
   }
@@ -1245,7 +1250,7 @@ int ec_step_async(ec_comm_t* c, int li, int64_t t, const void* grad, uint32_t fl
     ProfScope ps(1, stream);
     CK(launch_update_gen(c->dtype, w, (mom && mu != 0.0) ? mom : nullptr, r->ring, c->slot_bytes, c->R,
                          r->local, lr, mu, c->n, r->hd, t, c->timeout_ns, seq + 1, r->send,
-                         r->gbuf, c->d_descs + li, prog ? 1 : 0, s));
+                         r->gbuf, c->d_descs + li, prog ? 1 : 0, c->n_local, s));
   }
   if (seq_out) *seq_out = seq;
   return EC_OK;

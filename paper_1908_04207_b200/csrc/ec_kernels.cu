@@ -378,7 +378,7 @@ __device__ void round_ldg(const EcDesc& d, const char* const* sp, int w, long lo
     if (old + 1 == (unsigned long long)d.W * seen) {
       fence_acq_rel_sys();
       for (int q = 0; q < d.P; ++q) st_release_sys(&d.ctrl[q]->rsdone_from[d.rank], (unsigned long long)g + 1);
-      L->t_rs = globaltimer_ns();
+      L->t_rs4[(seen - 1) & 3] = globaltimer_ns();
     }
     const unsigned long long t0 = globaltimer_ns();
     for (int q = 0; q < d.P; ++q) {
@@ -499,7 +499,7 @@ __device__ void round_nvls(const EcDesc& d, const char* const* sp, int w, long l
       }
     }
     fence_proxy_alias();
-    if (w == 0) L->t_rs = globaltimer_ns();   // staged everywhere (timeline stamp)
+    if (w == 0) L->t_rs4[(seen - 1) & 3] = globaltimer_ns();   // staged everywhere (timeline stamp)
   }
   __syncthreads();
   // 3. my shard: switch-reduced sum, / P, broadcast into every rank's slot
@@ -570,13 +570,15 @@ __device__ void engine_worker(const EcDesc& d, int w, unsigned long long epoch) 
     if (tid == 0) {
       unsigned ns = 32;
       while (true) {
+        // commands are taken one at a time, in order (up to `lead` may be out)
         unsigned long long s = ld_acquire_gpu(&L->cmd_seq);
-        if (s != seen) {
-          s_seq = s;
-          s_gen = *(volatile long long*)&L->cmd_gen;
-          s_has = *(volatile unsigned long long*)&L->cmd_has;
-          s_updm = *(volatile unsigned long long*)&L->cmd_updm;
-          s_src = *(volatile unsigned long long*)&L->cmd_src;
+        if (s > seen) {
+          const EcCmd* cm = &L->cmd[seen & 3];
+          s_seq = seen + 1;
+          s_gen = *(volatile const long long*)&cm->gen;
+          s_has = *(volatile const unsigned long long*)&cm->has;
+          s_updm = *(volatile const unsigned long long*)&cm->updm;
+          s_src = *(volatile const unsigned long long*)&cm->src;
           s_exit = 0;
           break;
         }
@@ -605,18 +607,19 @@ __device__ void engine_worker(const EcDesc& d, int w, unsigned long long epoch) 
     } else {
       round_ldg<T>(d, sp, w, g, has, seen);
     }
-    if (__syncthreads_or(bad) && tid == 0) atomicOr(&L->round_poison, 1u);
+    const int cs = (int)((seen - 1) & 3);     // this command's counter slot
+    if (__syncthreads_or(bad) && tid == 0) atomicOr(&L->rpoison[cs], 1u);
     if (tid == 0) {
       fence_acq_rel_sys();
-      const unsigned long long old = atomicAdd(&L->ag_count, 1ull);
-      if (old + 1 == (unsigned long long)d.W * seen) {
+      const unsigned long long old = atomicAdd(&L->ag_cnt[cs], 1ull);
+      if (old + 1 == (unsigned long long)d.W * (((seen - 1) >> 2) + 1)) {
         // every CTA of this rank is done: tell the world (TMA mode: our pushes
         // into every slot have landed) / ourselves (pull mode)
         fence_acq_rel_sys();
         unsigned long long word = (unsigned long long)g + 1;
-        if (atomicExch(&L->round_poison, 0u)) word |= EC_DONE_POISON;
+        if (atomicExch(&L->rpoison[cs], 0u)) word |= EC_DONE_POISON;
         if (d.mode != 1) {
-          if (d.mode == 0) L->t_rs = globaltimer_ns();
+          if (d.mode == 0) L->t_rs4[cs] = globaltimer_ns();
           for (int q = 0; q < d.P; ++q) st_relaxed_sys(&d.ctrl[q]->done_from[d.rank], word);
         } else {
           st_release_sys(&d.ctrl[d.rank]->done_from[d.rank], word);
@@ -635,6 +638,14 @@ __device__ __forceinline__ unsigned int ld_relaxed_sys_u32(const unsigned int* p
   return v;
 }
 
+// The controller runs the protocol of one "open" generation go (requests,
+// activation, snapshot, command) while up to two rounds are in flight: once
+// round g's command is out, the open generation is g + 1, so a rank whose next
+// offer is already queued (back-to-back rounds, the nccl-tests pattern) snapshots
+// g + 1 and exchanges its snapshot words DURING round g's data phase, and the
+// workers find g + 1's command waiting when they finish g (EcDesc::lead == 2,
+// fused TMA mode with R >= 3 result slots).  Round g is published when every
+// owner's done word for g is in; rounds publish in order.
 __device__ void engine_controller(const EcDesc& d, unsigned long long epoch) {
   EcLocal* L = d.local;
   EcHostCtl* H = d.hctl;
@@ -651,6 +662,11 @@ __device__ void engine_controller(const EcDesc& d, unsigned long long epoch) {
   unsigned long long t_snap = L->t_snap;
   unsigned long long t_req = 0;
   unsigned ns = 32;
+  // rounds whose command is out (0, 1 or d.lead), oldest = g; the open
+  // generation is go = g + n_issued.  Log data of an issued round, by gen & 1.
+  int n_issued = 0;
+  long long go = g;
+  unsigned long long iss_fresh[2], iss_has[2], iss_tsnap[2], iss_tcmd[2], iss_treq[2], iss_seq[2];
 
   // write this rank's word into every rank's control block (peer stores over NVLink)
   // (one sys-scope fence, then relaxed stores: a fence-based release; every
@@ -667,7 +683,7 @@ __device__ void engine_controller(const EcDesc& d, unsigned long long epoch) {
   };
   auto activate = [&]() {
     internal_act = 1;
-    if (d.flavor != 0 && !d.replay) push_all(0, (unsigned long long)g + 1);
+    if (d.flavor != 0 && !d.replay) push_all(0, (unsigned long long)go + 1);
   };
   auto forced_bit = [&](long long gen) -> int {
     if (gen >= d.n_forced) return -1;
@@ -679,8 +695,12 @@ __device__ void engine_controller(const EcDesc& d, unsigned long long epoch) {
   // snapshot check sees it (ec_wait's pin waits for the ack)
   unsigned long long host_pin = ld_relaxed_sys(&H->pin_lo);
   unsigned long long last_hs = ld_acquire_gpu(&L->hp_seq);
+  bool failed = false;
   while (true) {
     bool progress = false;
+    // the open generation takes protocol steps only while fewer than `lead`
+    // rounds are in flight
+    const bool open_ok = n_issued < d.lead;
     // Host-mapped words cost a PCIe round trip; the poller mirrors them (and
     // copies host-posted requests into the device ring), so this thread only
     // reads device memory.
@@ -699,7 +719,7 @@ __device__ void engine_controller(const EcDesc& d, unsigned long long epoch) {
     }
     // ---- requests, strictly in sequence order: stream-posted ones sit in the
     // device ring (cheap), host-posted ones only in the host-mapped ring
-    while (true) {
+    while (open_ok) {
       EcReq* dq = &L->dreq[next_req % EC_REQ_RING];
       unsigned type, fl;
       long long t, arg;
@@ -713,16 +733,23 @@ __device__ void engine_controller(const EcDesc& d, unsigned long long epoch) {
       dev_req = !(fl & EC_CF_HOSTPOSTED);
       fl &= ~EC_CF_HOSTPOSTED;
       unsigned long long status = 3;  // OK
-      // An offer for the NEXT generation while this rank has already done its
-      // part for round g (contributed or snapshotted): keep it at the head of
-      // the queue until g completes, then take it at once -- back-to-back
-      // rounds posted without host waits pay no post latency between them.
-      // (The application API never posts early; a buffer re-offered early must
-      // not change while round g still reads it.)
-      if (type == EC_REQ_CONTRIB && !(fl & EC_CF_POISON) && t == g + 1 &&
-          (snapped || contributed_round == g))
+      // while a round is in flight the open generation only moves on this
+      // rank's own boarding (its offer for go, or an activation of go); any
+      // other request waits for the round to publish, as the generation
+      // ordering of the reference's engine has it (SPEC.md concurrency model)
+      if (n_issued > 0 && !((type == EC_REQ_CONTRIB || type == EC_REQ_ACTIVATE) && t == go &&
+                            !(fl & EC_CF_POISON)))
         break;
-      if (type == EC_REQ_CONTRIB && !(fl & EC_CF_POISON) && t <= g) {
+      // An offer for the generation after the open one while this rank has
+      // already done its part for go (contributed or snapshotted): keep it at
+      // the head of the queue until go's command is out, then take it at once
+      // -- back-to-back rounds posted without host waits pay no post latency
+      // between them.  (The application API never posts early; a buffer
+      // re-offered early must not change while round go still reads it.)
+      if (type == EC_REQ_CONTRIB && !(fl & EC_CF_POISON) && t == go + 1 &&
+          (snapped || contributed_round == go))
+        break;
+      if (type == EC_REQ_CONTRIB && !(fl & EC_CF_POISON) && t <= go) {
         // guard ages: the offered stash now holds round t's gradient until a
         // fresh snapshot delivers it (eagersgd.py:117-124)
         if (t < pend_lo) pend_lo = t;
@@ -731,14 +758,14 @@ __device__ void engine_controller(const EcDesc& d, unsigned long long epoch) {
       if (type == EC_REQ_CONTRIB) {
         if (fl & EC_CF_POISON) {
           status = 4;
-        } else if (t < g || (t == g && snapped)) {
+        } else if (t < go || (t == go && snapped)) {
           status = 2;  // the round already consumed this rank's slot
           if (fl & EC_CF_SRC_GRAD) *(volatile int*)&L->late_copy = 1;  // keep the gradient
-        } else if (t > g) {
+        } else if (t > go) {
           status = 5;
           st_release_sys(&H->error_info, (unsigned long long)t);   // info before the code
           st_release_sys(&H->error, EC_DERR_ORDER);
-        } else if (d.replay && forced_bit(g) != 1) {
+        } else if (d.replay && forced_bit(go) != 1) {
           status = 2;
           if (fl & EC_CF_SRC_GRAD) *(volatile int*)&L->late_copy = 1;
         } else {
@@ -746,10 +773,10 @@ __device__ void engine_controller(const EcDesc& d, unsigned long long epoch) {
                           ((fl & EC_CF_SRC_GRAD) ? EC_SNAP_SRC_GRAD : 0ull));
           if ((fl & EC_CF_STEP) && dev_req && d.mode == 0 && d.W <= EC_PROG_W) {
             // the step's update kernel (already resident behind the offer)
-            // consumes round g's chunks as they land: owners publish arrival
-            // words to us; pin slot g on its behalf now (it unpins when done),
-            // before round g can even start
-            *(volatile unsigned long long*)&L->pin_dev = (unsigned long long)g;
+            // consumes round go's chunks as they land: owners publish arrival
+            // words to us; pin slot go on its behalf now (it unpins when
+            // done), before round go can even start
+            *(volatile unsigned long long*)&L->pin_dev = (unsigned long long)go;
             L->fuse_seq = next_req + 1;
             contrib |= (int)EC_SNAP_UPD;
           }
@@ -763,7 +790,7 @@ __device__ void engine_controller(const EcDesc& d, unsigned long long epoch) {
             // (nap = P), one NVLink exchange sooner than the arrival barrier
             internal_act = 1;
           } else if (fl & 4u) {  // all-arrive (majority: the initiator activates)
-            push_all(2, (unsigned long long)g + 1);
+            push_all(2, (unsigned long long)go + 1);
             arrive_pending = 1;
             arrive_activate = (fl & 2u) ? 1 : 0;
           } else if (fl & 2u) {
@@ -771,7 +798,7 @@ __device__ void engine_controller(const EcDesc& d, unsigned long long epoch) {
           }
         }
       } else if (type == EC_REQ_ACTIVATE) {
-        if (t == g) activate();
+        if (t == go) activate();
       } else if (type == EC_REQ_HOLD) {
         hold_from = arg;
       } else if (type == EC_REQ_GUARD) {
@@ -785,51 +812,52 @@ __device__ void engine_controller(const EcDesc& d, unsigned long long epoch) {
       progress = true;
     }
     // ---- all-arrive barrier (bench): everyone boarded -> activate
-    if (arrive_pending) {
+    if (open_ok && arrive_pending) {
       bool all = true;
       for (int q = 0; q < P && all; ++q)
-        all = ld_acquire_sys(&C->arrive_from[q]) >= (unsigned long long)g + 1;
+        all = ld_acquire_sys(&C->arrive_from[q]) >= (unsigned long long)go + 1;
       if (all) {
         arrive_pending = 0;
         if (arrive_activate) activate();
         progress = true;
       }
     }
-    // ---- snapshot decision (collectives.py:146-153, schedule.py:452-455)
-    if (!snapped) {
-      bool go = false;
+    // ---- snapshot decision (collectives.py:146-153, schedule.py:452-455);
+    // with a round in flight only once this rank boarded go itself
+    if (open_ok && !snapped && (n_issued == 0 || contributed_round == go)) {
+      bool sgo = false;
       if (d.replay) {
-        int b = forced_bit(g);
-        if (b == 0) go = true;
-        else if (b == 1) go = contrib != 0;
+        int b = forced_bit(go);
+        if (b == 0) sgo = true;
+        else if (b == 1) sgo = contrib != 0;
       } else if (internal_act) {
-        go = true;
+        sgo = true;
       } else if (d.flavor != 0) {
         bool ext = false;
-        for (int q = 0; q < P && !ext; ++q) ext = ld_acquire_sys(&C->act_from[q]) >= (unsigned long long)g + 1;
+        for (int q = 0; q < P && !ext; ++q) ext = ld_acquire_sys(&C->act_from[q]) >= (unsigned long long)go + 1;
         if (ext) {
           // staleness guard: an explicit threshold (ec_post_hold) or the
           // device-tracked ages (ec_post_guard), eagersgd.py:102-108
           const long long lo = pend_lo < last_off + 1 ? pend_lo : last_off + 1;
-          const bool aged = guard_tau != EC_INF_GEN && g >= lo + guard_tau;
-          const bool held = !stopping && contributed_round < g && (g >= hold_from || aged);
-          go = !held;
+          const bool aged = guard_tau != EC_INF_GEN && go >= lo + guard_tau;
+          const bool held = !stopping && contributed_round < go && (go >= hold_from || aged);
+          sgo = !held;
         }
       }
-      if (go && g >= d.R) {
-        // Result-slot reuse guard: peers write our slot g % R once the round
-        // starts, so never snapshot g while a reader still needs generation
-        // g - R.  Device readers pin in device memory (SC fence pairs with
+      if (sgo && go >= d.R) {
+        // Result-slot reuse guard: peers write our slot go % R once the round
+        // starts, so never snapshot go while a reader still needs generation
+        // go - R.  Device readers pin in device memory (SC fence pairs with
         // wait_and_pin); the host pin is the acknowledged cached value; our
         // own updater CTAs finish a fused update before upd_fin_gen moves.
         fence_sc_gpu();
-        const unsigned long long gr = (unsigned long long)(g - d.R);
-        if (ld_acquire_gpu(&L->pin_dev) <= gr || host_pin <= gr) go = false;
+        const unsigned long long gr = (unsigned long long)(go - d.R);
+        if (ld_acquire_gpu(&L->pin_dev) <= gr || host_pin <= gr) sgo = false;
       }
-      if (go) {
-        push_all(1, (((unsigned long long)g + 1) << EC_SNAP_SHIFT) | (unsigned long long)contrib);
+      if (sgo) {
+        push_all(1, (((unsigned long long)go + 1) << EC_SNAP_SHIFT) | (unsigned long long)contrib);
         t_snap = globaltimer_ns();
-        st_relaxed_sys(&H->snap_gen1, (unsigned long long)g + 1);
+        st_relaxed_sys(&H->snap_gen1, (unsigned long long)go + 1);
         if (contrib & (int)EC_SNAP_FRESH) {
           hold_from = EC_INF_GEN;  // stash delivered (eagersgd.py:117-124)
           pend_lo = EC_INF_GEN;
@@ -839,85 +867,104 @@ __device__ void engine_controller(const EcDesc& d, unsigned long long epoch) {
         progress = true;
       }
     }
-    // ---- round: all snapshots in -> two-shot reduction -> publish
-    if (snapped) {
+    // ---- round go: all snapshots in -> command to the workers (two-shot
+    // reduction in the fused TMA pipeline)
+    if (open_ok && snapped) {
       bool all = true;
       unsigned long long fresh = 0, has = 0, srcg = 0, updm = 0;
       for (int q = 0; q < P; ++q) {
         unsigned long long w = ld_acquire_sys(&C->snap_from[q]);
-        if ((w >> EC_SNAP_SHIFT) < (unsigned long long)g + 1) { all = false; break; }
+        if ((w >> EC_SNAP_SHIFT) < (unsigned long long)go + 1) { all = false; break; }
         fresh |= (w & EC_SNAP_FRESH) << q;
         has |= ((w >> 1) & 1ull) << q;
         srcg |= ((w >> 2) & 1ull) << q;
         updm |= ((w >> 3) & 1ull) << q;
       }
       if (all) {
-        bool timed_out = false;
-        L->cmd_gen = g;
-        L->cmd_has = has;
-        L->cmd_src = srcg;
-        L->cmd_updm = updm;
+        EcCmd* cm = &L->cmd[seq & 3];   // the command of sequence number seq + 1
+        cm->gen = go;
+        cm->has = has;
+        cm->src = srcg;
+        cm->updm = updm;
         ++seq;
-        const unsigned long long t0 = globaltimer_ns();
+        const int k = (int)(go & 1);
+        iss_fresh[k] = fresh;
+        iss_has[k] = has;
+        iss_tsnap[k] = t_snap;
+        iss_treq[k] = t_req;
+        iss_seq[k] = seq;
+        iss_tcmd[k] = globaltimer_ns();
         st_release_gpu(&L->cmd_seq, seq);
-        unsigned ns3 = 32;
-        // round complete at this rank: TMA mode needs every owner's pushes into
-        // our slot, pull mode only our own all-gather
-        unsigned long long poison = 0;
-        for (int q = (d.mode != 1 ? 0 : r); q < (d.mode != 1 ? P : r + 1) && !timed_out; ++q) {
-          unsigned long long wq;
-          while (((wq = ld_acquire_sys(&C->done_from[q])) & ~EC_DONE_POISON) < (unsigned long long)g + 1) {
-            if (globaltimer_ns() - t0 > d.timeout_ns) { timed_out = true; break; }
-            __nanosleep(ns3);
-            if (ns3 < 128) ns3 <<= 1;
-          }
-          poison |= wq & EC_DONE_POISON;
-        }
-        if (timed_out) {
-          st_release_sys(&H->error_info, (unsigned long long)g);
-          st_release_sys(&H->error, EC_DERR_TIMEOUT);
-          break;
-        }
-        const unsigned long long t_done = globaltimer_ns();
-        EcLog* lg = &H->log[g % EC_LOG_RING];
-        st_relaxed_sys(&lg->mask, fresh);
-        st_relaxed_sys(&lg->has, has);
-        st_relaxed_sys(&lg->nap, (unsigned long long)__popcll(fresh));
-        st_relaxed_sys(&lg->t_snap, t_snap);
-        st_relaxed_sys(&lg->t_cmd, t0);
-        st_relaxed_sys(&lg->t_rs, *(volatile unsigned long long*)&L->t_rs);
-        st_relaxed_sys(&lg->t_done, t_done);
-        st_relaxed_sys(&lg->t_req, t_req);
-        st_relaxed_sys(&lg->poison, poison ? 1ull : 0ull);
-        // the entry's own generation tag is record data (ring-overwrite check):
-        // it must be visible before done_gen1, so it goes before the fence
-        st_relaxed_sys(&lg->gen1, (unsigned long long)g + 1);
-        t_req = 0;
-        st_release_gpu(&L->done_gen1_dev, (unsigned long long)g + 1);  // device waiters first
-        fence_acq_rel_sys();                     // log entry before the host-visible flags
-        st_relaxed_sys(&H->done_gen1, (unsigned long long)g + 1);
-        ++g;
+        ++n_issued;
+        ++go;
         snapped = 0;
         contrib = 0;
         internal_act = 0;
         arrive_pending = 0;
         arrive_activate = 0;
+        t_req = 0;
+        progress = true;
+        continue;   // the next generation may already be decidable
+      }
+    }
+    // ---- the oldest round in flight: complete at this rank once every owner's
+    // data for g is in our slot (TMA mode) / our own all-gather is done (pull)
+    if (n_issued > 0) {
+      const int k = (int)(g & 1);
+      bool all = true;
+      unsigned long long poison = 0;
+      for (int q = (d.mode != 1 ? 0 : r); q < (d.mode != 1 ? P : r + 1) && all; ++q) {
+        const unsigned long long wq = ld_acquire_sys(&C->done_from[q]);
+        if ((wq & ~EC_DONE_POISON) < (unsigned long long)g + 1) all = false;
+        else if ((wq & ~EC_DONE_POISON) == (unsigned long long)g + 1) poison |= wq & EC_DONE_POISON;
+      }
+      if (!all) {
+        if (globaltimer_ns() - iss_tcmd[k] > d.timeout_ns) {
+          st_release_sys(&H->error_info, (unsigned long long)g);
+          st_release_sys(&H->error, EC_DERR_TIMEOUT);
+          failed = true;
+          break;
+        }
+      } else {
+        const unsigned long long t_done = globaltimer_ns();
+        EcLog* lg = &H->log[g % EC_LOG_RING];
+        st_relaxed_sys(&lg->mask, iss_fresh[k]);
+        st_relaxed_sys(&lg->has, iss_has[k]);
+        st_relaxed_sys(&lg->nap, (unsigned long long)__popcll(iss_fresh[k]));
+        st_relaxed_sys(&lg->t_snap, iss_tsnap[k]);
+        st_relaxed_sys(&lg->t_cmd, iss_tcmd[k]);
+        st_relaxed_sys(&lg->t_rs, *(volatile unsigned long long*)&L->t_rs4[(iss_seq[k] - 1) & 3]);
+        st_relaxed_sys(&lg->t_done, t_done);
+        st_relaxed_sys(&lg->t_req, iss_treq[k]);
+        st_relaxed_sys(&lg->poison, poison ? 1ull : 0ull);
+        // the entry's own generation tag is record data (ring-overwrite check):
+        // it must be visible before done_gen1, so it goes before the fence
+        st_relaxed_sys(&lg->gen1, (unsigned long long)g + 1);
+        st_release_gpu(&L->done_gen1_dev, (unsigned long long)g + 1);  // device waiters first
+        fence_acq_rel_sys();                     // log entry before the host-visible flags
+        st_relaxed_sys(&H->done_gen1, (unsigned long long)g + 1);
+        ++g;
+        --n_issued;
         progress = true;
         continue;
       }
     }
     if (stopping) {
-      const bool idle = !snapped && !arrive_pending;
-      if (idle || globaltimer_ns() - stop_t0 > 2000000000ull) break;
+      const bool idle = n_issued == 0 && !snapped && !arrive_pending;
+      if (idle || (n_issued == 0 && globaltimer_ns() - stop_t0 > 2000000000ull)) break;
     }
     if (progress) {
       ns = 32;
     } else {
       __nanosleep(ns);
-      if (ns < 512) ns <<= 1;
+      // a round in flight: poll its done words at a short interval
+      if (ns < (n_issued ? 128u : 512u)) ns <<= 1;
     }
   }
-  // park: persist the protocol state, release the workers, acknowledge
+  (void)failed;
+  // park: persist the protocol state, release the workers, acknowledge.  A
+  // parked engine has no round in flight (a watchdog timeout parks with the
+  // round abandoned; its error word is set).
   L->g = g;
   L->hold_from = hold_from;
   L->contributed_round = contributed_round;
@@ -1440,7 +1487,10 @@ ec_fold_auto_kernel(T* __restrict__ stash, const T* __restrict__ grad, long long
 }
 
 // wait for a generation >= t, pin it, publish it for the update (one thread)
-__device__ void wait_and_pin(EcLocal* L, EcHostCtl* H, long long t, int R,
+// `lead`: how far the engine's snapshot frontier may run ahead of the last
+// published generation (EcDesc::lead); a pin of G is safe once no snapshot of
+// G + R can have happened, i.e. while done + lead < G + R
+__device__ void wait_and_pin(EcLocal* L, EcHostCtl* H, long long t, int R, int lead,
                              unsigned long long timeout_ns, unsigned long long seq1) {
   const unsigned long long t0 = globaltimer_ns();
   unsigned long long d1;
@@ -1480,7 +1530,7 @@ __device__ void wait_and_pin(EcLocal* L, EcHostCtl* H, long long t, int R,
     st_relaxed_gpu(&L->pin_dev, (unsigned long long)G);
     fence_sc_gpu();
     const long long D = (long long)ld_acquire_gpu(&L->done_gen1_dev) - 1;
-    if (D < G + R - 1) break;
+    if (D < G + R - lead) break;
     G = D;
   }
   L->step_gen = G;
@@ -1504,10 +1554,10 @@ __global__ void ec_wait_done_kernel(EcLocal* L, EcHostCtl* H, long long t,
   }
 }
 
-__global__ void ec_wait_gen_kernel(EcLocal* L, EcHostCtl* H, long long t, int R,
+__global__ void ec_wait_gen_kernel(EcLocal* L, EcHostCtl* H, long long t, int R, int lead,
                                    unsigned long long timeout_ns) {
   if (threadIdx.x == 0) {
-    wait_and_pin(L, H, t, R, timeout_ns, 0);
+    wait_and_pin(L, H, t, R, lead, timeout_ns, 0);
     st_release_sys(&H->steptag[t % EC_REQ_RING], (unsigned long long)t + 1);
   }
 }
@@ -1687,7 +1737,7 @@ __device__ __forceinline__ void update_gen_body(T* __restrict__ w, T* __restrict
   __shared__ int s_late, s_fusedu;
   if (threadIdx.x == 0) {
     if (H != nullptr) {
-      if (blockIdx.x == 0) wait_and_pin(L, H, t, R, timeout_ns, seq1);
+      if (blockIdx.x == 0) wait_and_pin(L, H, t, R, dp->lead, timeout_ns, seq1);
       while (ld_acquire_gpu(&L->step_tag) != (unsigned long long)t + 1) __nanosleep(256);
     }
     s_gen = *(volatile const long long*)&L->step_gen;
@@ -2187,10 +2237,10 @@ cudaError_t launch_wait_done(EcLocal* L, EcHostCtl* H, long long t, unsigned lon
   return cudaGetLastError();
 }
 
-cudaError_t launch_wait_gen(EcLocal* L, EcHostCtl* H, long long t, int R, unsigned long long timeout_ns,
-                            cudaStream_t s) {
+cudaError_t launch_wait_gen(EcLocal* L, EcHostCtl* H, long long t, int R, int lead,
+                            unsigned long long timeout_ns, cudaStream_t s) {
   counted();
-  ec_wait_gen_kernel<<<1, 32, 0, s>>>(L, H, t, R, timeout_ns);
+  ec_wait_gen_kernel<<<1, 32, 0, s>>>(L, H, t, R, lead, timeout_ns);
   return cudaGetLastError();
 }
 
@@ -2198,7 +2248,7 @@ cudaError_t launch_update_gen(int dtype, void* w, void* mom, const char* ring, l
                               int R, EcLocal* L, double lr, double mu, long long n, EcHostCtl* H,
                               long long t, unsigned long long timeout_ns, unsigned long long seq1,
                               void* stash, const void* gbuf, const EcDesc* dp, int progressive,
-                              cudaStream_t s) {
+                              int share, cudaStream_t s) {
   counted();
   const int vec_ok = ((((uintptr_t)w) | ((uintptr_t)mom) | ((uintptr_t)ring) | slot_bytes) & 15) == 0;
   const int V = dtype == 0 ? 4 : 2;
@@ -2209,6 +2259,10 @@ cudaError_t launch_update_gen(int dtype, void* w, void* mom, const char* ring, l
   // much of the update after the round)
   const int per_sm = progressive ? 2 : 4;
   int grid = (int)(gb < (long long)sms() * per_sm ? gb : (long long)sms() * per_sm);
+  // ranks sharing one GPU (emulated worlds): each rank's update may spin on a
+  // round another local rank has yet to join, so together they must leave that
+  // rank room to run -- split the wave between the local ranks
+  if (share > 1) grid = grid / share > 0 ? grid / share : 1;
   if (const char* e = getenv("EC_UPD_GRID")) {
     const int g = atoi(e);
     if (g > 0 && g < grid) grid = g;

@@ -95,6 +95,8 @@ def replay_training(trace, element: str = "f4", device: int = 0, world=None, rin
     ledger=dict, masks=[steps] device masks, rows=eagercoll-train-v1 rows
     sorted by (round, rank); see replay_rank for loss_fn).
     """
+    if hasattr(trace, "files"):       # an NpzFile is not safe to read from P threads
+        trace = {k: trace[k] for k in trace.files}
     p = int(trace["p"])
     steps = int(trace["steps"])
     masks = [int(m) for m in np.asarray(trace["masks"])]

@@ -851,3 +851,51 @@ def test_back_to_back_pinned_reads_and_concurrent_readers():
     world.close()
     assert not errors, errors[0]
     assert not bad, bad[:5]
+
+
+@pytest.mark.parametrize("flavor", ["solo", "majority"])
+def test_pipelined_rounds_with_two_in_flight(flavor):
+    """Back-to-back rounds posted without waits (the nccl-tests pattern): the
+    engine snapshots round g+1 and issues its command while round g's data
+    phase runs (EcDesc::lead = 2).  Every round's mask is all-ones and the
+    result is the tree-order sum; rounds publish in order."""
+    from paper_1908_04207_b200.harness import _gen_times, rounds_pipelined
+    p, n, k = 4, 300_001, 24
+    world = EmulatedWorld(p)
+    cfg = CollectiveConfig(p=p, flavor=flavor, vector_len=n, element="f4", seed=1234)
+    hs = [AllreduceHandle(cfg, r, world) for r in range(p)]
+    rng = np.random.default_rng(5)
+    x = rng.standard_normal((p, n)).astype(np.float32)
+    for r in range(p):
+        hs[r].send_buffer().copy_(torch.as_tensor(x[r], device="cuda"))
+    streams = [torch.cuda.Stream() for _ in range(p)]
+    world.synchronize()
+    errors: list = []
+
+    def body(r):
+        try:
+            torch.cuda.set_device(0)
+            with torch.cuda.stream(streams[r]):
+                rounds_pipelined(hs[r], 0, k)
+        except BaseException as e:  # surfaced below
+            errors.append(e)
+
+    th = [threading.Thread(target=body, args=(r,), daemon=True) for r in range(p)]
+    for t in th:
+        t.start()
+    for t in th:
+        t.join()
+    assert not errors, errors[0]
+    u, inc, _ = R.allreduce_round(list(x), [True] * p, np.float32)
+    overlapped = 0
+    for r in range(p):
+        assert hs[r].done_generation == k - 1
+        g, res = hs[r].wait_blocking(k - 1)
+        assert g == k - 1 and res.included == inc and res.nap == p
+        assert _np(res.u).tobytes() == u.tobytes()
+        times = [_gen_times(hs[r], gg) for gg in range(k)]
+        for gg in range(1, k):
+            assert times[gg][3] >= times[gg - 1][3]            # published in order
+            overlapped += times[gg][1] < times[gg - 1][3]      # g+1 issued before g published
+    print(f"{flavor}: {overlapped} of {p * (k - 1)} rounds issued before the previous published")
+    world.close()

@@ -84,6 +84,12 @@ def test_lstm_config4_eager_sgd_steps():
     w0 = states[0].w.cpu().numpy().copy()
     data = SyntheticUCF101(batch=4, max_len=48)
     streams = [torch.cuda.Stream() for _ in range(p)]
+    # a library's first use on a new stream (cuBLAS workspaces, autograd) may
+    # synchronise the device: warm every rank's stream before an engine is
+    # resident (library hazards)
+    for r in range(p):
+        with torch.cuda.stream(streams[r]):
+            lstm_grad_step(models[r], hs[r].grad_buffer(), data.batch_for(r, 99))
     world.synchronize()
     g_first, w_first, losses, naps, errors = {}, {}, {}, {}, []
 
