@@ -101,6 +101,14 @@ int ec_comm_start(ec_comm_t* c);
 /* Drain and stop the engine at a round boundary so device-wide syncs return;
  * ec_comm_start resumes it with all protocol state preserved. */
 int ec_comm_pause(ec_comm_t* c, int timeout_ms);
+/* Idle park (no reference counterpart; the simulator has no resident kernel):
+ * after EC_IDLE_PARK_MS (default 100, 0 = never) with no API call and no
+ * completed round, and nothing outstanding, a library thread parks the
+ * engine so device-wide syncs in user code (torch.cuda.synchronize,
+ * cudaFree) return; the next post relaunches it, and for remote peers the
+ * thread relaunches it when a peer activates, snapshots or boards the next
+ * generation.  Counters of parks / wakes and whether it is parked now. */
+int ec_comm_idle_stats(ec_comm_t* c, uint64_t* parks, uint64_t* wakes, int* parked);
 int ec_comm_destroy(ec_comm_t* c);
 /* Device error word (watchdog timeout, out-of-order round): the reference's
  * TimeoutError / AssertionError (collectives.py:298,331). */

@@ -146,7 +146,9 @@ struct alignas(128) EcLocal {
   unsigned long long hp_seq;       // changes of the mirrored host pin (monotone)
   unsigned long long hp_lo;        // mirrored host pin (EcHostCtl::pin_lo)
   unsigned long long hp_ps;        // the pin_seq it was read with (acknowledged)
-  unsigned long long hp_stop;      // epoch whose stop request the poller saw
+  unsigned long long hp_stop;      // epoch whose stop request the poller saw (0: none)
+  unsigned long long hp_stop_kind; // 1 = explicit pause, 2 = idle park (only when idle)
+  unsigned long long park_votes;   // rank_lo's copy: local controllers agreeing to an idle park
   // staleness guard (controller-owned, persisted across pause/resume): a
   // generation g is held until this rank contributes when
   // g >= min(pend_lo, last_off + 1) + guard_tau -- the oldest gradient not yet
@@ -174,7 +176,7 @@ struct alignas(64) EcLog {
 };
 
 struct alignas(128) EcHostCtl {
-  unsigned long long stop;          // host -> engine: drain and exit
+  unsigned long long stop;          // host -> engine: 1 drain and exit, 2 exit if idle (idle park)
   unsigned long long pin_lo;        // host -> engine: lowest generation the host still reads
   unsigned long long pin_seq;       // host -> engine: bumped with every host pin
   unsigned long long pin_ack;       // engine -> host: last pin_seq the controller has seen
@@ -218,6 +220,8 @@ struct EcDesc {
   char* uc_stage;                     // NVLS: this rank's unicast view of the staging region
   EcHostCtl* hctl;
   EcLocal* local;
+  unsigned long long* park_votes;     // &local of rank_lo ->park_votes (shared by the launch)
+  int n_local;                        // controllers in this launch
   const unsigned long long* forced;
 };
 

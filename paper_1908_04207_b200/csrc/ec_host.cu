@@ -11,9 +11,12 @@
 #include <string.h>
 #include <time.h>
 
+#include <atomic>
+#include <chrono>
 #include <map>
 #include <mutex>
 #include <string>
+#include <thread>
 #include <vector>
 
 #include "../../include/eagercoll_b200.h"
@@ -170,6 +173,18 @@ struct ec_comm {
   CUdeviceptr mc_va = 0, uc_va = 0;
   size_t mc_size = 0;
   char* ring_cuda = nullptr;  // the cudaMalloc'd ring, restored when NVLS is torn down
+  // idle park (see watcher_main): the engine exits on its own after
+  // EC_IDLE_PARK_MS without work, so device-wide syncs in user code return;
+  // any post relaunches it, and a watcher relaunches it for remote peers
+  std::recursive_mutex live_mu;        // posts, starts, pauses, the watcher's park/relaunch
+  std::thread watcher;
+  std::atomic<bool> quit{false};
+  std::atomic<bool> parked_auto{false};
+  std::atomic<unsigned long long> last_api_ns{0};
+  unsigned long long idle_ns = 0;      // 0: never park on idleness
+  unsigned long long* poll_buf = nullptr;   // pinned: peers' words, read while parked
+  cudaStream_t ws = nullptr;           // watcher's copy stream
+  unsigned long long idle_parks = 0, idle_wakes = 0;
 };
 
 static int check_li(ec_comm_t* c, int li) {
@@ -545,6 +560,11 @@ int ec_comm_create(int world_size, int rank_lo, int n_local, int device, int64_t
     }
   }
   if (const char* env = getenv("EC_TIMEOUT_S")) c->timeout_ns = (unsigned long long)(atof(env) * 1e9);
+  {
+    const char* env = getenv("EC_IDLE_PARK_MS");
+    const double ms = env ? atof(env) : 100.0;
+    c->idle_ns = ms > 0 ? (unsigned long long)(ms * 1e6) : 0ull;
+  }
   c->ctrl.assign(world_size, nullptr);
   c->send.assign(world_size, nullptr);
   c->ring.assign(world_size, nullptr);
@@ -721,6 +741,8 @@ static int upload_descs(ec_comm_t* c) {
     }
     x.hctl = r->hd;
     x.local = r->local;
+    x.park_votes = &c->L[0]->local->park_votes;
+    x.n_local = c->n_local;
     x.forced = r->forced;
     astore(&r->h->stop, 0ull);
   }
@@ -728,26 +750,159 @@ static int upload_descs(ec_comm_t* c) {
   return EC_OK;
 }
 
+static inline void touch(ec_comm_t* c) { c->last_api_ns.store(now_ns(), std::memory_order_relaxed); }
+
+// (re)launch the persistent engine for a new epoch; caller holds live_mu
+static int launch_epoch(ec_comm_t* c) {
+  CK(cudaSetDevice(c->device));
+  for (EcRankHost* r : c->L) astore(&r->h->stop, 0ull);
+  c->epoch += 1;
+  // the launch's park-vote counter starts from zero (stream-ordered before it)
+  CK(cudaMemsetAsync(&c->L[0]->local->park_votes, 0, sizeof(unsigned long long), c->es));
+  CK(launch_engine(c->dtype, c->d_descs, c->n_local, 1 + c->W, c->epoch, c->smem_bytes, c->es));
+  c->parked_auto.store(false);
+  return EC_OK;
+}
+
+// Every posting entry point runs under live_mu and calls this first: a
+// communicator the watcher parked for idleness is relaunched before the post.
+static int ensure_live(ec_comm_t* c) {
+  touch(c);
+  if (c->running && c->parked_auto.load()) {
+    c->idle_wakes += 1;
+    return launch_epoch(c);
+  }
+  return EC_OK;
+}
+
+// True when every local rank's engine has exited launch `epoch`.
+static bool all_exited(ec_comm_t* c) {
+  for (EcRankHost* r : c->L)
+    if (aload(&r->h->exited) != c->epoch) return false;
+  return true;
+}
+
+// Idle park.  A persistent engine makes every device-wide synchronisation
+// (torch.cuda.synchronize, cudaFree in the caching allocator, cuDNN's RNN
+// setup, lazy module loads) wait for it.  This thread parks the engine once
+// the communicator has had no API call and completed no round for idle_ns and
+// nothing is outstanding (every reserved request processed, no snapshot
+// pending publication): it asks the controllers to exit if idle (stop = 2;
+// the local controllers vote and exit together), so user syncs return.  The
+// next post relaunches the engine (ensure_live).  While parked, a rank with
+// remote peers polls its control block for their activation / snapshot /
+// arrival words of its next generation and relaunches when one appears (the
+// peers' round needs this rank's snapshot and owner shard).
+static void watcher_main(ec_comm_t* c) {
+  cudaSetDevice(c->device);
+  unsigned long long last_done = ~0ull, last_change = now_ns();
+  const bool remote = c->P > c->n_local;
+  while (!c->quit.load()) {
+    const bool parked = c->parked_auto.load();
+    std::this_thread::sleep_for(std::chrono::microseconds(parked && remote ? 100 : 1000));
+    std::unique_lock<std::recursive_mutex> lk(c->live_mu);
+    if (c->quit.load() || !c->running) continue;
+    const unsigned long long now = now_ns();
+    if (!c->parked_auto.load()) {
+      unsigned long long dsum = 0;
+      for (EcRankHost* r : c->L) dsum += aload(&r->h->done_gen1);
+      if (dsum != last_done) {
+        last_done = dsum;
+        last_change = now;
+      }
+      const unsigned long long api = c->last_api_ns.load(std::memory_order_relaxed);
+      const unsigned long long last = api > last_change ? api : last_change;
+      if (now - last < c->idle_ns) continue;
+      bool idle = true;
+      for (EcRankHost* r : c->L)
+        idle = idle && aload(&r->h->req_done) == r->next_seq &&
+               aload(&r->h->snap_gen1) == aload(&r->h->done_gen1) && !aload(&r->h->error);
+      if (!idle) continue;
+      for (EcRankHost* r : c->L) astore(&r->h->stop, 2ull);
+      Backoff bo;
+      while (!all_exited(c) && !bo.expired(20)) bo.pause();
+      if (!all_exited(c)) {
+        // not idle after all (a peer's round arrived): withdraw; a park the
+        // controllers had already committed to still completes
+        for (EcRankHost* r : c->L) astore(&r->h->stop, 0ull);
+        Backoff b2;
+        bool any = false;
+        while (!b2.expired(2)) b2.pause();
+        for (EcRankHost* r : c->L) any = any || aload(&r->h->exited) == c->epoch;
+        if (!any) {
+          last_change = now_ns();
+          continue;
+        }
+        while (!all_exited(c)) std::this_thread::sleep_for(std::chrono::microseconds(50));
+      }
+      cudaStreamSynchronize(c->es);
+      for (EcRankHost* r : c->L) astore(&r->h->stop, 0ull);
+      c->parked_auto.store(true);
+      c->idle_parks += 1;
+    } else if (remote) {
+      bool wake = false;
+      for (EcRankHost* r : c->L) {
+        const unsigned long long g1 = aload(&r->h->done_gen1) + 1;   // next generation + 1
+        const size_t words = (size_t)3 * EC_MAX_P;
+        if (cudaMemcpyAsync(c->poll_buf, r->ctrl, words * sizeof(unsigned long long),
+                            cudaMemcpyDeviceToHost, c->ws) != cudaSuccess ||
+            cudaStreamSynchronize(c->ws) != cudaSuccess)
+          break;
+        const unsigned long long* act = c->poll_buf;
+        const unsigned long long* snap = c->poll_buf + EC_MAX_P;
+        for (int q = 0; q < c->P && !wake; ++q)
+          wake = act[q] >= g1 || (snap[q] >> EC_SNAP_SHIFT) >= g1;
+        if (!wake) {   // arrive_from sits after rsdone_from in EcCtrl
+          if (cudaMemcpyAsync(c->poll_buf, r->ctrl->arrive_from, EC_MAX_P * sizeof(unsigned long long),
+                              cudaMemcpyDeviceToHost, c->ws) == cudaSuccess &&
+              cudaStreamSynchronize(c->ws) == cudaSuccess)
+            for (int q = 0; q < c->P && !wake; ++q) wake = c->poll_buf[q] >= g1;
+        }
+        if (wake) break;
+      }
+      if (wake) {
+        c->idle_wakes += 1;
+        launch_epoch(c);
+        last_change = now_ns();
+      }
+    }
+  }
+}
+
 int ec_comm_start(ec_comm_t* c) {
   if (!c) return fail(EC_E_ARG, "null communicator");
-  if (c->running) return EC_OK;
+  std::lock_guard<std::recursive_mutex> lk(c->live_mu);
+  touch(c);
+  if (c->running) return ensure_live(c);
   int rc = upload_descs(c);
   if (rc) return rc;
   if (c->direct) {
     c->running = true;
     return EC_OK;
   }
-  c->epoch += 1;
-  CK(launch_engine(c->dtype, c->d_descs, c->n_local, 1 + c->W, c->epoch, c->smem_bytes, c->es));
+  if ((rc = launch_epoch(c))) return rc;
   c->running = true;
+  if (c->idle_ns && !c->watcher.joinable()) {
+    if (!c->poll_buf && cudaHostAlloc((void**)&c->poll_buf, 3 * EC_MAX_P * sizeof(unsigned long long),
+                                      cudaHostAllocDefault) != cudaSuccess)
+      return fail(EC_E_NOMEM, "watcher buffer");
+    if (!c->ws) CK(cudaStreamCreateWithFlags(&c->ws, cudaStreamNonBlocking));
+    c->watcher = std::thread(watcher_main, c);
+  }
   return EC_OK;
 }
 
 int ec_comm_pause(ec_comm_t* c, int timeout_ms) {
   if (!c) return fail(EC_E_ARG, "null communicator");
+  std::lock_guard<std::recursive_mutex> lk(c->live_mu);
   if (!c->running) return EC_OK;
   if (c->direct) {
     c->running = false;
+    return EC_OK;
+  }
+  if (c->parked_auto.load()) {     // already parked by the idle watcher
+    c->running = false;
+    c->parked_auto.store(false);
     return EC_OK;
   }
   for (EcRankHost* r : c->L) astore(&r->h->stop, 1ull);
@@ -769,6 +924,8 @@ int ec_comm_pause(ec_comm_t* c, int timeout_ms) {
 int ec_comm_destroy(ec_comm_t* c) {
   if (!c) return EC_OK;
   int rc = EC_OK;
+  c->quit.store(true);
+  if (c->watcher.joinable()) c->watcher.join();
   cudaSetDevice(c->device);
   if (c->running) rc = ec_comm_pause(c, 10000);
   if (c->running) {
@@ -797,6 +954,8 @@ int ec_comm_destroy(ec_comm_t* c) {
   }
   if (c->d_descs) cudaFree(c->d_descs);
   if (c->es) cudaStreamDestroy(c->es);
+  if (c->ws) cudaStreamDestroy(c->ws);
+  if (c->poll_buf) cudaFreeHost(c->poll_buf);
   budget_release(c);
   delete c;
   return rc;
@@ -894,6 +1053,8 @@ static int host_post(ec_comm_t* c, int li, unsigned type, unsigned flags, long l
   int rc = check_li(c, li);
   if (rc) return rc;
   EcRankHost* r = c->L[li];
+  std::lock_guard<std::recursive_mutex> live(c->live_mu);
+  if ((rc = ensure_live(c))) return rc;
   std::lock_guard<std::mutex> g(r->mu);
   unsigned long long seq;
   if ((rc = reserve_seq(c, r, &seq))) return rc;
@@ -919,6 +1080,8 @@ int ec_post_contribute(ec_comm_t* c, int li, int64_t t, uint32_t flags, void* st
   int rc = check_li(c, li);
   if (rc) return rc;
   EcRankHost* r = c->L[li];
+  std::lock_guard<std::recursive_mutex> live(c->live_mu);
+  if ((rc = ensure_live(c))) return rc;
   std::lock_guard<std::mutex> g(r->mu);
   unsigned long long seq;
   if ((rc = reserve_seq(c, r, &seq))) return rc;
@@ -950,6 +1113,7 @@ int ec_post_guard(ec_comm_t* c, int li, int64_t tau, int64_t pending_lo, uint64_
 int ec_reply(ec_comm_t* c, int li, uint64_t seq, int timeout_ms, int* status) {
   int rc = check_li(c, li);
   if (rc) return rc;
+  touch(c);
   EcRankHost* r = c->L[li];
   Backoff bo;
   while (true) {
@@ -1037,6 +1201,7 @@ int ec_wait(ec_comm_t* c, int li, int64_t t, int timeout_ms, int pin, int64_t* g
             uint64_t* mask, int* nap) {
   int rc = check_li(c, li);
   if (rc) return rc;
+  touch(c);
   EcRankHost* r = c->L[li];
   Backoff bo;
   unsigned long long d1;
@@ -1065,7 +1230,8 @@ int ec_wait(ec_comm_t* c, int li, int64_t t, int timeout_ms, int pin, int64_t* g
       __atomic_store_n(&r->h->pin_lo, (unsigned long long)G, __ATOMIC_SEQ_CST);
       const unsigned long long ps = __atomic_add_fetch(&r->h->pin_seq, 1ull, __ATOMIC_SEQ_CST);
       Backoff ab;
-      while (c->running && aload(&r->h->pin_ack) < ps) {  // a parked engine re-reads at start
+      // a parked engine (paused, or parked for idleness) re-reads the pin at start
+      while (c->running && !c->parked_auto.load() && aload(&r->h->pin_ack) < ps) {
         if ((rc = device_error(r))) return rc;
         if (ab.expired(timeout_ms < 0 ? 10000 : timeout_ms))
           return fail(EC_E_TIMEOUT, "rank %d: engine did not acknowledge the pin", r->rank);
@@ -1214,7 +1380,11 @@ int ec_step_async(ec_comm_t* c, int li, int64_t t, const void* grad, uint32_t fl
   if (c->dtype == EC_I64) return fail(EC_E_ARG, "eager-SGD step needs a float dtype");
   EcRankHost* r = c->L[li];
   cudaStream_t s = (cudaStream_t)stream;
+  // reservation and launches under live_mu: the idle watcher never parks with
+  // a reserved request outstanding
+  std::lock_guard<std::recursive_mutex> live(c->live_mu);
   if (!c->running && (rc = ec_comm_start(c))) return rc;
+  if ((rc = ensure_live(c))) return rc;
   unsigned long long seq;
   {
     std::lock_guard<std::mutex> g(r->mu);
@@ -1260,6 +1430,7 @@ int ec_step_result(ec_comm_t* c, int li, uint64_t seq, int64_t t, int timeout_ms
                    int64_t* gen, uint64_t* mask, int* nap) {
   int rc = check_li(c, li);
   if (rc) return rc;
+  touch(c);
   EcRankHost* r = c->L[li];
   if ((rc = ec_reply(c, li, seq, timeout_ms, status))) return rc;
   if (status && (*status == EC_R_POISONED || *status == EC_R_ERROR)) return EC_OK;
@@ -1381,6 +1552,15 @@ int ec_debug_state(ec_comm_t* c, int li, int64_t* out) {
   out[13] = (int64_t)loc.cmd_seq;
   out[14] = (int64_t)loc.round_done;
   out[15] = (int64_t)loc.next_req;
+  return EC_OK;
+}
+
+int ec_comm_idle_stats(ec_comm_t* c, uint64_t* parks, uint64_t* wakes, int* parked) {
+  if (!c) return fail(EC_E_ARG, "null communicator");
+  std::lock_guard<std::recursive_mutex> lk(c->live_mu);
+  if (parks) *parks = c->idle_parks;
+  if (wakes) *wakes = c->idle_wakes;
+  if (parked) *parked = c->parked_auto.load() ? 1 : 0;
   return EC_OK;
 }
 

@@ -657,7 +657,8 @@ __device__ void engine_controller(const EcDesc& d, unsigned long long epoch) {
   int snapped = L->snapped, contrib = L->contrib, internal_act = L->internal_act;
   int arrive_pending = L->arrive_pending, arrive_activate = L->arrive_activate;
   unsigned long long seq = L->cmd_seq;
-  bool stopping = false;
+  bool stopping = false, idle_stop = false;
+  bool voted = false, park_now = false;
   unsigned long long stop_t0 = 0;
   unsigned long long t_snap = L->t_snap;
   unsigned long long t_req = 0;
@@ -712,9 +713,24 @@ __device__ void engine_controller(const EcDesc& d, unsigned long long epoch) {
         st_release_sys(&H->pin_ack, *(volatile unsigned long long*)&L->hp_ps);
         last_hs = hs;
       }
-      if (!stopping && ld_acquire_gpu(&L->hp_stop) == epoch) {
-        stopping = true;
-        stop_t0 = globaltimer_ns();
+      // stop requests: an explicit pause drains the open generation (a held
+      // one is let go); an idle park (host watchdog, ec_host.cu) exits only
+      // while nothing is in flight, and may be withdrawn
+      const bool st_now = ld_acquire_gpu(&L->hp_stop) == epoch;
+      if (st_now && !stopping) stop_t0 = globaltimer_ns();
+      stopping = st_now;
+      idle_stop = st_now && *(volatile unsigned long long*)&L->hp_stop_kind == 2;
+      if (!idle_stop && voted) {
+        // withdrawn: take the vote back -- unless every controller had voted,
+        // in which case the park is committed (the others may be gone)
+        unsigned long long v = ld_acquire_gpu(d.park_votes);
+        while (v < (unsigned long long)d.n_local) {
+          const unsigned long long o = atomicCAS(d.park_votes, v, v - 1);
+          if (o == v) break;
+          v = o;
+        }
+        if (v >= (unsigned long long)d.n_local) park_now = true;
+        else voted = false;
       }
     }
     // ---- requests, strictly in sequence order: stream-posted ones sit in the
@@ -840,7 +856,8 @@ __device__ void engine_controller(const EcDesc& d, unsigned long long epoch) {
           // device-tracked ages (ec_post_guard), eagersgd.py:102-108
           const long long lo = pend_lo < last_off + 1 ? pend_lo : last_off + 1;
           const bool aged = guard_tau != EC_INF_GEN && go >= lo + guard_tau;
-          const bool held = !stopping && contributed_round < go && (go >= hold_from || aged);
+          const bool held = !(stopping && !idle_stop) && contributed_round < go &&
+                            (go >= hold_from || aged);
           sgo = !held;
         }
       }
@@ -949,9 +966,20 @@ __device__ void engine_controller(const EcDesc& d, unsigned long long epoch) {
         continue;
       }
     }
+    if (park_now) break;
     if (stopping) {
       const bool idle = n_issued == 0 && !snapped && !arrive_pending;
-      if (idle || (n_issued == 0 && globaltimer_ns() - stop_t0 > 2000000000ull)) break;
+      if (idle_stop) {
+        // every controller of the launch must agree (they exit together and the
+        // host relaunches them together): vote while idle, leave when all have
+        if (idle && !voted) {
+          atomicAdd(d.park_votes, 1ull);
+          voted = true;
+        }
+        if (voted && ld_acquire_gpu(d.park_votes) >= (unsigned long long)d.n_local) break;
+      } else if (idle || (n_issued == 0 && globaltimer_ns() - stop_t0 > 2000000000ull)) {
+        break;
+      }
     }
     if (progress) {
       ns = 32;
@@ -1006,7 +1034,14 @@ __device__ void engine_host_poller(const EcDesc& d, unsigned long long epoch) {
       last_ps = ps;
       last_lo = lo;
     }
-    if (ld_relaxed_sys(&H->stop)) st_release_gpu(&L->hp_stop, epoch);
+    {
+      const unsigned long long sk = ld_relaxed_sys(&H->stop);
+      if (sk != *(volatile unsigned long long*)&L->hp_stop_kind ||
+          (sk != 0) != (ld_acquire_gpu(&L->hp_stop) == epoch)) {
+        *(volatile unsigned long long*)&L->hp_stop_kind = sk;
+        st_release_gpu(&L->hp_stop, sk ? epoch : 0ull);
+      }
+    }
     while (true) {
       EcReq* dq = &L->dreq[pn % EC_REQ_RING];
       if (ld_acquire_gpu(&dq->seq1) == pn + 1) {   // stream-posted: nothing to copy

@@ -8,6 +8,7 @@ prints one JSON object with every check's outcome; the exit code is non-zero
 if any check failed on any rank.  Driven by tests/test_multigpu.py.
 """
 
+import ctypes as C
 import hashlib
 import json
 import os
@@ -289,6 +290,99 @@ def main():
                 out[f"{flavor}_{element}"] = "bit-exact"
         return out
 
+    def bench_schedule_replay():
+        """The reference's config-2/3 bench schedules for this world size
+        (tests/golden/c2c3_bench.npz) replayed with forced masks across
+        processes at N = 25,559,081 fp32: accepted offers and masks as
+        recorded, every observed slot bit-exact vs the fp32 restatement."""
+        from paper_1908_04207_b200.replay import replay_bench_rank
+        z = np.load(os.path.join(ROOT, "tests", "golden", "c2c3_bench.npz"))
+        names = sorted({k.split("/")[0] for k in z.files if k.endswith(f"_p{world}/meta")})
+        if not names:
+            return {"skipped": f"no recorded schedule for p={world}"}
+        n = 25_559_081
+        out = {}
+        for name in names:
+            flavor = name.split("_")[0]
+            p, rounds, seed = (int(x) for x in z[f"{name}/meta"])
+            masks, acc, obs = z[f"{name}/masks"], z[f"{name}/accepted"], z[f"{name}/observed"]
+            host = [np.random.default_rng([seed, r]).standard_normal(n, dtype=np.float32)
+                    for r in range(p)]
+            expected = {}
+            for m in sorted(set(int(x) for x in masks)):
+                c = [host[r] if (m >> r) & 1 else None for r in range(p)]
+                u, _, _ = R.allreduce_round(c, [x is not None for x in c], np.float32, n)
+                expected[m] = torch.as_tensor(u, device="cuda")
+            cfg = CollectiveConfig(p=p, flavor=flavor, vector_len=n, element="f4", seed=seed)
+            h = AllreduceHandle(cfg, rank, pw, cid=next_cid())
+            pw.pause()
+            h.comm.set_replay(0, [int(m) for m in masks])
+            pw.resume()
+            vec = torch.as_tensor(host[rank], device="cuda")
+            dist.barrier()
+            o = replay_bench_rank(h, vec, masks, acc[rank], obs[rank],
+                                  lambda g, m, slot: m == int(masks[g]) and
+                                  torch.equal(slot, expected[m]))
+            h.close()
+            assert o["accepted"] == [bool(a) for a in acc[rank]], name
+            assert o["masks_seen"] == [int(masks[g]) for g in obs[rank]], name
+            assert all(o["verified"]), (name, o["verified"].index(False))
+            out[name] = f"{rounds} rounds bit-exact"
+        return out
+
+    def pipelined_two_in_flight():
+        """Back-to-back 100 MB rounds posted without waits: round g+1's
+        snapshot exchange overlaps round g's data phase (EcDesc lead 2); the
+        results are bit-exact and rounds publish in order."""
+        from paper_1908_04207_b200.harness import _gen_times, rounds_pipelined
+        n, k = 25_000_000, 12
+        out = {}
+        for flavor in ("solo", "majority"):
+            rng = np.random.default_rng(11)
+            contrib = rng.standard_normal((world, n), dtype=np.float32)
+            want, inc, _ = R.allreduce_round(list(contrib), [True] * world, np.float32)
+            cfg = CollectiveConfig(p=world, flavor=flavor, vector_len=n, element="f4", seed=1234)
+            h = AllreduceHandle(cfg, rank, pw, cid=next_cid())
+            h.send_buffer().copy_(torch.as_tensor(contrib[rank], device="cuda"))
+            torch.cuda.current_stream().synchronize()
+            dist.barrier()
+            ms = rounds_pipelined(h, 0, k)
+            g, res = h.wait_blocking(k - 1)
+            assert g == k - 1 and res.included == inc
+            assert res.u.cpu().numpy().tobytes() == want.tobytes(), flavor
+            times = [_gen_times(h, gg) for gg in range(k)]
+            ov = sum(times[i][1] < times[i - 1][3] for i in range(1, k))
+            h.close()
+            out[flavor] = {"overlapped": int(ov), "us_per_round": ms * 1e3 / k}
+        return out
+
+    def idle_park_remote_wake():
+        """Every engine parks after EC_IDLE_PARK_MS without work (device-wide
+        syncs return); then rank 0 alone starts a solo round: the other ranks'
+        watchers see its activation in their control blocks and relaunch their
+        engines, so the round completes for everyone without their hosts posting."""
+        cfg = CollectiveConfig(p=world, flavor="solo", vector_len=4096, element="f4")
+        h = AllreduceHandle(cfg, rank, pw, cid=next_cid())
+        vec = torch.full((4096,), float(rank + 1), device="cuda")
+        for t in range(2):
+            h._contribute(t, vec, fresh=True, activate=True, all_arrive=True)
+            h.wait_blocking(t)
+        dist.barrier()
+        time.sleep(0.5)                       # > EC_IDLE_PARK_MS (100 ms): every engine parks
+        torch.cuda.synchronize()              # returns: no resident engine
+        parks, wakes, parked = C.c_uint64(), C.c_uint64(), C.c_int()
+        call("ec_comm_idle_stats", h.comm.ptr, C.byref(parks), C.byref(wakes), C.byref(parked))
+        assert parked.value == 1 and parks.value >= 1, (parks.value, parked.value)
+        dist.barrier()
+        if rank == 0:
+            assert h._contribute(2, vec, fresh=True, activate=True)
+        g, res = h.wait_blocking(2, timeout=20.0)
+        call("ec_comm_idle_stats", h.comm.ptr, C.byref(parks), C.byref(wakes), C.byref(parked))
+        h.close()
+        assert g == 2 and res.included == 1 and res.u.cpu()[0].item() == 1.0 / world
+        assert wakes.value >= 1
+        return {"parks": int(parks.value), "wakes": int(wakes.value)}
+
     check("sync_f64_golden", sync_f64_golden)
     check("sync_f32_sizes", sync_f32_sizes)
     check("solo_first_arrival", solo_first_arrival)
@@ -298,6 +392,10 @@ def main():
     check("stream_barrier", stream_barrier)
     check("nvls_fast_mode", nvls_fast_mode)
     check("replay_c1", replay_c1)
+    check("bench_schedule_replay", bench_schedule_replay)
+    check("pipelined_two_in_flight", pipelined_two_in_flight)
+    if not shared_gpus:
+        check("idle_park_remote_wake", idle_park_remote_wake)
 
     gathered = [None] * world
     dist.all_gather_object(gathered, results)

@@ -899,3 +899,76 @@ def test_pipelined_rounds_with_two_in_flight(flavor):
             overlapped += times[gg][1] < times[gg - 1][3]      # g+1 issued before g published
     print(f"{flavor}: {overlapped} of {p * (k - 1)} rounds issued before the previous published")
     world.close()
+
+
+def test_idle_park_lets_device_syncs_return():
+    """A resident engine makes device-wide syncs wait for it.  After
+    EC_IDLE_PARK_MS (100 ms) without work the library parks it, so a user's
+    bare torch.cuda.synchronize() / empty_cache() between steps returns; the
+    next step relaunches the engine and results stay bit-exact."""
+    import ctypes as C
+
+    from paper_1908_04207_b200 import finish_step, train_step_async
+    from paper_1908_04207_b200._lib import call
+    p, n, lr = 2, 10_007, 0.05
+    world = EmulatedWorld(p)
+    cfg = CollectiveConfig(p=p, flavor="solo", vector_len=n, element="f4")
+    hs = [AllreduceHandle(cfg, r, world) for r in range(p)]
+    rng = np.random.default_rng(4)
+    grads = rng.standard_normal((6, p, n)).astype(np.float32)
+    w0 = rng.standard_normal(n).astype(np.float32)
+    st = [TrainState.fresh(w0, lr, rank=r, tau=None) for r in range(p)]
+    streams = [torch.cuda.Stream() for _ in range(p)]
+    world.synchronize()
+
+    def run(t0, k):
+        errs = []
+
+        def body(r):
+            try:
+                torch.cuda.set_device(0)
+                with torch.cuda.stream(streams[r]):
+                    for t in range(t0, t0 + k):
+                        g = torch.as_tensor(grads[t, r], device="cuda")
+                        finish_step(st[r], hs[r], train_step_async(st[r], hs[r], g,
+                                                                    all_arrive=True))
+                    streams[r].synchronize()
+            except BaseException as e:  # surfaced below
+                errs.append(e)
+
+        th = [threading.Thread(target=body, args=(r,), daemon=True) for r in range(p)]
+        for x in th:
+            x.start()
+        for x in th:
+            x.join()
+        assert not errs, errs[0]
+
+    run(0, 3)
+    done = threading.Event()
+
+    def user_sync():
+        torch.cuda.synchronize()
+        torch.cuda.empty_cache()
+        done.set()
+
+    t0 = time.time()
+    th = threading.Thread(target=user_sync, daemon=True)
+    th.start()
+    th.join(timeout=15)
+    assert done.is_set(), "device-wide sync did not return with an idle engine resident"
+    waited = time.time() - t0
+    parks, wakes, parked = C.c_uint64(), C.c_uint64(), C.c_int()
+    call("ec_comm_idle_stats", hs[0].comm.ptr, C.byref(parks), C.byref(wakes), C.byref(parked))
+    assert parks.value >= 1 and parked.value == 1
+    run(3, 3)                                  # the next post relaunches the engine
+    call("ec_comm_idle_stats", hs[0].comm.ptr, C.byref(parks), C.byref(wakes), C.byref(parked))
+    assert wakes.value >= 1
+    w = w0.copy()
+    for t in range(6):
+        u, _, _ = R.allreduce_round(list(grads[t]), [True] * p, np.float32)
+        w = R.sgd_update(w, u, lr)
+    world.synchronize()
+    for r in range(p):
+        assert st[r].w.cpu().numpy().tobytes() == w.tobytes()
+    print(f"device sync returned after {waited * 1e3:.0f} ms (idle park)")
+    world.close()
