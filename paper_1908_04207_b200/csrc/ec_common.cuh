@@ -202,8 +202,9 @@ struct EcDesc {
   int R, W, replay, vec;              // ring slots, worker CTAs, replay flag, elems / 16 B
   int lead;                           // rounds the engine may have in flight (1, or 2: the
                                       // next round's snapshot overlaps the current data phase)
-  int mode;                           // data phase: 0 = fused TMA, 1 = two-phase ld.cg pull,
-                                      // 2 = NVLS (multimem.ld_reduce / multimem.st, fast mode)
+  int mode;                           // data phase: 0 = fused TMA two-shot, 1 = two-phase ld.cg
+                                      // pull, 2 = NVLS (multimem.ld_reduce / multimem.st, fast
+                                      // mode), 3 = fused TMA one-shot (small messages)
   int chv, stages;                    // TMA chunk (16-B vectors) and pipeline depth
   int sig_every;                      // chunks per arrival word (progressive updates; 0 = ~4/round)
   int smem_bytes;

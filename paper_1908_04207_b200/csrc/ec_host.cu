@@ -550,7 +550,15 @@ int ec_comm_create(int world_size, int rank_lo, int n_local, int device, int64_t
     while (chb > 1024 && (long long)st * (world_size + 1) * chb > 200 * 1024) chb /= 2;
     c->chv = chb / 16;
     c->stages = st;
-    c->smem_bytes = c->mode == 0 ? st * (world_size + 1) * chb : 0;
+    // one-shot for small messages (each rank pulls every slice and reduces
+    // the whole vector into its own slot): no push / remote completion on the
+    // round's critical path
+    if (c->mode == 0 && world_size > 1) {
+      const char* e = getenv("EC_ONESHOT_BYTES");
+      const long long lim = e ? atoll(e) : 65536;
+      if (n_elems * c->elem <= lim) c->mode = 3;
+    }
+    c->smem_bytes = (c->mode == 0 || c->mode == 3) ? st * (world_size + 1) * chb : 0;
   }
   if (!c->direct) {
     const int brc = budget_engine(c, w_default);
@@ -726,7 +734,7 @@ static int upload_descs(ec_comm_t* c) {
     x.smem_bytes = c->smem_bytes;
     // two rounds in flight (the next one's snapshot overlaps this one's data
     // phase) need the fused TMA pipeline and a third result slot for readers
-    c->lead = (c->mode == 0 && c->R >= 3 && !getenv("EC_NO_LEAD")) ? 2 : 1;
+    c->lead = ((c->mode == 0 || c->mode == 3) && c->R >= 3 && !getenv("EC_NO_LEAD")) ? 2 : 1;
     x.lead = c->lead;
     for (int q = 0; q < c->P; ++q) {
       x.ctrl[q] = c->ctrl[q];

@@ -266,14 +266,23 @@ __device__ __forceinline__ void signal_chunks(const EcDesc& d, int w, long long 
   }
 }
 
+//
+// One-shot (mode 3, small messages): every rank's workers take ALL chunks,
+// pull every contributing rank's slice and store the reduced chunk into the
+// rank's OWN slot only -- no push to peers and no remote-store completion on
+// the critical path.  The done word then means "my reads of everyone's
+// buffers and my own slot are complete", which is what both the peers (their
+// send buffers are free) and this rank (its result is in) wait for.
 template <typename T>
 __device__ void round_tma(const EcDesc& d, const char* const* sp, int w, long long g,
                           unsigned long long has, char* smem, unsigned long long* full,
-                          unsigned long long& it, bool& bad, unsigned long long updm) {
+                          unsigned long long& it, bool& bad, unsigned long long updm,
+                          bool oneshot) {
   const int P = d.P, r = d.rank, S = d.stages;
   const int chv = d.chv, chb = d.chv * 16;
   const long long nch = (d.nvec + chv - 1) / chv;
-  const long long c0 = chunk_lo(nch, r, P), c1 = chunk_lo(nch, r + 1, P);
+  const long long c0 = oneshot ? 0 : chunk_lo(nch, r, P), c1 = oneshot ? nch : chunk_lo(nch, r + 1, P);
+  if (oneshot) updm = 0;
   const long long mine = (c1 - c0 > w) ? (c1 - c0 - w + d.W - 1) / d.W : 0;
   const long long off = (g % d.R) * d.slot_bytes;
   const size_t stage_bytes = (size_t)(P + 1) * chb;
@@ -316,7 +325,7 @@ __device__ void round_tma(const EcDesc& d, const char* const* sp, int w, long lo
     fence_proxy_async_smem();
     __syncthreads();
     if (threadIdx.x == 0) {
-      for (int j = 0; j < P; ++j) {
+      for (int j = 0; j < (oneshot ? 1 : P); ++j) {
         const int q = (r + j) % P;  // own slot first, then peers round-robin
         tma_store(d.ring[q] + off + v0 * 16, out, (unsigned)nvv * 16);
       }
@@ -341,7 +350,7 @@ __device__ void round_tma(const EcDesc& d, const char* const* sp, int w, long lo
 // scalar tail (n % V elements): reduced by the last owner, pushed to every slot
 template <typename T>
 __device__ void tail_push(const EcDesc& d, const char* const* sp, unsigned long long has,
-                          long long g) {
+                          long long g, bool oneshot = false) {
   const long long e = d.nvec * Ops<T>::V + threadIdx.x;
   if (threadIdx.x >= Ops<T>::V || e >= d.n) return;
   const bool pow2 = (d.P & (d.P - 1)) == 0;
@@ -353,6 +362,10 @@ __device__ void tail_push(const EcDesc& d, const char* const* sp, unsigned long 
   };
   const T u = Ops<T>::divp(tree_sum_dyn<T>(d.P, leaf), d.P, inv, pow2);
   const long long off = (g % d.R) * d.slot_bytes;
+  if (oneshot) {
+    reinterpret_cast<volatile T*>(d.ring[d.rank] + off)[e] = u;
+    return;
+  }
   for (int q = 0; q < d.P; ++q) reinterpret_cast<volatile T*>(d.ring[q] + off)[e] = u;
 }
 
@@ -599,9 +612,12 @@ __device__ void engine_worker(const EcDesc& d, int w, unsigned long long epoch) 
     for (int q = tid; q < d.P; q += blockDim.x) sp[q] = ((s_src >> q) & 1ull) ? d.gbuf[q] : d.send[q];
     __syncthreads();
     bool bad = false;
-    if (d.mode == 0) {
-      round_tma<T>(d, sp, w, g, has, smem, full, it, bad, s_updm);
-      if (w == 0 && d.rank == d.P - 1) tail_push<T>(d, sp, has, g);
+    if (d.mode == 0 || d.mode == 3) {
+      const bool oneshot = d.mode == 3;
+      round_tma<T>(d, sp, w, g, has, smem, full, it, bad, s_updm, oneshot);
+      // the scalar tail: reduced by the last owner and pushed to every slot,
+      // or (one-shot) by every rank into its own slot
+      if (w == 0 && (oneshot || d.rank == d.P - 1)) tail_push<T>(d, sp, has, g, oneshot);
     } else if (d.mode == 2) {
       round_nvls<T>(d, sp, w, g, has, seen, bad);
     } else {
@@ -619,7 +635,7 @@ __device__ void engine_worker(const EcDesc& d, int w, unsigned long long epoch) 
         unsigned long long word = (unsigned long long)g + 1;
         if (atomicExch(&L->rpoison[cs], 0u)) word |= EC_DONE_POISON;
         if (d.mode != 1) {
-          if (d.mode == 0) L->t_rs4[cs] = globaltimer_ns();
+          if (d.mode == 0 || d.mode == 3) L->t_rs4[cs] = globaltimer_ns();
           for (int q = 0; q < d.P; ++q) st_relaxed_sys(&d.ctrl[q]->done_from[d.rank], word);
         } else {
           st_release_sys(&d.ctrl[d.rank]->done_from[d.rank], word);
