@@ -684,6 +684,44 @@ __device__ void engine_controller(const EcDesc& d, unsigned long long epoch) {
   int n_issued = 0;
   long long go = g;
   unsigned long long iss_fresh[2], iss_has[2], iss_tsnap[2], iss_tcmd[2], iss_treq[2], iss_seq[2];
+  // Host-visible words (replies, the log, done_gen1) cost a PCIe drain at the
+  // next sys fence, so they are written after the NVLink-facing work of the
+  // iteration (the next snapshot's push) and published behind ONE fence:
+  // replies of processed requests are buffered (status by seq & 15) ...
+  unsigned char rep_st[16];
+  unsigned long long rep_from = next_req;
+  // ... and a completed round's log entry waits as the pending publication
+  int pub_pending = 0;
+  long long pub_gen = 0;
+  unsigned long long pub_fresh = 0, pub_has = 0, pub_tsnap = 0, pub_tcmd = 0, pub_trs = 0,
+                     pub_tdone = 0, pub_treq = 0, pub_poison = 0;
+  auto flush_replies = [&]() {
+    if (rep_from == next_req) return;
+    for (unsigned long long q = rep_from; q < next_req; ++q)
+      st_relaxed_sys(&H->reply[q % EC_REQ_RING], ((q + 1) << 8) | rep_st[q & 15]);
+    st_relaxed_sys(&H->req_done, next_req);
+    rep_from = next_req;
+  };
+  auto publish_host = [&]() {
+    flush_replies();
+    if (!pub_pending) return;
+    EcLog* lg = &H->log[pub_gen % EC_LOG_RING];
+    st_relaxed_sys(&lg->mask, pub_fresh);
+    st_relaxed_sys(&lg->has, pub_has);
+    st_relaxed_sys(&lg->nap, (unsigned long long)__popcll(pub_fresh));
+    st_relaxed_sys(&lg->t_snap, pub_tsnap);
+    st_relaxed_sys(&lg->t_cmd, pub_tcmd);
+    st_relaxed_sys(&lg->t_rs, pub_trs);
+    st_relaxed_sys(&lg->t_done, pub_tdone);
+    st_relaxed_sys(&lg->t_req, pub_treq);
+    st_relaxed_sys(&lg->poison, pub_poison);
+    // the entry's own generation tag is record data (ring-overwrite check):
+    // it must be visible before done_gen1, so it goes before the fence
+    st_relaxed_sys(&lg->gen1, (unsigned long long)pub_gen + 1);
+    fence_acq_rel_sys();                     // log entry (and replies) before done_gen1
+    st_relaxed_sys(&H->done_gen1, (unsigned long long)pub_gen + 1);
+    pub_pending = 0;
+  };
 
   // write this rank's word into every rank's control block (peer stores over NVLink)
   // (one sys-scope fence, then relaxed stores: a fence-based release; every
@@ -815,13 +853,15 @@ __device__ void engine_controller(const EcDesc& d, unsigned long long epoch) {
           contributed_round = t;
           status = 1;
           t_req = globaltimer_ns();
-          if ((fl & 4u) && (fl & 2u) && d.flavor != 2 && !d.replay) {
-            // all-arrive, solo/sync: every rank boards with its own activation,
-            // so each snapshots its own fresh offer without broadcasting one;
-            // the round still starts only when every rank's snapshot is in
-            // (nap = P), one NVLink exchange sooner than the arrival barrier
+          if ((fl & 4u) && !d.replay && ((fl & 2u) || d.flavor == 2)) {
+            // all-arrive: every rank boards, so every rank's snapshot is its
+            // own fresh offer whatever activates the round (solo/sync: its own
+            // activation; majority: the designated initiator, which activates
+            // only after everyone arrived) -- each snapshots at once and the
+            // round starts when every snapshot is in (nap = P), without the
+            // arrival barrier and activation exchanges
             internal_act = 1;
-          } else if (fl & 4u) {  // all-arrive (majority: the initiator activates)
+          } else if (fl & 4u) {  // all-arrive in replay mode: arrival barrier
             push_all(2, (unsigned long long)go + 1);
             arrive_pending = 1;
             arrive_activate = (fl & 2u) ? 1 : 0;
@@ -837,10 +877,10 @@ __device__ void engine_controller(const EcDesc& d, unsigned long long epoch) {
         guard_tau = arg < 0 ? EC_INF_GEN : arg;
         if (t >= 0 && t < pend_lo) pend_lo = t;
       }
-      st_relaxed_sys(&H->reply[next_req % EC_REQ_RING], ((next_req + 1) << 8) | status);
+      rep_st[next_req & 15] = (unsigned char)status;
       ++next_req;
-      st_relaxed_sys(&H->req_done, next_req);
       st_release_gpu(&L->req_done_dev, next_req);
+      if (next_req - rep_from >= 16) flush_replies();
       progress = true;
     }
     // ---- all-arrive barrier (bench): everyone boarded -> activate
@@ -940,6 +980,8 @@ __device__ void engine_controller(const EcDesc& d, unsigned long long epoch) {
         continue;   // the next generation may already be decidable
       }
     }
+    // host-visible words of this iteration's work (after any snapshot push)
+    publish_host();
     // ---- the oldest round in flight: complete at this rank once every owner's
     // data for g is in our slot (TMA mode) / our own all-gather is done (pull)
     if (n_issued > 0) {
@@ -960,22 +1002,20 @@ __device__ void engine_controller(const EcDesc& d, unsigned long long epoch) {
         }
       } else {
         const unsigned long long t_done = globaltimer_ns();
-        EcLog* lg = &H->log[g % EC_LOG_RING];
-        st_relaxed_sys(&lg->mask, iss_fresh[k]);
-        st_relaxed_sys(&lg->has, iss_has[k]);
-        st_relaxed_sys(&lg->nap, (unsigned long long)__popcll(iss_fresh[k]));
-        st_relaxed_sys(&lg->t_snap, iss_tsnap[k]);
-        st_relaxed_sys(&lg->t_cmd, iss_tcmd[k]);
-        st_relaxed_sys(&lg->t_rs, *(volatile unsigned long long*)&L->t_rs4[(iss_seq[k] - 1) & 3]);
-        st_relaxed_sys(&lg->t_done, t_done);
-        st_relaxed_sys(&lg->t_req, iss_treq[k]);
-        st_relaxed_sys(&lg->poison, poison ? 1ull : 0ull);
-        // the entry's own generation tag is record data (ring-overwrite check):
-        // it must be visible before done_gen1, so it goes before the fence
-        st_relaxed_sys(&lg->gen1, (unsigned long long)g + 1);
-        st_release_gpu(&L->done_gen1_dev, (unsigned long long)g + 1);  // device waiters first
-        fence_acq_rel_sys();                     // log entry before the host-visible flags
-        st_relaxed_sys(&H->done_gen1, (unsigned long long)g + 1);
+        publish_host();                          // at most one publication waits
+        pub_gen = g;
+        pub_fresh = iss_fresh[k];
+        pub_has = iss_has[k];
+        pub_tsnap = iss_tsnap[k];
+        pub_tcmd = iss_tcmd[k];
+        pub_trs = *(volatile unsigned long long*)&L->t_rs4[(iss_seq[k] - 1) & 3];
+        pub_tdone = t_done;
+        pub_treq = iss_treq[k];
+        pub_poison = poison ? 1ull : 0ull;
+        pub_pending = 1;
+        // device waiters (the async step's update) see it at once; the host
+        // after the next snapshot push (publish_host)
+        st_release_gpu(&L->done_gen1_dev, (unsigned long long)g + 1);
         ++g;
         --n_issued;
         progress = true;
@@ -1006,6 +1046,7 @@ __device__ void engine_controller(const EcDesc& d, unsigned long long epoch) {
     }
   }
   (void)failed;
+  publish_host();
   // park: persist the protocol state, release the workers, acknowledge.  A
   // parked engine has no round in flight (a watchdog timeout parks with the
   // round abandoned; its error word is set).

@@ -188,9 +188,11 @@ def allreduce_sweep(world, rank, p, sizes_bytes, flavor="solo", rounds_cap=50, w
 
 
 def bench_flavor(world, rank, p, flavor, model, rounds=64, vector_len=64, link_slack_us=1000,
-                 seed=1234):
+                 seed=1234, barrier=None, close=True, cid=None):
     """harness.py:206-241 on hardware: rank r sleeps to t*period + delay[r, t],
-    then call_round; returns its BenchRecords."""
+    then call_round; returns its BenchRecords.  `barrier` aligns the ranks'
+    round origin (default: the world's process-group barrier; emulated ranks
+    in threads pass a thread barrier and close=False, closing after all)."""
     import numpy as np
 
     from .collectives import AllreduceHandle, CollectiveConfig, drive, initiator_for_round
@@ -198,10 +200,10 @@ def bench_flavor(world, rank, p, flavor, model, rounds=64, vector_len=64, link_s
     delays = delay_table(model, p, rounds)
     period = int(delays.max()) + link_slack_us + 1000
     cfg = CollectiveConfig(p=p, flavor=flavor, vector_len=vector_len, element="f8", seed=seed)
-    h = AllreduceHandle(cfg, rank, world, cid=2000 + hash(flavor) % 100)
+    h = AllreduceHandle(cfg, rank, world, cid=2000 + hash(flavor) % 100 if cid is None else cid)
     vec = np.full(vector_len, float(rank + 1))
     recs = []
-    world._barrier()
+    (barrier or world._barrier)()
     origin = time.perf_counter()
     for t in range(rounds):
         target = origin + (t * period + int(delays[rank, t])) * 1e-6
@@ -213,7 +215,8 @@ def bench_flavor(world, rank, p, flavor, model, rounds=64, vector_len=64, link_s
         lat = int((time.perf_counter() - t0) * 1e6)
         init = initiator_for_round(seed, res.rnd, p) if flavor == "majority" else -1
         recs.append(BenchRecord(flavor, t, rank, lat, res.nap, init))
-    h.close()
+    if close:
+        h.close()
     return recs
 
 

@@ -1,0 +1,79 @@
+"""The reference's analytic latency / NAP oracles for the imbalance bench
+(pkg/tests/test_harness.py:41-76) on the device, through harness.bench_flavor:
+P=4, per-round skew (r+1)*unit.  A sync round closes when rank 3 arrives, so
+rank r waits (3-r)*unit inside the call; a solo round is over before anyone
+else arrives (latency ~0, nap 1); a majority round closes when its designated
+initiator arrives: rank r waits max(0, init-r)*unit and nap = init+1.
+
+Real clocks replace the simulator's: unit = 2 ms and latencies are checked
+within a host-jitter tolerance; masks and naps exactly."""
+
+import threading
+
+import numpy as np
+import pytest
+import torch
+
+from paper_1908_04207_b200 import EmulatedWorld, initiator_for_round
+from paper_1908_04207_b200.harness import bench_flavor, summarize
+from paper_1908_04207_b200.transport import DelayModel
+
+pytestmark = pytest.mark.gpu
+
+UNIT_US = 2000
+TOL_US = 700
+
+
+def _run(flavor, rounds, p=4, seed=1234):
+    world = EmulatedWorld(p)
+    model = DelayModel("linear_skew", unit_ms=UNIT_US / 1000)
+    bar = threading.Barrier(p)
+    out, errors = {}, []
+
+    def body(r):
+        try:
+            torch.cuda.set_device(0)
+            out[r] = bench_flavor(world, r, p, flavor, model, rounds=rounds, vector_len=8,
+                                  seed=seed, barrier=bar.wait, close=False, cid=7)
+        except BaseException as e:  # surfaced below
+            errors.append(e)
+
+    th = [threading.Thread(target=body, args=(r,), daemon=True) for r in range(p)]
+    for x in th:
+        x.start()
+    for x in th:
+        x.join()
+    world.close()
+    assert not errors, errors[0]
+    return [b for r in range(p) for b in out[r]]
+
+
+def test_sync_latency_matches_the_arrival_math():
+    recs = _run("sync", rounds=4)
+    for b in recs:
+        assert b.nap == 4
+        assert abs(b.latency_us - (3 - b.rank) * UNIT_US) < TOL_US, b
+
+
+def test_solo_latency_is_near_zero_and_nap_one_under_strict_skew():
+    recs = _run("solo", rounds=4)
+    for b in recs:
+        assert b.nap == 1, b
+        assert b.latency_us < TOL_US, b
+
+
+def test_majority_latency_tracks_the_initiator():
+    recs = _run("majority", rounds=8)
+    for b in recs:
+        init = initiator_for_round(1234, b.round, 4)
+        assert b.initiator == init
+        assert b.nap == init + 1, b
+        assert abs(b.latency_us - max(0, init - b.rank) * UNIT_US) < TOL_US, b
+
+
+def test_flavor_ordering_under_skew():
+    recs = _run("sync", 4) + _run("solo", 4) + _run("majority", 4)
+    s = summarize(recs)
+    lat = {f: s["flavors"][f]["mean_latency_us"] for f in ("sync", "solo", "majority")}
+    assert lat["solo"] < lat["majority"] < lat["sync"]
+    assert s["flavors"]["solo"]["mean_nap"] == 1.0 and s["flavors"]["sync"]["mean_nap"] == 4.0
