@@ -79,6 +79,12 @@ int ec_comm_export(ec_comm_t* c, int local_idx, void* blob, size_t cap, size_t* 
 /* Map a remote rank's buffers from its exported blob (the peer side of
  * transport.register_engine, transport.py:205-214). */
 int ec_comm_import(ec_comm_t* c, int peer_rank, const void* blob, size_t len);
+/* Majority with a quorum (opt-in extension; the reference's rule, the default
+ * 0, activates at the designated initiator's arrival without counting,
+ * collectives.py:311-317): the initiator_for_round rank activates only once
+ * at least `min_arrivals` ranks (ceil(P/2) for "at least half", the
+ * north_star's phrasing) have boarded the generation.  Before ec_comm_start. */
+int ec_comm_set_quorum(ec_comm_t* c, int min_arrivals);
 /* Replay mode: force generation g's inclusion mask to masks[g] (g < n) --
  * participation recorded from a reference run, so the
  * snapshot decisions of collectives.py:146-153 are reproduced exactly. */

@@ -175,14 +175,14 @@ def bench_delays(model: DelayModel, p: int, rounds: int) -> np.ndarray:
     return d
 
 
-def bench_masks(flavor: str, delays: np.ndarray, seed: int) -> np.ndarray:
+def bench_masks(flavor: str, delays: np.ndarray, seed: int, quorum: int = 0) -> np.ndarray:
     """Inclusion mask of every bench round (harness.py:206-241 with the
     activation rules of collectives.py:146-153, 311-317).
 
     The bench cadence gives every round its own slot, so rank r arrives at
     offset delays[r, t] and the round starts when its activator arrives: the
-    first arrival (solo), the designated initiator (majority) or the last
-    arrival (sync).  A rank is fresh iff it arrived no later than that moment
+    first arrival (solo), the designated initiator (majority; with the opt-in
+    quorum rule, not before the quorum-th arrival) or the last arrival (sync).  A rank is fresh iff it arrived no later than that moment
     (the injected offsets differ by >= 200 us, far above the few link hops the
     activation takes); everyone else's slot is snapshotted null."""
     p, rounds = delays.shape
@@ -193,6 +193,8 @@ def bench_masks(flavor: str, delays: np.ndarray, seed: int) -> np.ndarray:
             a = arr.min()
         elif flavor == MAJORITY:
             a = arr[initiator_for_round(seed, t, p)]
+            if quorum:   # the opt-in quorum rule: also wait for the quorum-th arrival
+                a = max(a, np.sort(arr)[quorum - 1])
         else:
             a = arr.max()
         out[t] = sum(1 << r for r in range(p) if arr[r] <= a)

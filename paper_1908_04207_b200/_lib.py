@@ -37,6 +37,7 @@ _SIGS = {
     "ec_comm_export": (_i32, [_vp, _i32, _vp, C.c_size_t, _P(C.c_size_t)]),
     "ec_comm_import": (_i32, [_vp, _i32, _vp, C.c_size_t]),
     "ec_comm_set_replay": (_i32, [_vp, _i32, _P(_u64), _i64]),
+    "ec_comm_set_quorum": (_i32, [_vp, _i32]),
     "ec_comm_start": (_i32, [_vp]),
     "ec_nvls_supported": (_i32, [_i32]),
     "ec_nvls_create": (_i32, [_vp, _vp, C.c_size_t, _P(C.c_size_t)]),

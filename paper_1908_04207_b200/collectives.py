@@ -47,9 +47,10 @@ REDUCTION_MODES = ("fixed_order", "fast")
 
 @dataclass(frozen=True)
 class CollectiveConfig:
-    """collectives.py:43-67, plus `element="f4"` (the product's fp32 path) and
+    """collectives.py:43-67, plus `element="f4"` (the product's fp32 path),
     `reduction_mode`: "fixed_order" (bit-exact tree order) or "fast" (NVSwitch
-    in-switch reduction; results within fp32 rounding, identical on all ranks)."""
+    in-switch reduction; results within fp32 rounding, identical on all ranks),
+    and the opt-in `majority_quorum`."""
 
     p: int
     flavor: str
@@ -57,6 +58,11 @@ class CollectiveConfig:
     element: str = "f8"
     seed: int = 0
     reduction_mode: str = "fixed_order"
+    # majority only, opt-in: the designated initiator activates once at least
+    # half the ranks (ceil(p/2)) have boarded -- the north_star's phrasing;
+    # False (default) is the reference's rule: it activates on arrival
+    # without counting (collectives.py:311-317)
+    majority_quorum: bool = False
 
     def __post_init__(self):
         if self.p < 1:
@@ -71,6 +77,8 @@ class CollectiveConfig:
             raise ValueError(f"element must be one of {sorted(ELEMENTS)}")
         if self.reduction_mode not in REDUCTION_MODES:
             raise ValueError(f"reduction_mode must be one of {REDUCTION_MODES}")
+        if self.majority_quorum and self.flavor != MAJORITY:
+            raise ValueError("majority_quorum applies to the majority flavor only")
 
     @property
     def mask_words(self) -> int:

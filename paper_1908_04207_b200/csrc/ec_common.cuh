@@ -200,6 +200,8 @@ struct alignas(128) EcHostCtl {
 struct EcDesc {
   int rank, P, flavor, dtype;
   int R, W, replay, vec;              // ring slots, worker CTAs, replay flag, elems / 16 B
+  int quorum;                         // majority: arrivals the initiator waits for (0: none,
+                                      // the reference's rule, collectives.py:311-317)
   int lead;                           // rounds the engine may have in flight (1, or 2: the
                                       // next round's snapshot overlaps the current data phase)
   int mode;                           // data phase: 0 = fused TMA two-shot, 1 = two-phase ld.cg

@@ -166,6 +166,7 @@ struct ec_comm {
   unsigned long long epoch = 0;
   int mode = 0, chv = 256, stages = 4, smem_bytes = 0;  // data phase (see EcDesc)
   int lead = 1;                                        // rounds in flight (EcDesc::lead)
+  int quorum = 0;                                      // majority quorum (EcDesc::quorum)
   double budget = 0.0;                                 // SMs' worth of engine CTAs held
   // NVLS (reduction_mode "fast"): multicast object over every rank's GPU
   CUmemGenericAllocationHandle mc_handle = 0, mc_phys = 0;
@@ -634,6 +635,14 @@ int ec_comm_create(int world_size, int rank_lo, int n_local, int device, int64_t
   return EC_OK;
 }
 
+int ec_comm_set_quorum(ec_comm_t* c, int min_arrivals) {
+  if (!c) return fail(EC_E_ARG, "null communicator");
+  if (c->running) return fail(EC_E_STATE, "set the quorum before the engine starts");
+  if (min_arrivals < 0 || min_arrivals > c->P) return fail(EC_E_ARG, "quorum out of range");
+  c->quorum = min_arrivals;
+  return EC_OK;
+}
+
 int ec_comm_export(ec_comm_t* c, int li, void* blob, size_t cap, size_t* len) {
   int rc = check_li(c, li);
   if (rc) return rc;
@@ -736,6 +745,7 @@ static int upload_descs(ec_comm_t* c) {
     // phase) need the fused TMA pipeline and a third result slot for readers
     c->lead = ((c->mode == 0 || c->mode == 3) && c->R >= 3 && !getenv("EC_NO_LEAD")) ? 2 : 1;
     x.lead = c->lead;
+    x.quorum = c->flavor == EC_MAJORITY ? c->quorum : 0;
     for (int q = 0; q < c->P; ++q) {
       x.ctrl[q] = c->ctrl[q];
       x.send[q] = c->send[q];

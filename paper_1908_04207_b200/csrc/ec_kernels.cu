@@ -740,6 +740,18 @@ __device__ void engine_controller(const EcDesc& d, unsigned long long epoch) {
     internal_act = 1;
     if (d.flavor != 0 && !d.replay) push_all(0, (unsigned long long)go + 1);
   };
+  // majority with a quorum (EcDesc::quorum > 0, the north_star's phrasing):
+  // the designated initiator activates only once at least `quorum` ranks have
+  // boarded this generation (every boarding rank pushes an arrival word)
+  const bool quorum_mode = d.flavor == 2 && d.quorum > 0 && !d.replay;
+  auto initiator_activate = [&]() {
+    if (quorum_mode) {
+      arrive_pending = d.quorum;      // arrivals needed before activating
+      arrive_activate = 1;
+    } else {
+      activate();
+    }
+  };
   auto forced_bit = [&](long long gen) -> int {
     if (gen >= d.n_forced) return -1;
     return (int)((d.forced[gen] >> r) & 1ull);
@@ -863,14 +875,18 @@ __device__ void engine_controller(const EcDesc& d, unsigned long long epoch) {
             internal_act = 1;
           } else if (fl & 4u) {  // all-arrive in replay mode: arrival barrier
             push_all(2, (unsigned long long)go + 1);
-            arrive_pending = 1;
+            arrive_pending = P;
             arrive_activate = (fl & 2u) ? 1 : 0;
-          } else if (fl & 2u) {
-            activate();
+          } else {
+            if (quorum_mode) push_all(2, (unsigned long long)go + 1);   // counted by the initiator
+            if (fl & 2u) initiator_activate();
           }
         }
       } else if (type == EC_REQ_ACTIVATE) {
-        if (t == go) activate();
+        if (t == go) {
+          if (quorum_mode && contributed_round == go) initiator_activate();
+          else activate();
+        }
       } else if (type == EC_REQ_HOLD) {
         hold_from = arg;
       } else if (type == EC_REQ_GUARD) {
@@ -883,12 +899,13 @@ __device__ void engine_controller(const EcDesc& d, unsigned long long epoch) {
       if (next_req - rep_from >= 16) flush_replies();
       progress = true;
     }
-    // ---- all-arrive barrier (bench): everyone boarded -> activate
+    // ---- arrival barrier: `arrive_pending` ranks boarded (all of them in
+    // all-arrive replay mode, the quorum in majority-quorum mode) -> activate
     if (open_ok && arrive_pending) {
-      bool all = true;
-      for (int q = 0; q < P && all; ++q)
-        all = ld_acquire_sys(&C->arrive_from[q]) >= (unsigned long long)go + 1;
-      if (all) {
+      int n_arr = 0;
+      for (int q = 0; q < P; ++q)
+        n_arr += ld_acquire_sys(&C->arrive_from[q]) >= (unsigned long long)go + 1;
+      if (n_arr >= arrive_pending) {
         arrive_pending = 0;
         if (arrive_activate) activate();
         progress = true;

@@ -75,6 +75,15 @@ def _round(h, t, all_arrive=True):
     return gen.value
 
 
+def _round_flags(h, t0, k, all_arrive):
+    """Offer flags of rounds t0..t0+k-1, computed before a timed issue loop:
+    the majority initiator (numpy Philox, collectives.py:78-88) costs tens of
+    microseconds of host time per round, more than a small round itself."""
+    from . import _lib
+    return [_lib.EC_CF_FRESH | (_lib.EC_CF_ALL_ARRIVE if all_arrive else 0) |
+            (_lib.EC_CF_ACTIVATE if h._may_activate(t) else 0) for t in range(t0, t0 + k)]
+
+
 def rounds_back_to_back(h, t0, k, all_arrive=True):
     """k rounds t0..t0+k-1 enqueued on the current stream, each behind a
     device-side wait for the previous one (ec_round_async); returns device ms
@@ -84,14 +93,13 @@ def rounds_back_to_back(h, t0, k, all_arrive=True):
     from . import _lib
     from ._lib import call
     h._ensure_started()
+    flags = _round_flags(h, t0, k, all_arrive)
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     seqs = []
     e0.record()
     for t in range(t0, t0 + k):
-        flags = _lib.EC_CF_FRESH | (_lib.EC_CF_ALL_ARRIVE if all_arrive else 0) | \
-            (_lib.EC_CF_ACTIVATE if h._may_activate(t) else 0)
         seq = C.c_uint64()
-        call("ec_round_async", h.comm.ptr, h.li, t, flags, h._stream(), C.byref(seq))
+        call("ec_round_async", h.comm.ptr, h.li, t, flags[t - t0], h._stream(), C.byref(seq))
         seqs.append(seq.value)
     e1.record()
     e1.synchronize()
@@ -112,15 +120,14 @@ def rounds_pipelined(h, t0, k, all_arrive=True):
     from . import _lib
     from ._lib import call
     h._ensure_started()
+    flags = _round_flags(h, t0, k, all_arrive)
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     seqs = []
     e0.record()
     for t in range(t0, t0 + k):
-        flags = _lib.EC_CF_FRESH | (_lib.EC_CF_ALL_ARRIVE if all_arrive else 0) | \
-            (_lib.EC_CF_ACTIVATE if h._may_activate(t) else 0)
         seq = C.c_uint64()
         fn = "ec_round_async" if t == t0 + k - 1 else "ec_post_contribute"
-        call(fn, h.comm.ptr, h.li, t, flags, h._stream(), C.byref(seq))
+        call(fn, h.comm.ptr, h.li, t, flags[t - t0], h._stream(), C.byref(seq))
         seqs.append(seq.value)
     e1.record()
     e1.synchronize()

@@ -69,6 +69,8 @@ class Comm:
             call("ec_comm_create", cfg.p, rank_lo, n_local, self.device, cfg.vector_len,
                  self.dtype_code, FLAVOR_CODE[cfg.flavor], self.ring_slots, world.workers,
                  C.byref(self.ptr))
+        if getattr(cfg, "majority_quorum", False):
+            call("ec_comm_set_quorum", self.ptr, (cfg.p + 1) // 2)
         self.running = False
         self.closed = False
         self.nvls = False

@@ -972,3 +972,25 @@ def test_idle_park_lets_device_syncs_return():
         assert st[r].w.cpu().numpy().tobytes() == w.tobytes()
     print(f"device sync returned after {waited * 1e3:.0f} ms (idle park)")
     world.close()
+
+
+@pytest.mark.parametrize("seed", [31, 32, 33, 34])
+def test_majority_quorum_waits_for_half_the_ranks(seed):
+    """Opt-in majority_quorum (the north_star's "a randomly chosen initiator
+    once at least half the ranks have arrived"): under skew r * 2 ms the mask
+    is the arrival prefix up to max(initiator, ceil(P/2) - 1)."""
+    p, n = 4, 16
+    cfg = CollectiveConfig(p=p, flavor="majority", vector_len=n, element="f8", seed=seed,
+                           majority_quorum=True)
+    delays = np.array([[2000 * r] for r in range(p)])
+    want = int(R.bench_masks("majority", delays, seed, quorum=(p + 1) // 2)[0])
+    res, handles, world = run_allreduce(cfg, lambda r, t: np.full(n, 10.0 * r + t),
+                                        delay_us=lambda r, t: 2000 * r)
+    try:
+        for r in range(p):
+            assert res[(r, 0)].included == want, (seed, r, res[(r, 0)].included, want)
+        vecs = [np.full(n, 10.0 * r) if (want >> r) & 1 else None for r in range(p)]
+        u, _, _ = R.allreduce_round(vecs, [v is not None for v in vecs])
+        assert _np(res[(0, 0)].u).tobytes() == u.tobytes()
+    finally:
+        world.close()
