@@ -159,3 +159,22 @@ def test_bench_schedules_match_the_restated_activation_rules(golden_dir):
         if flavor == "majority":
             inits = z[f"{name}/initiator"]
             assert all((int(masks[t]) >> int(inits[t])) & 1 for t in range(rounds))
+
+
+def test_majority_quorum_oracle_and_config():
+    """The opt-in quorum rule (north_star: the initiator activates "once at
+    least half the ranks have arrived"): under linear skew the fresh set is the
+    arrival prefix up to max(initiator, ceil(P/2) - 1); the default is the
+    reference's rule (no counting)."""
+    from paper_1908_04207_b200.collectives import CollectiveConfig
+    p = 8
+    delays = R.bench_delays(R.DelayModel("linear_skew", 1.0), p, 64)
+    plain = R.bench_masks("majority", delays, 1234)
+    quor = R.bench_masks("majority", delays, 1234, quorum=(p + 1) // 2)
+    for t in range(64):
+        init = R.initiator_for_round(1234, t, p)
+        assert int(plain[t]) == (1 << (init + 1)) - 1
+        assert int(quor[t]) == (1 << (max(init, 3) + 1)) - 1
+    assert CollectiveConfig(p=4, flavor="majority", vector_len=2).majority_quorum is False
+    with pytest.raises(ValueError):
+        CollectiveConfig(p=4, flavor="solo", vector_len=2, majority_quorum=True)
