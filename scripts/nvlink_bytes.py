@@ -21,18 +21,55 @@ import torch  # noqa: E402
 import torch.distributed as dist  # noqa: E402
 
 
+def _nvml_counters(dev: int):
+    """(tx, rx) bytes summed over the GPU's NVLinks from NVML field values
+    (NVLINK_COUNT_XMIT/RCV_BYTES per link, else THROUGHPUT_DATA_TX/RX in KiB)."""
+    import pynvml as N
+    N.nvmlInit()
+    h = N.nvmlDeviceGetHandleByIndex(dev)
+    for tx_id, rx_id, scale in ((N.NVML_FI_DEV_NVLINK_COUNT_XMIT_BYTES,
+                                 N.NVML_FI_DEV_NVLINK_COUNT_RCV_BYTES, 1),
+                                (N.NVML_FI_DEV_NVLINK_THROUGHPUT_DATA_TX,
+                                 N.NVML_FI_DEV_NVLINK_THROUGHPUT_DATA_RX, 1024)):
+        tx = rx = 0
+        ok = False
+        for link in range(18):
+            try:
+                vals = N.nvmlDeviceGetFieldValues(h, [(tx_id, link), (rx_id, link)])
+            except Exception:
+                continue
+            for v, which in zip(vals, ("tx", "rx")):
+                if v.nvmlReturn != 0:
+                    continue
+                ok = True
+                x = v.value.ullVal * scale
+                if which == "tx":
+                    tx += x
+                else:
+                    rx += x
+        if ok and (tx or rx):
+            return (tx, rx), ""
+    return None, "NVML NVLink byte counters unsupported"
+
+
 def counters(dev: int):
-    """(tx, rx) KiB summed over the GPU's links, or None if unsupported."""
+    """(tx, rx) bytes summed over the GPU's links, or None if unsupported."""
+    try:
+        c, err = _nvml_counters(dev)
+        if c:
+            return c, ""
+    except Exception as e:  # noqa: BLE001
+        err = str(e)
     try:
         out = subprocess.run(["nvidia-smi", "nvlink", "-gt", "d", "-i", str(dev)],
                              capture_output=True, text=True, timeout=30).stdout
     except Exception:
-        return None, ""
+        return None, err
     tx = sum(int(x) for x in re.findall(r"Tx:\s*(\d+)\s*KiB", out))
     rx = sum(int(x) for x in re.findall(r"Rx:\s*(\d+)\s*KiB", out))
     if not tx and not rx:
-        return None, out[-500:]
-    return (tx, rx), ""
+        return None, err + " | nvidia-smi: " + out[-200:]
+    return (tx * 1024, rx * 1024), ""
 
 
 def main():
@@ -61,8 +98,8 @@ def main():
     c1, _ = counters(local)
     res = {"rank": rank, "ms": ms}
     if c0 and c1:
-        res["tx_bytes_per_round"] = (c1[0] - c0[0]) * 1024 / args.rounds
-        res["rx_bytes_per_round"] = (c1[1] - c0[1]) * 1024 / args.rounds
+        res["tx_bytes_per_round"] = (c1[0] - c0[0]) / args.rounds
+        res["rx_bytes_per_round"] = (c1[1] - c0[1]) / args.rounds
     else:
         res["error"] = err or "no counters"
     allr = [None] * world

@@ -129,3 +129,91 @@ def test_gloo_world_size_2_handle_exchange():
     for pr in procs:
         pr.join(60)
     assert res == [(0, [0, 1], True), (1, [0, 1], True)]
+
+
+def _process_world_worker(rank, world, port, q):
+    """ProcessWorld's real host logic over gloo, with the device layer faked
+    (no GPU here): attach exchanges every rank's export blob through the
+    process group and imports each peer's under its own rank, a second
+    communicator gets its own exchange, and release/close are collective."""
+    import struct
+
+    import torch.distributed as dist
+
+    import paper_1908_04207_b200.world as W
+    from paper_1908_04207_b200.collectives import CollectiveConfig
+
+    calls = []
+
+    class FakeComm:
+        def __init__(self, world_, cfg, rank_lo, n_local):
+            self.cfg, self.rank_lo, self.n_local = cfg, rank_lo, n_local
+            self.running, self.closed, self.nvls = False, False, False
+            self.imports = {}
+
+        def export(self, li):
+            # the C blob's header fields (BlobV1: magic, rank, n, dtype, R)
+            return struct.pack("<Iiqii", 0x45434231, self.rank_lo + li, self.cfg.vector_len, 0, 3)
+
+        def import_peer(self, r, blob):
+            magic, br, n, _dt, _ring = struct.unpack("<Iiqii", blob[:24])
+            assert magic == 0x45434231 and br == r and n == self.cfg.vector_len
+            self.imports[r] = br
+            calls.append(("import", self.cfg.vector_len, r))
+
+        def start(self):
+            self.running = True
+
+        def pause(self, timeout_ms=30000):
+            calls.append(("pause", self.cfg.vector_len))
+            self.running = False
+
+        def close(self):
+            calls.append(("close", self.cfg.vector_len))
+            self.closed = True
+
+    W.Comm = FakeComm
+    W.warm_device_libraries = lambda device: None
+    dist.init_process_group("gloo", init_method=f"tcp://127.0.0.1:{port}", rank=rank,
+                            world_size=world)
+    try:
+        pw = W.ProcessWorld(device=0)
+        c1, li = pw.attach(CollectiveConfig(p=world, flavor="solo", vector_len=7, element="f4"),
+                           0, rank)
+        c2, _ = pw.attach(CollectiveConfig(p=world, flavor="sync", vector_len=9, element="f4"),
+                          1, rank)
+        errs = []
+        for bad in (lambda: pw.attach(CollectiveConfig(p=world + 1, flavor="solo", vector_len=7),
+                                      2, rank),
+                    lambda: pw.attach(CollectiveConfig(p=world, flavor="solo", vector_len=7),
+                                      0, rank),
+                    lambda: pw.attach(CollectiveConfig(p=world, flavor="solo", vector_len=7),
+                                      3, (rank + 1) % world)):
+            try:
+                bad()
+            except ValueError:
+                errs.append(True)
+        pw.release(1)
+        pw.close()
+        q.put((rank, li, sorted(c1.imports.items()), sorted(c2.imports.items()), len(errs),
+               calls.count(("close", 9)), calls.count(("close", 7)), 1 in pw.comms))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_gloo_world_size_2_process_world_exchange():
+    import multiprocessing as mp
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_process_world_worker, args=(r, 2, port, q)) for r in range(2)]
+    for pr in procs:
+        pr.start()
+    res = sorted(q.get(timeout=180) for _ in procs)
+    for pr in procs:
+        pr.join(60)
+    for rank, li, imp1, imp2, nerr, closed9, closed7, still in res:
+        assert li == 0
+        assert imp1 == [(0, 0), (1, 1)] and imp2 == [(0, 0), (1, 1)]
+        assert nerr == 3                      # wrong p, duplicate cid, foreign rank
+        assert closed9 == 1 and closed7 == 1 and not still
