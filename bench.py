@@ -99,7 +99,7 @@ def _ncu(kernel: str):
         with open(os.path.join(ROOT, "profiles", "ncu_summary.json")) as f:
             k = json.load(f)["kernels"][kernel]
         return {"duration_us": k["duration_us"], "gbs": k["algorithmic_gbs"],
-                "frac": k["frac_of_measured_6512"]}
+                "frac": k.get("frac_of_measured_peak")}
     except Exception:
         return None
 
