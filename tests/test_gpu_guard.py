@@ -102,3 +102,100 @@ def test_without_guard_the_tau_contract_breaks():
     ledger, _ = _run(tau=None, lag=0, rounds=rounds, p=p, unit_ms=1.0)
     assert not [v for v in ledger.audit() if v[0] not in ("undelivered", "staleness")]
     assert ledger.audit(tau=1, allow_pending_after=rounds - 2)
+
+
+@pytest.mark.parametrize("flavor,p,n", [("solo", 3, 200_003), ("majority", 3, 200_003),
+                                        ("solo", 5, 9_001)])
+def test_live_async_steps_under_random_skew_match_the_restatement(flavor, p, n):
+    """Protocol stress in place of a race checker (compute-sanitizer is closed
+    on this pool): P ranks issue async steps (lag 2, guard tau=2) with random
+    device-side delays, so offers race snapshots, refused offers fold into the
+    stash and zero-copy late offers are preserved.  Afterwards everything the
+    device decided is taken as the schedule -- the masks it logged, the
+    generation each step applied -- and the restatement recomputes every
+    stash, every u and every rank's weights from it: bit-exact, ledger clean."""
+    import ctypes as C
+
+    from paper_1908_04207_b200._lib import call
+    rounds, lr, tau = 40, 0.05, 2
+    rng = np.random.default_rng(p * 100 + n % 97)
+    spins = rng.integers(0, 400, size=(p, rounds))
+    grads = rng.standard_normal((p, rounds, n)).astype(np.float32)
+    w0 = rng.standard_normal(n).astype(np.float32)
+    world = EmulatedWorld(p)
+    cfg = CollectiveConfig(p=p, flavor=flavor, vector_len=n, element="f4", seed=3)
+    hs = [AllreduceHandle(cfg, r, world) for r in range(p)]
+    states = [TrainState.fresh(w0, lr, rank=r, tau=tau) for r in range(p)]
+    ledger = DeliveryLedger()
+    streams = [torch.cuda.Stream() for _ in range(p)]
+    torch.cuda.synchronize()
+    for r in range(p):
+        staleness_guard(hs[r], states[r])
+        attach_delivery_tracking(hs[r], states[r], ledger)
+    obs = np.zeros((p, rounds), np.int64)
+    errors: list = []
+    go = threading.Barrier(p)
+
+    def body(r):
+        try:
+            torch.cuda.set_device(0)
+            h, st = hs[r], states[r]
+            gd = torch.as_tensor(grads[r], device="cuda")
+            pend = []
+            with torch.cuda.stream(streams[r]):
+                go.wait()
+                for t in range(rounds):
+                    device_delay(int(spins[r, t]))
+                    if t % 3:
+                        h.grad_buffer().copy_(gd[t])
+                        g = h.grad_buffer()
+                    else:
+                        g = gd[t]
+                    ledger.generated(r, t)
+                    pend.append(train_step_async(st, h, g))
+                    while len(pend) > 2:
+                        pt = pend[0].t
+                        obs[r, pt] = finish_step(st, h, pend.pop(0))[2]
+                while pend:
+                    pt = pend[0].t
+                    obs[r, pt] = finish_step(st, h, pend.pop(0))[2]
+                streams[r].synchronize()
+        except BaseException as e:  # surfaced below
+            errors.append(e)
+
+    th = [threading.Thread(target=body, args=(r,), daemon=True) for r in range(p)]
+    for x in th:
+        x.start()
+    for x in th:
+        x.join()
+    assert not errors, errors[0]
+    world.synchronize()
+    last = int(obs.max())
+    masks = []
+    for g in range(last + 1):
+        m, hm, nap = C.c_uint64(), C.c_uint64(), C.c_int()
+        call("ec_gen_info", hs[0].comm.ptr, 0, g, C.byref(m), C.byref(hm), C.byref(nap))
+        for r in range(1, p):            # Lemma 1: the same mask at every rank
+            m2, hm2, nap2 = C.c_uint64(), C.c_uint64(), C.c_int()
+            call("ec_gen_info", hs[r].comm.ptr, r, g, C.byref(m2), C.byref(hm2), C.byref(nap2))
+            assert (m2.value, hm2.value) == (m.value, hm.value), (g, r)
+        assert nap.value == bin(m.value).count("1") >= 1
+        masks.append(m.value)
+    ws = [st.w.cpu().numpy() for st in states]
+    world.close()
+    # the device's schedule, restated: an offer of step t boarded round t iff
+    # bit r of mask[t] (a fresh snapshot of t consumes the stash)
+    acc = np.array([[(masks[t] >> r) & 1 if t <= last else 0 for t in range(rounds)]
+                    for r in range(p)], bool)
+    contribs, led = R.replay_stashes(grads, acc, np.float32)
+    u = [R.allreduce_round(contribs[t], [c is not None for c in contribs[t]], np.float32, n)[0]
+         for t in range(last + 1)]
+    for r in range(p):
+        w = w0.copy()
+        for t in range(rounds):
+            assert obs[r, t] >= t
+            w = R.sgd_update(w, u[int(obs[r, t])], lr)
+        assert ws[r].tobytes() == w.tobytes(), (flavor, r)
+    assert {k: v for k, v in led.items() if v is not None} == \
+        {k: v for k, v in ledger.as_dict().items() if v is not None}
+    assert not ledger.audit(tau=tau, allow_pending_after=rounds - 1 - tau)
