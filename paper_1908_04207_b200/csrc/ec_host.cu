@@ -26,7 +26,7 @@
 cudaError_t launch_engine(int dtype, const EcDesc* d_descs, int n_local, int blocks_per_rank,
                           unsigned long long epoch, int smem_bytes, cudaStream_t s);
 cudaError_t launch_fold(int dtype, void* stash, const void* grad, long long n, int mode,
-                        unsigned int* nonfinite, cudaStream_t s);
+                        unsigned int* nonfinite, cudaStream_t s, int gated);
 cudaError_t launch_update(int dtype, void* w, const void* u, double lr, long long n, cudaStream_t s);
 cudaError_t launch_momentum(int dtype, void* w, void* buf, const void* u, double lr, double mu,
                             long long n, cudaStream_t s);
@@ -1040,7 +1040,10 @@ int ec_fold(ec_comm_t* c, int li, const void* grad, int mode, void* stream) {
   if (rc) return rc;
   if (!grad) return fail(EC_E_ARG, "null gradient");
   EcRankHost* r = c->L[li];
-  CK(launch_fold(c->dtype, r->send, grad, c->n, mode, &r->local->poison, (cudaStream_t)stream));
+  // into a pending stash: check first, so a non-finite gradient is refused
+  // (EC_R_POISONED at the post) without touching the gradients it holds
+  CK(launch_fold(c->dtype, r->send, grad, c->n, mode, &r->local->poison, (cudaStream_t)stream,
+                 mode == EC_FOLD_ADD));
   return EC_OK;
 }
 
@@ -1502,7 +1505,7 @@ int ec_fold_raw(void* stash, const void* grad, int64_t n, int dtype, int mode, u
   if (!stash || !grad || n < 0) return fail(EC_E_ARG, "bad fold arguments");
   if (dtype < EC_F32 || dtype > EC_I64) return fail(EC_E_ARG, "bad dtype");
   if (n == 0) return EC_OK;
-  CK(launch_fold(dtype, stash, grad, n, mode, nonfinite, (cudaStream_t)stream));
+  CK(launch_fold(dtype, stash, grad, n, mode, nonfinite, (cudaStream_t)stream, 0));
   return EC_OK;
 }
 

@@ -1301,10 +1301,14 @@ __device__ void direct_publish(const EcDesc& d, long long g, int contrib, unsign
 // ---------------------------------------------------------------------------
 // standalone streaming kernels
 
+// gate != nullptr: a preceding ec_finite_kernel's verdict; a non-finite
+// gradient leaves the stash untouched (folding into a PENDING stash must not
+// poison the gradients it already holds, eagersgd.py:145-147)
 template <typename T, int MODE>
 __global__ void __launch_bounds__(256, 6)
 ec_fold_kernel(T* __restrict__ stash, const T* __restrict__ grad, long long n,
-               unsigned int* nonfinite, int vec_ok) {
+               unsigned int* nonfinite, int vec_ok, const unsigned int* gate) {
+  if (gate && *(volatile const unsigned int*)gate) return;
   constexpr int V = Ops<T>::V;
   constexpr int U = 4;
   bool bad = false;
@@ -1345,6 +1349,29 @@ ec_fold_kernel(T* __restrict__ stash, const T* __restrict__ grad, long long n,
     stash[e] = MODE == 1 ? Ops<T>::add(stash[e], gv) : Ops<T>::canon(gv);
   }
   if (nonfinite && __any_sync(0xffffffffu, bad) && (threadIdx.x & 31) == 0) atomicOr(nonfinite, 1u);
+}
+
+// flag |= any(!isfinite(grad)) -- the check pass ahead of a gated ADD fold
+template <typename T>
+__global__ void __launch_bounds__(256, 6)
+ec_finite_kernel(const T* __restrict__ grad, long long n, unsigned int* flag, int vec_ok) {
+  constexpr int V = Ops<T>::V;
+  const long long tid = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  const long long nth = (long long)gridDim.x * blockDim.x;
+  bool bad = false;
+  long long done = 0;
+  if (vec_ok) {
+    const long long nv = n / V;
+    for (long long v = tid; v < nv; v += nth) {
+      Vec16<T> g;
+      g.raw = ld_stream_v4(grad + v * V);
+#pragma unroll
+      for (int l = 0; l < V; ++l) bad |= !Ops<T>::finite(g.e[l]);
+    }
+    done = nv * V;
+  }
+  for (long long e = done + tid; e < n; e += nth) bad |= !Ops<T>::finite(grad[e]);
+  if (__any_sync(0xffffffffu, bad) && (threadIdx.x & 31) == 0) atomicOr(flag, 1u);
 }
 
 template <typename T>
@@ -2179,6 +2206,7 @@ cudaError_t preload_kernels() {
       (const void*)ec_fold_kernel<double, 0>, (const void*)ec_fold_kernel<double, 1>,
       (const void*)ec_fold_kernel<long long, 0>, (const void*)ec_fold_kernel<long long, 1>,
       (const void*)ec_update_kernel<float>, (const void*)ec_update_kernel<double>,
+      (const void*)ec_finite_kernel<float>, (const void*)ec_finite_kernel<double>,
       (const void*)ec_momentum_kernel<float>, (const void*)ec_momentum_kernel<double>,
       (const void*)ec_reduce_kernel<float>, (const void*)ec_reduce_kernel<double>,
       (const void*)ec_reduce_kernel<long long>,
@@ -2230,21 +2258,32 @@ cudaError_t launch_engine(int dtype, const EcDesc* d_descs, int n_local, int blo
   return cudaLaunchCooperativeKernel(fn, grid, block, args, smem_bytes, s);
 }
 
+// gated != 0 (ADD into a pending stash, float types, a poison flag given):
+// a check pass first, and the fold writes nothing if it found a non-finite value
 cudaError_t launch_fold(int dtype, void* stash, const void* grad, long long n, int mode,
-                        unsigned int* nonfinite, cudaStream_t s) {
+                        unsigned int* nonfinite, cudaStream_t s, int gated) {
   counted();
   const int vec_ok = ((((uintptr_t)stash) | ((uintptr_t)grad)) & 15) == 0;
   const int V = dtype == 0 ? 4 : 2;
   const int grid = grid_for((n / V + 3) / 4 + 1, 256);
+  const unsigned int* gate = nullptr;
+  if (gated && mode && nonfinite && dtype != 2) {
+    counted();
+    const int vg = (((uintptr_t)grad) & 15) == 0;
+    const int cg = grid_for(n / V + 1, 256);
+    if (dtype == 0) ec_finite_kernel<float><<<cg, 256, 0, s>>>((const float*)grad, n, nonfinite, vg);
+    else ec_finite_kernel<double><<<cg, 256, 0, s>>>((const double*)grad, n, nonfinite, vg);
+    gate = nonfinite;
+  }
   if (dtype == 0) {
-    if (mode) ec_fold_kernel<float, 1><<<grid, 256, 0, s>>>((float*)stash, (const float*)grad, n, nonfinite, vec_ok);
-    else ec_fold_kernel<float, 0><<<grid, 256, 0, s>>>((float*)stash, (const float*)grad, n, nonfinite, vec_ok);
+    if (mode) ec_fold_kernel<float, 1><<<grid, 256, 0, s>>>((float*)stash, (const float*)grad, n, nonfinite, vec_ok, gate);
+    else ec_fold_kernel<float, 0><<<grid, 256, 0, s>>>((float*)stash, (const float*)grad, n, nonfinite, vec_ok, gate);
   } else if (dtype == 1) {
-    if (mode) ec_fold_kernel<double, 1><<<grid, 256, 0, s>>>((double*)stash, (const double*)grad, n, nonfinite, vec_ok);
-    else ec_fold_kernel<double, 0><<<grid, 256, 0, s>>>((double*)stash, (const double*)grad, n, nonfinite, vec_ok);
+    if (mode) ec_fold_kernel<double, 1><<<grid, 256, 0, s>>>((double*)stash, (const double*)grad, n, nonfinite, vec_ok, gate);
+    else ec_fold_kernel<double, 0><<<grid, 256, 0, s>>>((double*)stash, (const double*)grad, n, nonfinite, vec_ok, gate);
   } else {
-    if (mode) ec_fold_kernel<long long, 1><<<grid, 256, 0, s>>>((long long*)stash, (const long long*)grad, n, nonfinite, vec_ok);
-    else ec_fold_kernel<long long, 0><<<grid, 256, 0, s>>>((long long*)stash, (const long long*)grad, n, nonfinite, vec_ok);
+    if (mode) ec_fold_kernel<long long, 1><<<grid, 256, 0, s>>>((long long*)stash, (const long long*)grad, n, nonfinite, vec_ok, gate);
+    else ec_fold_kernel<long long, 0><<<grid, 256, 0, s>>>((long long*)stash, (const long long*)grad, n, nonfinite, vec_ok, gate);
   }
   return cudaGetLastError();
 }

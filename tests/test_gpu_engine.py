@@ -994,3 +994,25 @@ def test_majority_quorum_waits_for_half_the_ranks(seed):
         assert _np(res[(0, 0)].u).tobytes() == u.tobytes()
     finally:
         world.close()
+
+
+def test_nonfinite_gradient_leaves_a_pending_stash_intact():
+    """eagersgd.py:145-147 (advisor r1): a non-finite gradient is refused with
+    DivergenceError before it can poison a stash that still holds an earlier
+    round's gradient -- the fold into a pending stash checks first and writes
+    nothing; the pending rounds are unchanged and training can go on."""
+    from paper_1908_04207_b200 import DivergenceError
+    world = EmulatedWorld(2)
+    cfg = CollectiveConfig(p=2, flavor="solo", vector_len=5, element="f4")
+    hs = [AllreduceHandle(cfg, r, world) for r in range(2)]
+    st = [TrainState.fresh(np.zeros(5, np.float32), 1.0, rank=r, tau=None) for r in range(2)]
+    g0 = torch.tensor([1.0, 2.0, 3.0, 4.0, 5.0], device="cuda")
+    drive(train_step(st[0], None, hs[0], grad=g0))               # round 0: rank 0 alone
+    drive(train_step(st[1], None, hs[1], grad=g0 * 10))          # late: refused, pending
+    assert st[1].send_buf.pending_rounds == [0]
+    bad = torch.tensor([1.0, float("nan"), 0.0, 0.0, 0.0], device="cuda")
+    with pytest.raises(DivergenceError):
+        drive(train_step(st[1], None, hs[1], grad=bad))
+    assert st[1].send_buf.pending_rounds == [0]
+    assert _np(hs[1].send_buffer()).tolist() == [10.0, 20.0, 30.0, 40.0, 50.0]
+    world.close()

@@ -105,7 +105,7 @@ def test_lstm_config4_eager_sgd_steps():
                                                train_step_async(states[r], hs[r],
                                                                 hs[r].grad_buffer(),
                                                                 loss=loss, all_arrive=True))
-                    losses[(r, t)] = float(lo)
+                    losses[(r, t)] = float(lo.detach())
                     naps[(r, t)] = res.nap
                     if t == 0:
                         w_first[r] = states[r].w.clone()
