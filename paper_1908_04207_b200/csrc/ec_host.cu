@@ -728,8 +728,9 @@ static int upload_descs(ec_comm_t* c) {
     x.dtype = c->dtype;
     x.R = c->R;
     x.W = c->W;
-    x.sig_every = getenv("EC_SIGNAL_EVERY") ? atoi(getenv("EC_SIGNAL_EVERY")) : 0;  // 0: adaptive
-    if (x.sig_every < 0) x.sig_every = 0;
+    // 0: ~4 words per worker per round; < 0: geometric (1/2, 3/4, 7/8, ...)
+    x.sig_every = getenv("EC_SIGNAL_EVERY") ? atoi(getenv("EC_SIGNAL_EVERY")) : 0;
+    if (x.sig_every < 0) x.sig_every = -1;
     x.replay = r->forced != nullptr;
     x.vec = V;
     x.n = c->n;

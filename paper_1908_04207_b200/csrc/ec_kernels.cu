@@ -293,6 +293,16 @@ __device__ void round_tma(const EcDesc& d, const char* const* sp, int w, long lo
   // final word, 260.9 with one per 8 chunks, 266.2 per 4); fewer words leave
   // more of the update after the round (done->offer 46 us with one)
   const long long sig = d.sig_every > 0 ? d.sig_every : (mine + 3) / 4 > 1 ? (mine + 3) / 4 : 1;
+  // sig_every < 0 (EC_SIGNAL_EVERY=-1): a geometric schedule instead -- words
+  // after 1/2, 3/4, 7/8, ... of the worker's chunks, so what the update has
+  // left once the round is over shrinks to about the last chunk
+  const bool geo = d.sig_every < 0;
+  auto signal_at = [&](long long done_chunks) -> bool {   // chunks < done_chunks landed
+    if (!geo) return ((done_chunks) % sig) == 0;
+    for (int j = 1; j <= 5; ++j)
+      if (done_chunks == mine - (mine >> j) && (mine >> j) > 0) return true;
+    return false;
+  };
   auto issue = [&](long long k) {  // thread 0: loads of my k-th chunk
     const int s = (int)((it + k) % S);
     const long long c = c0 + w + k * d.W;
@@ -331,7 +341,7 @@ __device__ void round_tma(const EcDesc& d, const char* const* sp, int w, long lo
       }
       tma_commit();
       if (k + S < mine) issue(k + S);
-      if (updm && k >= 2 && ((k - 1) % sig) == 0) {
+      if (updm && k >= 2 && signal_at(k - 1)) {
         // all but the 2 newest store groups have fully landed: chunks < k - 1
         // (one signal per sig_every chunks: each costs a sys fence)
         asm volatile("cp.async.bulk.wait_group 2;" ::: "memory");
