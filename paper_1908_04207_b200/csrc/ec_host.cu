@@ -555,8 +555,11 @@ int ec_comm_create(int world_size, int rank_lo, int n_local, int device, int64_t
     // the whole vector into its own slot): no push / remote completion on the
     // round's critical path
     if (c->mode == 0 && world_size > 1) {
+      // measured (profiles/r2_p2_oneshot.json, r2_sweep4_lead2.json): at P=2
+      // one-shot wins up to ~1 MB (14.4 vs 16.4 us at 256 KB), at P=4 up to
+      // 64 KB; beyond, the two-shot's split work (and progressive updates) win
       const char* e = getenv("EC_ONESHOT_BYTES");
-      const long long lim = e ? atoll(e) : 65536;
+      const long long lim = e ? atoll(e) : (world_size == 2 ? (1ll << 20) : 65536);
       if (n_elems * c->elem <= lim) c->mode = 3;
     }
     c->smem_bytes = (c->mode == 0 || c->mode == 3) ? st * (world_size + 1) * chb : 0;
