@@ -601,7 +601,14 @@ def bench_allreduce(args, pw, rank, world, dev, barrier, max_over_ranks, quiesce
         # each next offer the moment the previous round completes), and -- for
         # comparison -- each behind a device-side wait for the previous one
         from paper_1908_04207_b200.harness import rounds_pipelined
+        rx0, tx0 = C.c_uint64(), C.c_uint64()
+        _lib.lib.ec_comm_traffic(h.comm.ptr, h.li, C.byref(rx0), C.byref(tx0))
         ms = max_over_ranks(rounds_pipelined(h, 3, rounds)) / rounds
+        rx1, tx1 = C.c_uint64(), C.c_uint64()
+        _lib.lib.ec_comm_traffic(h.comm.ptr, h.li, C.byref(rx1), C.byref(tx1))
+        # the NVLink bytes this rank's workers issued per round (pulls + pushes),
+        # to compare with the algorithmic bus bytes 2(P-1)/P * S
+        issued = max_over_ranks(((rx1.value - rx0.value) + (tx1.value - tx0.value)) / rounds)
         busbw = 2 * (world - 1) / world * 4 * n / (ms / 1e3) / 1e9
         barrier()
         ms_ser = max_over_ranks(rounds_back_to_back(h, 3 + rounds, rounds)) / rounds
@@ -621,7 +628,9 @@ def bench_allreduce(args, pw, rank, world, dev, barrier, max_over_ranks, quiesce
                                       / (ms_ser / 1e3) / 1e9},
                        "blocking_api": {"us_per_round": ms_sync * 1e3,
                                         "busbw_gbs": busbw * ms / ms_sync},
-                       "workers": h.comm.world.workers or "auto"}
+                       "workers": h.comm.world.workers or "auto",
+                       "issued_nvlink_bytes_per_round": issued,
+                       "bus_bytes_per_round": 2 * (world - 1) / world * 4 * n}
         h.close()
     pw.workers = saved_workers
     return {"allreduce": out}

@@ -115,6 +115,12 @@ int ec_comm_pause(ec_comm_t* c, int timeout_ms);
  * thread relaunches it when a peer activates, snapshots or boards the next
  * generation.  Counters of parks / wakes and whether it is parked now. */
 int ec_comm_idle_stats(ec_comm_t* c, uint64_t* parks, uint64_t* wakes, int* parked);
+/* Bytes local rank `local_idx`'s workers have pulled from (rx) and pushed to
+ * (tx) OTHER ranks' memory since creation, in the fused TMA data phases: the
+ * NVLink traffic the engine issues (no reference counterpart; the hardware's
+ * NVLink byte counters are not exposed on every platform).  Two-shot rounds
+ * issue (P-1)/P * S each way per rank, 2(P-1)/P * S in all = the bus bytes. */
+int ec_comm_traffic(ec_comm_t* c, int local_idx, uint64_t* rx_bytes, uint64_t* tx_bytes);
 int ec_comm_destroy(ec_comm_t* c);
 /* Device error word (watchdog timeout, out-of-order round): the reference's
  * TimeoutError / AssertionError (collectives.py:298,331). */

@@ -154,6 +154,8 @@ struct alignas(128) EcLocal {
   // g >= min(pend_lo, last_off + 1) + guard_tau -- the oldest gradient not yet
   // delivered (a pending stash round, or the step in progress after the last
   // offer), eagersgd.py:102-108
+  unsigned long long nv_rx, nv_tx; // bytes this rank's workers pulled from / pushed to other
+                                   // ranks (fused TMA modes; monotone, ec_comm_traffic)
   long long guard_tau;             // EC_INF_GEN: guard off
   long long pend_lo;               // oldest offered round still in the stash (EC_INF_GEN: none)
   long long last_off;              // round of the last offer processed (-1: none yet)

@@ -1583,6 +1583,23 @@ int ec_debug_state(ec_comm_t* c, int li, int64_t* out) {
   return EC_OK;
 }
 
+int ec_comm_traffic(ec_comm_t* c, int li, uint64_t* rx_bytes, uint64_t* tx_bytes) {
+  int rc = check_li(c, li);
+  if (rc) return rc;
+  EcRankHost* r = c->L[li];
+  unsigned long long v[2] = {0, 0};
+  cudaStream_t s;
+  CK(cudaSetDevice(c->device));
+  CK(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
+  cudaError_t e = cudaMemcpyAsync(v, &r->local->nv_rx, sizeof(v), cudaMemcpyDeviceToHost, s);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+  cudaStreamDestroy(s);
+  if (e != cudaSuccess) return fail(EC_E_CUDA, "traffic copy: %s", cudaGetErrorString(e));
+  if (rx_bytes) *rx_bytes = v[0];
+  if (tx_bytes) *tx_bytes = v[1];
+  return EC_OK;
+}
+
 int ec_comm_idle_stats(ec_comm_t* c, uint64_t* parks, uint64_t* wakes, int* parked) {
   if (!c) return fail(EC_E_ARG, "null communicator");
   std::lock_guard<std::recursive_mutex> lk(c->live_mu);

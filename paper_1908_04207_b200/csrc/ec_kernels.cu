@@ -303,6 +303,9 @@ __device__ void round_tma(const EcDesc& d, const char* const* sp, int w, long lo
       if (done_chunks == mine - (mine >> j) && (mine >> j) > 0) return true;
     return false;
   };
+  // bytes this worker moves to / from OTHER ranks (the NVLink traffic it
+  // issues; EcLocal::nv_rx / nv_tx, read by ec_comm_traffic)
+  unsigned long long nv_rx = 0, nv_tx = 0;
   auto issue = [&](long long k) {  // thread 0: loads of my k-th chunk
     const int s = (int)((it + k) % S);
     const long long c = c0 + w + k * d.W;
@@ -311,7 +314,10 @@ __device__ void round_tma(const EcDesc& d, const char* const* sp, int w, long lo
     char* st = smem + s * stage_bytes;
     mbar_expect_tx(&full[s], npop * bytes);
     for (int q = 0; q < P; ++q)
-      if ((has >> q) & 1ull) tma_load(st + (size_t)q * chb, sp[q] + v0 * 16, bytes, &full[s]);
+      if ((has >> q) & 1ull) {
+        tma_load(st + (size_t)q * chb, sp[q] + v0 * 16, bytes, &full[s]);
+        if (q != r) nv_rx += bytes;
+      }
   };
   if (threadIdx.x == 0) {
     fence_proxy_async_global();  // peers' generic writes (acquired via flags) -> async-proxy reads
@@ -339,6 +345,7 @@ __device__ void round_tma(const EcDesc& d, const char* const* sp, int w, long lo
         const int q = (r + j) % P;  // own slot first, then peers round-robin
         tma_store(d.ring[q] + off + v0 * 16, out, (unsigned)nvv * 16);
       }
+      if (!oneshot) nv_tx += (unsigned long long)(P - 1) * nvv * 16;
       tma_commit();
       if (k + S < mine) issue(k + S);
       if (updm && k >= 2 && signal_at(k - 1)) {
@@ -354,6 +361,8 @@ __device__ void round_tma(const EcDesc& d, const char* const* sp, int w, long lo
     tma_wait_all();
     fence_proxy_async_global();
     if (updm) signal_chunks(d, w, g, updm, mine);
+    if (nv_rx) atomicAdd(&d.local->nv_rx, nv_rx);
+    if (nv_tx) atomicAdd(&d.local->nv_tx, nv_tx);
   }
 }
 
@@ -372,11 +381,15 @@ __device__ void tail_push(const EcDesc& d, const char* const* sp, unsigned long 
   };
   const T u = Ops<T>::divp(tree_sum_dyn<T>(d.P, leaf), d.P, inv, pow2);
   const long long off = (g % d.R) * d.slot_bytes;
+  unsigned long long rx = 0;
+  for (int q = 0; q < d.P; ++q) rx += (q != d.rank && ((has >> q) & 1ull)) ? sizeof(T) : 0;
+  atomicAdd(&d.local->nv_rx, rx);
   if (oneshot) {
     reinterpret_cast<volatile T*>(d.ring[d.rank] + off)[e] = u;
     return;
   }
   for (int q = 0; q < d.P; ++q) reinterpret_cast<volatile T*>(d.ring[q] + off)[e] = u;
+  atomicAdd(&d.local->nv_tx, (unsigned long long)(d.P - 1) * sizeof(T));
 }
 
 // Two-phase pull data path (ld.global.cg): reduce-scatter, then all-gather.

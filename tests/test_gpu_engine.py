@@ -1016,3 +1016,62 @@ def test_nonfinite_gradient_leaves_a_pending_stash_intact():
     assert st[1].send_buf.pending_rounds == [0]
     assert _np(hs[1].send_buffer()).tolist() == [10.0, 20.0, 30.0, 40.0, 50.0]
     world.close()
+
+
+@pytest.mark.parametrize("p,n", [(4, 1_000_003), (3, 77_777), (2, 2_000_001)])
+def test_issued_nvlink_bytes_equal_the_bus_bytes(p, n):
+    """The engine's own count of bytes it moves to/from other ranks
+    (ec_comm_traffic): an all-arrive two-shot round issues exactly
+    2(P-1) * S over all ranks -- each element pulled once from every other
+    rank by its owner and pushed once to every other rank -- i.e. the bus
+    bytes 2(P-1)/P * S per rank, nothing redundant.  One-shot rounds (small
+    payloads) issue (P-1) * S pulls per rank and no pushes."""
+    import ctypes as C
+
+    from paper_1908_04207_b200._lib import call
+    from paper_1908_04207_b200.harness import rounds_pipelined
+    k = 5
+    world = EmulatedWorld(p)
+    cfg = CollectiveConfig(p=p, flavor="solo", vector_len=n, element="f4")
+    hs = [AllreduceHandle(cfg, r, world) for r in range(p)]
+    streams = [torch.cuda.Stream() for _ in range(p)]
+
+    def traffic():
+        out = []
+        for r in range(p):
+            rx, tx = C.c_uint64(), C.c_uint64()
+            call("ec_comm_traffic", hs[r].comm.ptr, r, C.byref(rx), C.byref(tx))
+            out.append((rx.value, tx.value))
+        return out
+
+    world.synchronize()
+    t0 = traffic()
+    errs = []
+
+    def body(r):
+        try:
+            torch.cuda.set_device(0)
+            with torch.cuda.stream(streams[r]):
+                rounds_pipelined(hs[r], 0, k)
+        except BaseException as e:  # surfaced below
+            errs.append(e)
+
+    th = [threading.Thread(target=body, args=(r,), daemon=True) for r in range(p)]
+    for x in th:
+        x.start()
+    for x in th:
+        x.join()
+    assert not errs, errs[0]
+    world.synchronize()
+    t1 = traffic()
+    world.close()
+    s = 4 * n
+    rx = [(t1[r][0] - t0[r][0]) / k for r in range(p)]
+    tx = [(t1[r][1] - t0[r][1]) / k for r in range(p)]
+    oneshot = s <= (1 << 20 if p == 2 else 65536)
+    if oneshot:
+        assert all(x == (p - 1) * s for x in rx) and not any(tx)
+    else:
+        assert sum(rx) + sum(tx) == 2 * (p - 1) * s
+        for r in range(p):        # per rank: the bus bytes, up to one chunk per owner
+            assert abs(rx[r] + tx[r] - 2 * (p - 1) / p * s) <= 2 * (p - 1) * 16384
