@@ -47,8 +47,6 @@
 #define EC_CF_SRC_GRAD 8u
 // direct mode: offer the gradient buffer iff the stash is still null at decision time
 #define EC_CF_SRC_GRAD_AUTO 16u
-// direct step: load the likely source and w while block 0 decides
-#define EC_CF_SPECULATE 0x1000u
 // done word: gen + 1, top bit = a reduced value of this owner's shard was non-finite
 #define EC_DONE_POISON (1ull << 63)
 

@@ -2034,8 +2034,7 @@ ec_direct_step_kernel(const EcDesc* __restrict__ dp, unsigned long long seq,
   T* stash = reinterpret_cast<T*>(d.send[d.rank]);
   const T* gbuf = reinterpret_cast<const T*>(d.gbuf[d.rank]);
   Vec16<T> pre_x, pre_w, pre_b;
-  const bool spec = (flags & EC_CF_SPECULATE) != 0;
-  if (spec && v < nv) {
+  if (v < nv) {
     pre_x.raw = ld_stream_v4((zc ? gbuf : stash) + v * V);
     pre_w.raw = ld_stream_v4(w + v * V);
     if (MOM) pre_b.raw = ld_stream_v4(mom + v * V);
@@ -2081,25 +2080,16 @@ ec_direct_step_kernel(const EcDesc* __restrict__ dp, unsigned long long seq,
   };
   bool bad = false;
   if (v < nv) {
-    Vec16<T> xv, wv, bv, gv;
-    if (spec) {
-      wv = pre_w;
-      if (MOM) bv = pre_b;
-      if (fold) {              // zero-copy call, pending stash: x = stash + g
-        gv = pre_x;
-        xv.raw = ld_stream_v4(stash + v * V);
-      } else if (!has) {
-        xv.raw = make_uint4(0, 0, 0, 0);
-      } else if (srcg == zc) { // the speculated source
-        xv = pre_x;
-      } else {
-        xv.raw = ld_stream_v4(src + v * V);
-      }
+    Vec16<T> xv, wv = pre_w, bv = pre_b, gv;
+    if (fold) {              // zero-copy call, pending stash: x = stash + g
+      gv = pre_x;
+      xv.raw = ld_stream_v4(stash + v * V);
+    } else if (!has) {
+      xv.raw = make_uint4(0, 0, 0, 0);
+    } else if (srcg == zc) { // the speculated source
+      xv = pre_x;
     } else {
-      xv.raw = has ? ld_stream_v4(src + v * V) : make_uint4(0, 0, 0, 0);
-      if (fold) gv.raw = ld_stream_v4(gbuf + v * V);
-      wv.raw = ld_stream_v4(w + v * V);
-      if (MOM) bv.raw = ld_stream_v4(mom + v * V);
+      xv.raw = ld_stream_v4(src + v * V);
     }
     if (fold) {
 #pragma unroll
@@ -2500,9 +2490,6 @@ cudaError_t launch_direct_step(int dtype, const EcDesc* d_desc, unsigned long lo
   attr[0].val.programmaticStreamSerializationAllowed = getenv("EC_NO_PDL") ? 0 : 1;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
-  // speculative loads during block 0's decision (EC_NO_SPEC=1 turns them off)
-  static const int no_spec = getenv("EC_NO_SPEC") ? 1 : 0;
-  if (!no_spec) flags |= EC_CF_SPECULATE;
   // full-occupancy shape: one CTA per 256 vectors (>= 1 CTA for the tail)
   const long long nvv = vec_ok ? n / V : 0;
   cfg.gridDim = dim3((unsigned)((nvv + 255) / 256 > 0 ? (nvv + 255) / 256 : 1));
