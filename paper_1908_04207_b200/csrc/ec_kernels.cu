@@ -2022,23 +2022,7 @@ ec_direct_step_kernel(const EcDesc* __restrict__ dp, unsigned long long seq,
   const EcDesc& d = *dp;
   EcLocal* L = d.local;
   __shared__ unsigned long long s_dw;
-  constexpr int V = Ops<T>::V;
   asm volatile("griddepcontrol.wait;" ::: "memory");
-  // Speculative loads while block 0 decides: this thread's vector of the
-  // likely source (the registered bucket for a zero-copy call, else the
-  // stash the fold kernel just wrote), of w and of the momentum buffer; the
-  // decision only confirms (or, rarely, redirects) them
-  const long long v = (long long)blockIdx.x * blockDim.x + threadIdx.x;
-  const long long nv = vec_ok ? d.n / V : 0;
-  const bool zc = (flags & EC_CF_SRC_GRAD_AUTO) != 0;
-  T* stash = reinterpret_cast<T*>(d.send[d.rank]);
-  const T* gbuf = reinterpret_cast<const T*>(d.gbuf[d.rank]);
-  Vec16<T> pre_x, pre_w, pre_b;
-  if (v < nv) {
-    pre_x.raw = ld_stream_v4((zc ? gbuf : stash) + v * V);
-    pre_w.raw = ld_stream_v4(w + v * V);
-    if (MOM) pre_b.raw = ld_stream_v4(mom + v * V);
-  }
   if (threadIdx.x == 0) {
     unsigned long long dw;
     if (blockIdx.x == 0) {
@@ -2069,28 +2053,25 @@ ec_direct_step_kernel(const EcDesc* __restrict__ dp, unsigned long long seq,
   }
   // an accepted offer with activation opened round g == t (P == 1)
   const long long g = t;
+  constexpr int V = Ops<T>::V;
   const bool has = (dw & EC_DW_HAS) != 0, fold = (dw & EC_DW_FOLD) != 0;
-  const bool srcg = (dw & EC_DW_SRCG) != 0;
-  const T* src = srcg ? gbuf : stash;
+  T* stash = reinterpret_cast<T*>(d.send[d.rank]);
+  const T* gbuf = reinterpret_cast<const T*>(d.gbuf[d.rank]);
+  const T* src = (dw & EC_DW_SRCG) ? gbuf : stash;
   T* slot = reinterpret_cast<T*>(d.ring[d.rank] + (g % d.R) * d.slot_bytes);
-  const long long n = d.n;
+  const long long n = d.n, nv = vec_ok ? n / V : 0;
   auto reduce1 = [&](T x) -> T {   // rs_fixed<T, 1>: tree of one canonical leaf, / 1
     T c[1] = {Ops<T>::canon(x)};
     return Ops<T>::divp(tree_sum<T, 1>(c), 1, (T)1, true);
   };
   bool bad = false;
+  const long long v = (long long)blockIdx.x * blockDim.x + threadIdx.x;
   if (v < nv) {
-    Vec16<T> xv, wv = pre_w, bv = pre_b, gv;
-    if (fold) {              // zero-copy call, pending stash: x = stash + g
-      gv = pre_x;
-      xv.raw = ld_stream_v4(stash + v * V);
-    } else if (!has) {
-      xv.raw = make_uint4(0, 0, 0, 0);
-    } else if (srcg == zc) { // the speculated source
-      xv = pre_x;
-    } else {
-      xv.raw = ld_stream_v4(src + v * V);
-    }
+    Vec16<T> xv, wv, bv, gv;
+    xv.raw = has ? ld_stream_v4(src + v * V) : make_uint4(0, 0, 0, 0);
+    if (fold) gv.raw = ld_stream_v4(gbuf + v * V);
+    wv.raw = ld_stream_v4(w + v * V);
+    if (MOM) bv.raw = ld_stream_v4(mom + v * V);
     if (fold) {
 #pragma unroll
       for (int l = 0; l < V; ++l) xv.e[l] = Ops<T>::add(xv.e[l], gv.e[l]);
