@@ -797,6 +797,10 @@ __device__ void engine_controller(const EcDesc& d, unsigned long long epoch) {
     {
       const unsigned long long hs = ld_acquire_gpu(&L->hp_seq);
       if (hs != last_hs) {
+        // A host reader re-checks done_gen1 after our ack (ec_wait): every
+        // completed round must be host-visible before the ack, or a deferred
+        // publication would let it pin a slot an early snapshot already took
+        publish_host();
         host_pin = *(volatile unsigned long long*)&L->hp_lo;
         // release: orders the pin read before the ack
         st_release_sys(&H->pin_ack, *(volatile unsigned long long*)&L->hp_ps);
