@@ -12,7 +12,9 @@ import os
 import re
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "lib", "libeagercoll_b200.so")
+# EC_DEBUG_LIB=1: the checked build (device assertions, build.py --debug)
+LIB_PATH = os.path.join(HERE, "lib", "libeagercoll_b200_debug.so" if os.environ.get("EC_DEBUG_LIB")
+                        else "libeagercoll_b200.so")
 HEADER = os.path.join(os.path.dirname(HERE), "include", "eagercoll_b200.h")
 
 EC_F32, EC_F64, EC_I64 = 0, 1, 2

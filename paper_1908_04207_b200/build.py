@@ -19,6 +19,11 @@ ROOT = os.path.dirname(HERE)
 CSRC = os.path.join(HERE, "csrc")
 LIB_DIR = os.path.join(HERE, "lib")
 LIB = os.path.join(LIB_DIR, "libeagercoll_b200.so")
+# the checked build: device assertions on ring indices, chunk ranges, slot
+# offsets and protocol invariants (EC_ASSERT in csrc/ec_common.cuh); selected
+# at import with EC_DEBUG_LIB=1 -- the bounds/race tooling while
+# compute-sanitizer is unavailable
+LIB_DEBUG = os.path.join(LIB_DIR, "libeagercoll_b200_debug.so")
 SOURCES = ["ec_kernels.cu", "ec_host.cu"]
 HEADERS = ["ec_common.cuh", "ec_ops.cuh"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
@@ -27,25 +32,26 @@ FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC,-O2", "-Xptxas",
          "--expt-relaxed-constexpr"]
 
 
-def _stale() -> bool:
-    if not os.path.exists(LIB):
+def _stale(lib: str = LIB) -> bool:
+    if not os.path.exists(lib):
         return True
-    t = os.path.getmtime(LIB)
+    t = os.path.getmtime(lib)
     deps = [os.path.join(CSRC, f) for f in SOURCES + HEADERS]
     deps.append(os.path.join(ROOT, "include", "eagercoll_b200.h"))
     deps.append(os.path.abspath(__file__))
     return any(os.path.getmtime(p) > t for p in deps)
 
 
-def build(force: bool = False, verbose: bool = False) -> str:
-    if not force and not _stale():
-        return LIB
+def build(force: bool = False, verbose: bool = False, debug: bool = False) -> str:
+    lib = LIB_DEBUG if debug else LIB
+    if not force and not _stale(lib):
+        return lib
     os.makedirs(LIB_DIR, exist_ok=True)
-    tmp = LIB + ".tmp"
-    cmd = [NVCC, *ARCH, *FLAGS, "-shared", "-o", tmp,
+    tmp = lib + ".tmp"
+    cmd = [NVCC, *ARCH, *FLAGS, *(["-DEC_DEBUG"] if debug else []), "-shared", "-o", tmp,
            *[os.path.join(CSRC, f) for f in SOURCES], "-lcudart"]
     res = subprocess.run(cmd, capture_output=True, text=True)
-    log = os.path.join(LIB_DIR, "build.log")
+    log = os.path.join(LIB_DIR, "build_debug.log" if debug else "build.log")
     with open(log, "w") as f:
         f.write(" ".join(cmd) + "\n" + res.stdout + res.stderr)
     if res.returncode != 0:
@@ -53,9 +59,9 @@ def build(force: bool = False, verbose: bool = False) -> str:
         raise RuntimeError(f"nvcc failed ({res.returncode}); see {log}")
     if verbose:
         sys.stdout.write(res.stdout + res.stderr)
-    os.replace(tmp, LIB)
-    return LIB
+    os.replace(tmp, lib)
+    return lib
 
 
 if __name__ == "__main__":
-    print(build(force="--force" in sys.argv, verbose="-v" in sys.argv))
+    print(build(force="--force" in sys.argv, verbose="-v" in sys.argv, debug="--debug" in sys.argv))

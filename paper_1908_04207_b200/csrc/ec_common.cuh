@@ -12,7 +12,16 @@
 //   send       the rank's contribution / eager-SGD stash (n elements).
 //   ring       R result slots of n elements; slot g % R holds u of generation g.
 #pragma once
+#include <assert.h>
 #include <stdint.h>
+
+// Device-side invariant checks of the checked build (-DEC_DEBUG, build.py
+// --debug): a failed check traps the kernel with file:line.  Free otherwise.
+#ifdef EC_DEBUG
+#define EC_ASSERT(x) assert(x)
+#else
+#define EC_ASSERT(x) ((void)0)
+#endif
 
 #define EC_MAX_P 64
 #define EC_REQ_RING 1024

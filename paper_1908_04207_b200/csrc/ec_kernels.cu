@@ -283,6 +283,7 @@ __device__ void round_tma(const EcDesc& d, const char* const* sp, int w, long lo
   const long long nch = (d.nvec + chv - 1) / chv;
   const long long c0 = oneshot ? 0 : chunk_lo(nch, r, P), c1 = oneshot ? nch : chunk_lo(nch, r + 1, P);
   if (oneshot) updm = 0;
+  EC_ASSERT(0 <= c0 && c0 <= c1 && c1 <= nch && g >= 0);
   const long long mine = (c1 - c0 > w) ? (c1 - c0 - w + d.W - 1) / d.W : 0;
   const long long off = (g % d.R) * d.slot_bytes;
   const size_t stage_bytes = (size_t)(P + 1) * chb;
@@ -312,6 +313,8 @@ __device__ void round_tma(const EcDesc& d, const char* const* sp, int w, long lo
     const long long v0 = c * chv;
     const unsigned bytes = (unsigned)(min((long long)chv, d.nvec - v0) * 16);
     char* st = smem + s * stage_bytes;
+    EC_ASSERT(c >= c0 && c < c1 && v0 < d.nvec && bytes > 0 && bytes <= (unsigned)chb);
+    EC_ASSERT((size_t)(s + 1) * stage_bytes <= (size_t)d.smem_bytes);
     mbar_expect_tx(&full[s], npop * bytes);
     for (int q = 0; q < P; ++q)
       if ((has >> q) & 1ull) {
@@ -341,6 +344,7 @@ __device__ void round_tma(const EcDesc& d, const char* const* sp, int w, long lo
     fence_proxy_async_smem();
     __syncthreads();
     if (threadIdx.x == 0) {
+      EC_ASSERT(off + (v0 + nvv) * 16 <= (long long)d.R * d.slot_bytes && nvv > 0);
       for (int j = 0; j < (oneshot ? 1 : P); ++j) {
         const int q = (r + j) % P;  // own slot first, then peers round-robin
         tma_store(d.ring[q] + off + v0 * 16, out, (unsigned)nvv * 16);
@@ -610,6 +614,7 @@ __device__ void engine_worker(const EcDesc& d, int w, unsigned long long epoch) 
         unsigned long long s = ld_acquire_gpu(&L->cmd_seq);
         if (s > seen) {
           const EcCmd* cm = &L->cmd[seen & 3];
+          EC_ASSERT(s - seen <= 2);     // at most lead (<= 2) commands out
           s_seq = seen + 1;
           s_gen = *(volatile const long long*)&cm->gen;
           s_has = *(volatile const unsigned long long*)&cm->has;
@@ -920,6 +925,7 @@ __device__ void engine_controller(const EcDesc& d, unsigned long long epoch) {
         guard_tau = arg < 0 ? EC_INF_GEN : arg;
         if (t >= 0 && t < pend_lo) pend_lo = t;
       }
+      EC_ASSERT(next_req - rep_from < 16);
       rep_st[next_req & 15] = (unsigned char)status;
       ++next_req;
       st_release_gpu(&L->req_done_dev, next_req);
@@ -999,6 +1005,7 @@ __device__ void engine_controller(const EcDesc& d, unsigned long long epoch) {
       }
       if (all) {
         EcCmd* cm = &L->cmd[seq & 3];   // the command of sequence number seq + 1
+        EC_ASSERT(n_issued < d.lead && go == g + n_issued);
         cm->gen = go;
         cm->has = has;
         cm->src = srcg;
@@ -1046,6 +1053,7 @@ __device__ void engine_controller(const EcDesc& d, unsigned long long epoch) {
         }
       } else {
         const unsigned long long t_done = globaltimer_ns();
+        EC_ASSERT(L->cmd[(iss_seq[k] - 1) & 3].gen == g);   // rounds complete in order
         publish_host();                          // at most one publication waits
         pub_gen = g;
         pub_fresh = iss_fresh[k];
@@ -1571,6 +1579,7 @@ __device__ __forceinline__ void post_request(EcLocal* L, unsigned long long seq1
     if (!(flags & EC_CF_SRC_GRAD)) *(volatile int*)&L->stash_null = 0;
   }
   EcReq* rec = &L->dreq[(seq1 - 1) % EC_REQ_RING];
+  EC_ASSERT(seq1 - 1 - *(volatile unsigned long long*)&L->req_done_dev < EC_REQ_RING);
   volatile EcReq* v = rec;
   v->type = type;
   v->flags = flags;
@@ -1696,6 +1705,7 @@ __device__ void wait_and_pin(EcLocal* L, EcHostCtl* H, long long t, int R, int l
     if (D < G + R - lead) break;
     G = D;
   }
+  EC_ASSERT(G >= t || ld_relaxed_sys(&H->error) != 0);
   L->step_gen = G;
   L->upd_t0 = globaltimer_ns();
   st_relaxed_sys(&H->stepgen[t % EC_REQ_RING], (unsigned long long)G + 1);
@@ -1851,6 +1861,7 @@ __device__ bool progressive_update(const EcDesc& d, T* __restrict__ w, T* __rest
     __syncthreads();
     const long long c = s_item;
     if (c < 0) break;
+    EC_ASSERT(c < nch);
     const long long v0 = c * chv;
     const int nvv = (int)min((long long)chv, d.nvec - v0);
     for (int base = threadIdx.x; base < nvv; base += blockDim.x * U) {
