@@ -25,6 +25,18 @@ def test_library_exports_every_header_symbol():
     assert _lib.lib.ec_version() >= 10000
 
 
+def test_checked_build_exports_every_header_symbol():
+    """The checked build (device assertions, build.py --debug, EC_DEBUG_LIB=1)
+    is the same ABI."""
+    import ctypes as C
+    import os
+    path = os.path.join(os.path.dirname(_lib.LIB_PATH), "libeagercoll_b200_debug.so")
+    if not os.path.exists(path):
+        pytest.skip("checked build not built (python -m paper_1908_04207_b200.build --debug)")
+    dbg = C.CDLL(path)
+    assert not [s for s in _lib.header_symbols() if not hasattr(dbg, s)]
+
+
 def test_abi_argument_errors_without_gpu():
     # argument validation happens before any CUDA call
     import ctypes as C
