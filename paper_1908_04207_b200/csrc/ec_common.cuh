@@ -163,11 +163,6 @@ struct alignas(128) EcLocal {
   // g >= min(pend_lo, last_off + 1) + guard_tau -- the oldest gradient not yet
   // delivered (a pending stash round, or the step in progress after the last
   // offer), eagersgd.py:102-108
-  // the current async step's own-shard update (written by its fold/post
-  // kernel before the offer): this rank's workers apply w - lr*u to the chunks
-  // they own straight from shared memory; own_w == 0: off
-  unsigned long long own_w, own_mom;
-  double own_lr, own_mu;
   unsigned long long nv_rx, nv_tx; // bytes this rank's workers pulled from / pushed to other
                                    // ranks (fused TMA modes; monotone, ec_comm_traffic)
   long long guard_tau;             // EC_INF_GEN: guard off

@@ -41,7 +41,6 @@ cudaError_t launch_stream_barrier(unsigned long long* count, unsigned long long 
                                   EcHostCtl* H, unsigned long long timeout_ns, cudaStream_t s);
 cudaError_t launch_fold_auto(int dtype, void* stash, const void* grad, long long n, EcLocal* L,
                              unsigned long long seq1, unsigned flags, long long t, int zero_copy,
-                             void* own_w, void* own_mom, double own_lr, double own_mu,
                              cudaStream_t s);
 cudaError_t launch_wait_gen(EcLocal* L, EcHostCtl* H, long long t, int R, int lead,
                             unsigned long long timeout_ns, cudaStream_t s);
@@ -51,7 +50,7 @@ cudaError_t launch_update_gen(int dtype, void* w, void* mom, const char* ring, l
                               int R, EcLocal* L, double lr, double mu, long long n, EcHostCtl* H,
                               long long t, unsigned long long timeout_ns, unsigned long long seq1,
                               void* stash, const void* gbuf, const EcDesc* dp, int progressive,
-                              int share, int own, cudaStream_t s);
+                              int share, cudaStream_t s);
 cudaError_t launch_write_u64(unsigned long long* p, unsigned long long v, cudaStream_t s);
 cudaError_t launch_direct_step(int dtype, const EcDesc* d_desc, unsigned long long seq,
                                unsigned int flags, void* w, void* mom, const void* ring,
@@ -1425,18 +1424,13 @@ int ec_step_async(ec_comm_t* c, int li, int64_t t, const void* grad, uint32_t fl
   const void* mom_eff = (mom && mu != 0.0) ? mom : nullptr;
   const bool prog = !c->direct && ec_comm_progressive(c) == 1 && !getenv("EC_NO_PROGRESSIVE") &&
                     ((((uintptr_t)w) | ((uintptr_t)mom_eff)) & 15) == 0;
-  // the owner's workers also apply the update to their own shard straight
-  // from shared memory (the update kernel skips those chunks)
-  static const int no_own = getenv("EC_NO_OWN_UPDATE") ? 1 : 0;
-  const bool own = prog && !no_own;
   if (!(c->direct && zero_copy)) {
     // fold (+ the offer's post, fused into the fold's last CTA, engine mode).
     // A world of one offering its registered buffer needs no fold launch: the
     // step kernel offers it in place, or folds it into a pending stash in-pass
     ProfScope ps(0, stream);
     CK(launch_fold_auto(c->dtype, r->send, grad, c->n, r->local, c->direct ? 0 : seq + 1,
-                        (flags & 7u) | (prog ? EC_CF_STEP : 0u), t, zero_copy ? 1 : 0,
-                        own ? w : nullptr, own ? (void*)mom_eff : nullptr, lr, mu, s));
+                        (flags & 7u) | (prog ? EC_CF_STEP : 0u), t, zero_copy ? 1 : 0, s));
   }
   if (c->direct) {
     // decide + round + update in one launch (see ec_direct_step_kernel)
@@ -1454,7 +1448,7 @@ int ec_step_async(ec_comm_t* c, int li, int64_t t, const void* grad, uint32_t fl
     ProfScope ps(1, stream);
     CK(launch_update_gen(c->dtype, w, (mom && mu != 0.0) ? mom : nullptr, r->ring, c->slot_bytes, c->R,
                          r->local, lr, mu, c->n, r->hd, t, c->timeout_ns, seq + 1, r->send,
-                         r->gbuf, c->d_descs + li, prog ? 1 : 0, c->n_local, own ? 1 : 0, s));
+                         r->gbuf, c->d_descs + li, prog ? 1 : 0, c->n_local, s));
   }
   if (seq_out) *seq_out = seq;
   return EC_OK;

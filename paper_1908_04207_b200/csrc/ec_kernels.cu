@@ -273,38 +273,11 @@ __device__ __forceinline__ void signal_chunks(const EcDesc& d, int w, long long 
 // the critical path.  The done word then means "my reads of everyone's
 // buffers and my own slot are complete", which is what both the peers (their
 // send buffers are free) and this rank (its result is in) wait for.
-// w -= lr * u (or the momentum form) for one chunk of u held in shared
-// memory: the owner's own-shard share of the step's update (same _rn
-// expressions as update_body)
-template <typename T>
-__device__ __forceinline__ void own_update_chunk(const char* out, int nvv, long long v0, T* w, T* mom,
-                                                 T lr, T mu) {
-  constexpr int V = Ops<T>::V;
-  for (int i = threadIdx.x; i < nvv; i += blockDim.x) {
-    Vec16<T> uv, wv, bv;
-    uv.raw = *reinterpret_cast<const uint4*>(out + (size_t)i * 16);
-    wv.raw = ld_stream_v4(w + (v0 + i) * V);
-    if (mom) bv.raw = ld_stream_v4(mom + (v0 + i) * V);
-#pragma unroll
-    for (int l = 0; l < V; ++l) {
-      if (mom) {
-        bv.e[l] = Ops<T>::mom(mu, bv.e[l], uv.e[l]);
-        wv.e[l] = Ops<T>::sgd(wv.e[l], lr, bv.e[l]);
-      } else {
-        wv.e[l] = Ops<T>::sgd(wv.e[l], lr, uv.e[l]);
-      }
-    }
-    if (mom) st_v4(mom + (v0 + i) * V, bv.raw);
-    st_v4(w + (v0 + i) * V, wv.raw);
-  }
-}
-
 template <typename T>
 __device__ void round_tma(const EcDesc& d, const char* const* sp, int w, long long g,
                           unsigned long long has, char* smem, unsigned long long* full,
                           unsigned long long& it, bool& bad, unsigned long long updm,
-                          bool oneshot, T* own_w = nullptr, T* own_mom = nullptr, T own_lr = 0,
-                          T own_mu = 0) {
+                          bool oneshot) {
   const int P = d.P, r = d.rank, S = d.stages;
   const int chv = d.chv, chb = d.chv * 16;
   const long long nch = (d.nvec + chv - 1) / chv;
@@ -386,9 +359,6 @@ __device__ void round_tma(const EcDesc& d, const char* const* sp, int w, long lo
         signal_chunks(d, w, g, updm, k - 1);
       }
     }
-    // the own shard's share of the step's update, from shared memory while
-    // the next chunk's loads are in flight (the update kernel skips it)
-    if (own_w) own_update_chunk<T>(out, nvv, v0, own_w, own_mom, own_lr, own_mu);
   }
   it += (unsigned long long)mine;
   if (threadIdx.x == 0) {
@@ -672,19 +642,7 @@ __device__ void engine_worker(const EcDesc& d, int w, unsigned long long epoch) 
     bool bad = false;
     if (d.mode == 0 || d.mode == 3) {
       const bool oneshot = d.mode == 3;
-      // this rank's own-shard update: only in a round where it updates
-      // progressively and its step's post set the parameters
-      T* ow = nullptr;
-      T* om = nullptr;
-      T olr = 0, omu = 0;
-      if (!oneshot && ((s_updm >> d.rank) & 1ull)) {
-        ow = reinterpret_cast<T*>(*(volatile unsigned long long*)&L->own_w);
-        om = reinterpret_cast<T*>(*(volatile unsigned long long*)&L->own_mom);
-        olr = (T)*(volatile double*)&L->own_lr;
-        omu = (T)*(volatile double*)&L->own_mu;
-      }
-      round_tma<T>(d, sp, w, g, has, smem, full, it, bad, s_updm, oneshot, ow, om, olr, omu);
-      if (ow && bad && threadIdx.x == 0) atomicOr(&L->upd_bad, 1u);
+      round_tma<T>(d, sp, w, g, has, smem, full, it, bad, s_updm, oneshot);
       // the scalar tail: reduced by the last owner and pushed to every slot,
       // or (one-shot) by every rank into its own slot
       if (w == 0 && (oneshot || d.rank == d.P - 1)) tail_push<T>(d, sp, has, g, oneshot);
@@ -1638,25 +1596,14 @@ template <typename T>
 __global__ void __launch_bounds__(256, 6)
 ec_fold_auto_kernel(T* __restrict__ stash, const T* __restrict__ grad, long long n,
                     EcLocal* __restrict__ L, int vec_ok, unsigned long long seq1, unsigned flags,
-                    long long t, int zero_copy, T* own_w, T* own_mom, double own_lr,
-                    double own_mu) {
+                    long long t, int zero_copy) {
   asm volatile("griddepcontrol.wait;" ::: "memory");   // PDL-launched behind the previous step
   const int add = *(volatile int*)&L->stash_null ? 0 : 1;
-  // the step's own-shard update parameters go out with the offer (read by
-  // this rank's workers in the round the offer joins)
-  auto set_own = [&]() {
-    *(volatile unsigned long long*)&L->own_w = (unsigned long long)own_w;
-    *(volatile unsigned long long*)&L->own_mom = (unsigned long long)own_mom;
-    *(volatile double*)&L->own_lr = own_lr;
-    *(volatile double*)&L->own_mu = own_mu;
-  };
   if (zero_copy && !add) {
     // null stash and the gradient sits in the registered buffer: offer it in
     // place (the reduction reads it over NVLink); nothing to fold
-    if (seq1 != 0 && blockIdx.x == 0 && threadIdx.x == 0) {
-      set_own();
+    if (seq1 != 0 && blockIdx.x == 0 && threadIdx.x == 0)
       post_request(L, seq1, EC_REQ_CONTRIB, flags | EC_CF_SRC_GRAD, t, 0);
-    }
     return;
   }
   constexpr int V = Ops<T>::V;
@@ -1706,7 +1653,6 @@ ec_fold_auto_kernel(T* __restrict__ stash, const T* __restrict__ grad, long long
     if (atomicAdd(&L->fold_count, 1ull) == gridDim.x - 1) {
       __threadfence();
       L->fold_count = 0;
-      set_own();
       post_request(L, seq1, EC_REQ_CONTRIB, flags, t, 0);
     }
   }
@@ -1858,7 +1804,7 @@ __device__ __forceinline__ bool update_body(T* __restrict__ w, T* __restrict__ m
 // expressions as update_body.  Returns whether a value of u was non-finite.
 template <typename T, bool MOM>
 __device__ bool progressive_update(const EcDesc& d, T* __restrict__ w, T* __restrict__ mom, T lr,
-                                   T mu, long long g, unsigned long long timeout_ns, int own) {
+                                   T mu, long long g, unsigned long long timeout_ns) {
   EcLocal* L = d.local;
   __shared__ long long s_item;
   constexpr int V = Ops<T>::V;
@@ -1876,7 +1822,6 @@ __device__ bool progressive_update(const EcDesc& d, T* __restrict__ w, T* __rest
     const long long rem = i % ((long long)P * W);
     q = (int)(rem / W);
     wq = (int)(rem % W);
-    if (own && q == d.rank) return -1;     // the owner's workers updated these chunks
     const long long c = chunk_lo(nch, q, P) + wq + k * W;
     return c < chunk_lo(nch, q + 1, P) ? c : -1;
   };
@@ -1961,7 +1906,7 @@ __device__ __forceinline__ void update_gen_body(T* __restrict__ w, T* __restrict
                                                 long long n, int vec_ok, EcHostCtl* H, long long t,
                                                 unsigned long long timeout_ns, unsigned long long seq1,
                                                 T* __restrict__ stash, const T* __restrict__ gbuf,
-                                                const EcDesc* __restrict__ dp, int own = 0) {
+                                                const EcDesc* __restrict__ dp) {
   __shared__ long long s_gen;
   __shared__ int s_late, s_fusedu;
   if (threadIdx.x == 0) {
@@ -1979,7 +1924,7 @@ __device__ __forceinline__ void update_gen_body(T* __restrict__ w, T* __restrict
   const T* __restrict__ u = reinterpret_cast<const T*>(ring + (G % R) * slot_bytes);
   bool bad;
   if (s_fusedu) {
-    bad = progressive_update<T, MOM>(*dp, w, mom, lr, mu, G, timeout_ns, own);
+    bad = progressive_update<T, MOM>(*dp, w, mom, lr, mu, G, timeout_ns);
   } else {
     if (s_late && stash && gbuf) {
       // a zero-copy offer missed its round: the gradient joins the stash (0 + g)
@@ -2038,9 +1983,9 @@ ec_update_gen_kernel(T* __restrict__ w, T* __restrict__ mom, const char* __restr
                      long long n, int vec_ok, EcHostCtl* H, long long t,
                      unsigned long long timeout_ns, unsigned long long seq1,
                      T* __restrict__ stash, const T* __restrict__ gbuf,
-                     const EcDesc* __restrict__ dp, int own) {
+                     const EcDesc* __restrict__ dp) {
   update_gen_body<T, MOM>(w, mom, ring, slot_bytes, R, L, lr, mu, n, vec_ok, H, t, timeout_ns, seq1,
-                          stash, gbuf, dp, own);
+                          stash, gbuf, dp);
 }
 
 // Direct mode (world of one) async step, ONE pass per element: decide the
@@ -2445,7 +2390,6 @@ cudaError_t launch_direct(int dtype, const EcDesc* d_desc, long long nvec, unsig
 
 cudaError_t launch_fold_auto(int dtype, void* stash, const void* grad, long long n, EcLocal* L,
                              unsigned long long seq1, unsigned flags, long long t, int zero_copy,
-                             void* own_w, void* own_mom, double own_lr, double own_mu,
                              cudaStream_t s) {
   counted();
   const int vec_ok = ((((uintptr_t)stash) | ((uintptr_t)grad)) & 15) == 0;
@@ -2464,15 +2408,12 @@ cudaError_t launch_fold_auto(int dtype, void* stash, const void* grad, long long
   cfg.numAttrs = 1;
   if (dtype == 0)
     return cudaLaunchKernelEx(&cfg, ec_fold_auto_kernel<float>, (float*)stash, (const float*)grad, n, L,
-                              vec_ok, seq1, flags, t, zero_copy, (float*)own_w, (float*)own_mom,
-                              own_lr, own_mu);
+                              vec_ok, seq1, flags, t, zero_copy);
   if (dtype == 1)
     return cudaLaunchKernelEx(&cfg, ec_fold_auto_kernel<double>, (double*)stash, (const double*)grad, n,
-                              L, vec_ok, seq1, flags, t, zero_copy, (double*)own_w, (double*)own_mom,
-                              own_lr, own_mu);
+                              L, vec_ok, seq1, flags, t, zero_copy);
   return cudaLaunchKernelEx(&cfg, ec_fold_auto_kernel<long long>, (long long*)stash,
-                            (const long long*)grad, n, L, vec_ok, seq1, flags, t, zero_copy,
-                            (long long*)nullptr, (long long*)nullptr, 0.0, 0.0);
+                            (const long long*)grad, n, L, vec_ok, seq1, flags, t, zero_copy);
 }
 
 cudaError_t launch_wait_done(EcLocal* L, EcHostCtl* H, long long t, unsigned long long timeout_ns,
@@ -2493,7 +2434,7 @@ cudaError_t launch_update_gen(int dtype, void* w, void* mom, const char* ring, l
                               int R, EcLocal* L, double lr, double mu, long long n, EcHostCtl* H,
                               long long t, unsigned long long timeout_ns, unsigned long long seq1,
                               void* stash, const void* gbuf, const EcDesc* dp, int progressive,
-                              int share, int own, cudaStream_t s) {
+                              int share, cudaStream_t s) {
   counted();
   const int vec_ok = ((((uintptr_t)w) | ((uintptr_t)mom) | ((uintptr_t)ring) | slot_bytes) & 15) == 0;
   const int V = dtype == 0 ? 4 : 2;
@@ -2515,12 +2456,11 @@ cudaError_t launch_update_gen(int dtype, void* w, void* mom, const char* ring, l
   if (dtype == 0) {
     auto kern = mom ? ec_update_gen_kernel<float, true> : ec_update_gen_kernel<float, false>;
     kern<<<grid, 256, 0, s>>>((float*)w, (float*)mom, ring, slot_bytes, R, L, (float)lr, (float)mu, n,
-                              vec_ok, H, t, timeout_ns, seq1, (float*)stash, (const float*)gbuf, dp,
-                              own);
+                              vec_ok, H, t, timeout_ns, seq1, (float*)stash, (const float*)gbuf, dp);
   } else if (dtype == 1) {
     auto kern = mom ? ec_update_gen_kernel<double, true> : ec_update_gen_kernel<double, false>;
     kern<<<grid, 256, 0, s>>>((double*)w, (double*)mom, ring, slot_bytes, R, L, lr, mu, n, vec_ok, H,
-                              t, timeout_ns, seq1, (double*)stash, (const double*)gbuf, dp, own);
+                              t, timeout_ns, seq1, (double*)stash, (const double*)gbuf, dp);
   }
   else
     return cudaErrorInvalidValue;
