@@ -207,7 +207,10 @@ def bench_flavor(world, rank, p, flavor, model, rounds=64, vector_len=64, link_s
     delays = delay_table(model, p, rounds)
     period = int(delays.max()) + link_slack_us + 1000
     cfg = CollectiveConfig(p=p, flavor=flavor, vector_len=vector_len, element="f8", seed=seed)
-    h = AllreduceHandle(cfg, rank, world, cid=2000 + hash(flavor) % 100 if cid is None else cid)
+    # a deterministic collective id per flavor (every rank must agree on it;
+    # str hashes are salted per process)
+    cid = 2000 + {"sync": 0, "solo": 1, "majority": 2}[flavor] if cid is None else cid
+    h = AllreduceHandle(cfg, rank, world, cid=cid)
     vec = np.full(vector_len, float(rank + 1))
     recs = []
     (barrier or world._barrier)()
