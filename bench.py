@@ -564,9 +564,33 @@ def device_timeline(h, t_end, k, max_over_ranks):
     data = [ts[i][3] - ts[i][1] for i in range(1, len(ts))]
     period = (ts[-1][3] - ts[0][3]) / (len(ts) - 1)
     m = lambda xs: max_over_ranks(sum(xs) / len(xs) / 1e3)  # noqa: E731
-    return {"done_to_offer": m(local), "offer_to_snapshot": m(arrive),
-            "snapshot_to_start": m(snap), "data_phase": m(data),
-            "period": max_over_ranks(period / 1e3)}
+    out = {"done_to_offer": m(local), "offer_to_snapshot": m(arrive),
+           "snapshot_to_start": m(snap), "data_phase": m(data),
+           "period": max_over_ranks(period / 1e3)}
+    # the step boundary inside done -> offer: round g-1 published -> step
+    # g-1's update reports -> step g's fold/post kernel starts -> it posts ->
+    # the controller takes the offer (steps are rounds here: t = g)
+    try:
+        import ctypes as C
+        from paper_1908_04207_b200 import _lib
+        st = {}
+        for g in [gens[0] - 1] + gens:
+            a = (C.c_uint64 * 3)()
+            _lib.call("ec_step_times", h.comm.ptr, h.li, g, a)
+            st[g] = list(a)
+        upd, kb, post, take = [], [], [], []
+        for i, g in enumerate(gens):
+            done_prev = ts[i][3]
+            upd.append(st[g - 1][0] - done_prev)
+            kb.append(st[g][1] - st[g - 1][0])
+            post.append(st[g][2] - st[g][1])
+            take.append(ts[i + 1][4] - st[g][2])
+        out["done_to_offer_detail"] = {"done_to_update_report": m(upd),
+                                       "report_to_next_kernel": m(kb),
+                                       "kernel_to_post": m(post), "post_to_taken": m(take)}
+    except Exception as e:  # noqa: BLE001 - diagnostic only
+        out["done_to_offer_detail"] = {"error": str(e)[:100]}
+    return out
 
 
 def bench_allreduce(args, pw, rank, world, dev, barrier, max_over_ranks, quiesce):

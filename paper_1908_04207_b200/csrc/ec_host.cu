@@ -1583,6 +1583,22 @@ int ec_debug_state(ec_comm_t* c, int li, int64_t* out) {
   return EC_OK;
 }
 
+int ec_step_times(ec_comm_t* c, int li, int64_t t, uint64_t* t3) {
+  int rc = check_li(c, li);
+  if (rc) return rc;
+  if (t < 0 || !t3) return fail(EC_E_ARG, "bad step");
+  EcRankHost* r = c->L[li];
+  cudaStream_t s;
+  CK(cudaSetDevice(c->device));
+  CK(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
+  cudaError_t e = cudaMemcpyAsync(t3, &r->local->tl[t & 63][0], 3 * sizeof(unsigned long long),
+                                  cudaMemcpyDeviceToHost, s);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+  cudaStreamDestroy(s);
+  if (e != cudaSuccess) return fail(EC_E_CUDA, "step times copy: %s", cudaGetErrorString(e));
+  return EC_OK;
+}
+
 int ec_comm_traffic(ec_comm_t* c, int li, uint64_t* rx_bytes, uint64_t* tx_bytes) {
   int rc = check_li(c, li);
   if (rc) return rc;

@@ -1598,12 +1598,15 @@ ec_fold_auto_kernel(T* __restrict__ stash, const T* __restrict__ grad, long long
                     EcLocal* __restrict__ L, int vec_ok, unsigned long long seq1, unsigned flags,
                     long long t, int zero_copy) {
   asm volatile("griddepcontrol.wait;" ::: "memory");   // PDL-launched behind the previous step
+  if (seq1 != 0 && blockIdx.x == 0 && threadIdx.x == 0) L->tl[t & 63][1] = globaltimer_ns();
   const int add = *(volatile int*)&L->stash_null ? 0 : 1;
   if (zero_copy && !add) {
     // null stash and the gradient sits in the registered buffer: offer it in
     // place (the reduction reads it over NVLink); nothing to fold
-    if (seq1 != 0 && blockIdx.x == 0 && threadIdx.x == 0)
+    if (seq1 != 0 && blockIdx.x == 0 && threadIdx.x == 0) {
+      L->tl[t & 63][2] = globaltimer_ns();
       post_request(L, seq1, EC_REQ_CONTRIB, flags | EC_CF_SRC_GRAD, t, 0);
+    }
     return;
   }
   constexpr int V = Ops<T>::V;
@@ -1653,6 +1656,7 @@ ec_fold_auto_kernel(T* __restrict__ stash, const T* __restrict__ grad, long long
     if (atomicAdd(&L->fold_count, 1ull) == gridDim.x - 1) {
       __threadfence();
       L->fold_count = 0;
+      L->tl[t & 63][2] = globaltimer_ns();
       post_request(L, seq1, EC_REQ_CONTRIB, flags, t, 0);
     }
   }
@@ -1969,6 +1973,7 @@ __device__ __forceinline__ void update_gen_body(T* __restrict__ w, T* __restrict
       if (s_late) *(volatile int*)&L->stash_null = 0;
       st_relaxed_sys(&H->stepbad[t % EC_REQ_RING], atomicExch(&L->upd_bad, 0u) ? 1ull : 0ull);
       const unsigned long long t1 = globaltimer_ns();
+      L->tl[t & 63][0] = t1;
       st_release_gpu(&L->pin_dev, ~0ull);  // every CTA has read the slot: unpin
       st_relaxed_sys(&H->stepns[t % EC_REQ_RING], t1 - *(volatile unsigned long long*)&L->upd_t0);
       st_release_sys(&H->steptag[t % EC_REQ_RING], (unsigned long long)t + 1);
