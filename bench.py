@@ -574,12 +574,15 @@ def device_timeline(h, t_end, k, max_over_ranks):
         import ctypes as C
         from paper_1908_04207_b200 import _lib
         st = {}
-        for g in [gens[0] - 1] + gens:
+        tail = gens[-60:]           # the device keeps the last 64 steps' stamps
+        for g in [tail[0] - 1] + tail:
             a = (C.c_uint64 * 3)()
             _lib.call("ec_step_times", h.comm.ptr, h.li, g, a)
             st[g] = list(a)
         upd, kb, post, take = [], [], [], []
-        for i, g in enumerate(gens):
+        off = len(gens) - len(tail)
+        for j, g in enumerate(tail):
+            i = off + j
             done_prev = ts[i][3]
             upd.append(st[g - 1][0] - done_prev)
             kb.append(st[g][1] - st[g - 1][0])
