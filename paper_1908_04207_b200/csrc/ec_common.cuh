@@ -214,6 +214,7 @@ struct alignas(128) EcHostCtl {
 struct EcDesc {
   int rank, P, flavor, dtype;
   int R, W, replay, vec;              // ring slots, worker CTAs, replay flag, elems / 16 B
+  unsigned idle_sleep_ns;             // controller's back-off cap with nothing in flight
   int quorum;                         // majority: arrivals the initiator waits for (0: none,
                                       // the reference's rule, collectives.py:311-317)
   int lead;                           // rounds the engine may have in flight (1, or 2: the

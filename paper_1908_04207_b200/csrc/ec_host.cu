@@ -753,6 +753,8 @@ static int upload_descs(ec_comm_t* c) {
     c->lead = ((c->mode == 0 || c->mode == 3) && c->R >= 3 && !getenv("EC_NO_LEAD")) ? 2 : 1;
     x.lead = c->lead;
     x.quorum = c->flavor == EC_MAJORITY ? c->quorum : 0;
+    x.idle_sleep_ns = getenv("EC_IDLE_SLEEP_NS") ? (unsigned)atoi(getenv("EC_IDLE_SLEEP_NS")) : 512u;
+    if (x.idle_sleep_ns < 32) x.idle_sleep_ns = 32;
     for (int q = 0; q < c->P; ++q) {
       x.ctrl[q] = c->ctrl[q];
       x.send[q] = c->send[q];

@@ -1094,7 +1094,7 @@ __device__ void engine_controller(const EcDesc& d, unsigned long long epoch) {
     } else {
       __nanosleep(ns);
       // a round in flight: poll its done words at a short interval
-      if (ns < (n_issued ? 128u : 512u)) ns <<= 1;
+      if (ns < (n_issued ? 128u : d.idle_sleep_ns)) ns <<= 1;
     }
   }
   (void)failed;
