@@ -576,10 +576,10 @@ def device_timeline(h, t_end, k, max_over_ranks):
         st = {}
         tail = gens[-60:]           # the device keeps the last 64 steps' stamps
         for g in [tail[0] - 1] + tail:
-            a = (C.c_uint64 * 3)()
+            a = (C.c_uint64 * 4)()
             _lib.call("ec_step_times", h.comm.ptr, h.li, g, a)
             st[g] = list(a)
-        upd, kb, post, take = [], [], [], []
+        upd, kb, post, seen, take = [], [], [], [], []
         off = len(gens) - len(tail)
         for j, g in enumerate(tail):
             i = off + j
@@ -587,10 +587,12 @@ def device_timeline(h, t_end, k, max_over_ranks):
             upd.append(st[g - 1][0] - done_prev)
             kb.append(st[g][1] - st[g - 1][0])
             post.append(st[g][2] - st[g][1])
-            take.append(ts[i + 1][4] - st[g][2])
+            seen.append(st[g][3] - st[g][2])
+            take.append(ts[i + 1][4] - st[g][3])
         out["done_to_offer_detail"] = {"done_to_update_report": m(upd),
                                        "report_to_next_kernel": m(kb),
-                                       "kernel_to_post": m(post), "post_to_taken": m(take)}
+                                       "kernel_to_post": m(post), "post_to_seen": m(seen),
+                                       "seen_to_taken": m(take)}
     except Exception as e:  # noqa: BLE001 - diagnostic only
         out["done_to_offer_detail"] = {"error": str(e)[:100]}
     return out

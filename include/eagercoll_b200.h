@@ -122,10 +122,10 @@ int ec_comm_idle_stats(ec_comm_t* c, uint64_t* parks, uint64_t* wakes, int* park
  * issue (P-1)/P * S each way per rank, 2(P-1)/P * S in all = the bus bytes. */
 int ec_comm_traffic(ec_comm_t* c, int local_idx, uint64_t* rx_bytes, uint64_t* tx_bytes);
 /* %globaltimer stamps of async step t (one of the last 64; instrumentation,
- * no reference counterpart): t3 = {its update kernel's report, the next
- * step's fold/post kernel start, that kernel's post} -- the step boundary
- * between one round's completion and the next offer. */
-int ec_step_times(ec_comm_t* c, int local_idx, int64_t t, uint64_t* t3);
+ * no reference counterpart): t4 = {its update kernel's report, its fold/post
+ * kernel's start, that kernel's post, the controller seeing the offer} --
+ * the step boundary between one round's completion and the next offer. */
+int ec_step_times(ec_comm_t* c, int local_idx, int64_t t, uint64_t* t4);
 int ec_comm_destroy(ec_comm_t* c);
 /* Device error word (watchdog timeout, out-of-order round): the reference's
  * TimeoutError / AssertionError (collectives.py:298,331). */

@@ -165,7 +165,7 @@ struct alignas(128) EcLocal {
   // offer), eagersgd.py:102-108
   // %globaltimer stamps of async step t (slot t % 64): its update kernel's
   // report, the next fold/post kernel's start and its post (step timeline)
-  unsigned long long tl[64][3];
+  unsigned long long tl[64][4];    // [3]: the controller saw the step's offer
   unsigned long long nv_rx, nv_tx; // bytes this rank's workers pulled from / pushed to other
                                    // ranks (fused TMA modes; monotone, ec_comm_traffic)
   long long guard_tau;             // EC_INF_GEN: guard off

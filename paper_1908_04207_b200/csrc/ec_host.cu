@@ -1593,7 +1593,7 @@ int ec_step_times(ec_comm_t* c, int li, int64_t t, uint64_t* t3) {
   cudaStream_t s;
   CK(cudaSetDevice(c->device));
   CK(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
-  cudaError_t e = cudaMemcpyAsync(t3, &r->local->tl[t & 63][0], 3 * sizeof(unsigned long long),
+  cudaError_t e = cudaMemcpyAsync(t3, &r->local->tl[t & 63][0], 4 * sizeof(unsigned long long),
                                   cudaMemcpyDeviceToHost, s);
   if (e == cudaSuccess) e = cudaStreamSynchronize(s);
   cudaStreamDestroy(s);

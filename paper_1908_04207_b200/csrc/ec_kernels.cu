@@ -846,6 +846,7 @@ __device__ void engine_controller(const EcDesc& d, unsigned long long epoch) {
       arg = *(volatile long long*)&dq->arg;
       dev_req = !(fl & EC_CF_HOSTPOSTED);
       fl &= ~EC_CF_HOSTPOSTED;
+      if (type == EC_REQ_CONTRIB && (fl & EC_CF_STEP) && t >= 0) L->tl[t & 63][3] = globaltimer_ns();
       unsigned long long status = 3;  // OK
       // while a round is in flight the open generation only moves on this
       // rank's own boarding (its offer for go, or an activation of go); any
