@@ -938,7 +938,7 @@ __device__ void engine_controller(const EcDesc& d, unsigned long long epoch) {
     if (open_ok && arrive_pending) {
       int n_arr = 0;
       for (int q = 0; q < P; ++q)
-        n_arr += ld_relaxed_sys(&C->arrive_from[q]) >= (unsigned long long)go + 1;
+        n_arr += ld_acquire_sys(&C->arrive_from[q]) >= (unsigned long long)go + 1;
       if (n_arr >= arrive_pending) {
         arrive_pending = 0;
         if (arrive_activate) activate();
@@ -957,7 +957,7 @@ __device__ void engine_controller(const EcDesc& d, unsigned long long epoch) {
         sgo = true;
       } else if (d.flavor != 0) {
         bool ext = false;
-        for (int q = 0; q < P && !ext; ++q) ext = ld_relaxed_sys(&C->act_from[q]) >= (unsigned long long)go + 1;
+        for (int q = 0; q < P && !ext; ++q) ext = ld_acquire_sys(&C->act_from[q]) >= (unsigned long long)go + 1;
         if (ext) {
           // staleness guard: an explicit threshold (ec_post_hold) or the
           // device-tracked ages (ec_post_guard), eagersgd.py:102-108
@@ -997,7 +997,7 @@ __device__ void engine_controller(const EcDesc& d, unsigned long long epoch) {
       bool all = true;
       unsigned long long fresh = 0, has = 0, srcg = 0, updm = 0;
       for (int q = 0; q < P; ++q) {
-        unsigned long long w = ld_relaxed_sys(&C->snap_from[q]);
+        unsigned long long w = ld_acquire_sys(&C->snap_from[q]);
         if ((w >> EC_SNAP_SHIFT) < (unsigned long long)go + 1) { all = false; break; }
         fresh |= (w & EC_SNAP_FRESH) << q;
         has |= ((w >> 1) & 1ull) << q;
@@ -1005,9 +1005,6 @@ __device__ void engine_controller(const EcDesc& d, unsigned long long epoch) {
         updm |= ((w >> 3) & 1ull) << q;
       }
       if (all) {
-        // the words are polled relaxed (an acquire per poll costs the whole
-        // loop microseconds); one fence orders the peers' offers before the round
-        fence_acq_rel_sys();
         EcCmd* cm = &L->cmd[seq & 3];   // the command of sequence number seq + 1
         EC_ASSERT(n_issued < d.lead && go == g + n_issued);
         cm->gen = go;
@@ -1044,7 +1041,7 @@ __device__ void engine_controller(const EcDesc& d, unsigned long long epoch) {
       bool all = true;
       unsigned long long poison = 0;
       for (int q = (d.mode != 1 ? 0 : r); q < (d.mode != 1 ? P : r + 1) && all; ++q) {
-        const unsigned long long wq = ld_relaxed_sys(&C->done_from[q]);
+        const unsigned long long wq = ld_acquire_sys(&C->done_from[q]);
         if ((wq & ~EC_DONE_POISON) < (unsigned long long)g + 1) all = false;
         else if ((wq & ~EC_DONE_POISON) == (unsigned long long)g + 1) poison |= wq & EC_DONE_POISON;
       }
@@ -1056,7 +1053,6 @@ __device__ void engine_controller(const EcDesc& d, unsigned long long epoch) {
           break;
         }
       } else {
-        fence_acq_rel_sys();   // acquire: every owner's data for g is in our slot
         const unsigned long long t_done = globaltimer_ns();
         EC_ASSERT(L->cmd[(iss_seq[k] - 1) & 3].gen == g);   // rounds complete in order
         publish_host();                          // at most one publication waits
