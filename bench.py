@@ -33,6 +33,11 @@ import threading
 import time
 
 os.environ.setdefault("CUDA_MODULE_LOADING", "EAGER")
+# the bench parks and relaunches its engines itself around device-wide syncs
+# (quiesce()), so the library's idle park (a safety net for user code that
+# syncs the device between steps) stays off: it would otherwise relaunch an
+# engine inside a timed region after a slow untimed phase (NVML init)
+os.environ.setdefault("EC_IDLE_PARK_MS", "0")
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
