@@ -611,11 +611,12 @@ def bench_allreduce(args, pw, rank, world, dev, barrier, max_over_ranks, quiesce
     from paper_1908_04207_b200 import AllreduceHandle, CollectiveConfig, _lib
     n = ALLREDUCE_100MB_N
     out = {}
-    # a communicator that only runs plain rounds: 128 TMA workers at P >= 3
-    # (the measured best for back-to-back rounds, profiles/r2_geom4.json; the
-    # step's handle keeps the default 80, best beside its progressive update)
+    # a communicator that only runs plain rounds: 128 TMA workers (the
+    # measured best for back-to-back rounds, profiles/r2_geom4.json,
+    # r2_geom2.json; at P >= 3 the step's handle keeps the default 80, best
+    # beside its progressive update)
     saved_workers = pw.workers
-    if world >= 3 and not os.environ.get("EC_WORKERS"):
+    if world >= 2 and not os.environ.get("EC_WORKERS"):
         pw.workers = 128
     for cid, flavor in ((10, "solo"), (11, "majority")):
         cfg = CollectiveConfig(p=world, flavor=flavor, vector_len=n, element="f4", seed=1234)

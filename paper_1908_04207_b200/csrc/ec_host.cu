@@ -524,7 +524,10 @@ int ec_comm_create(int world_size, int rank_lo, int n_local, int device, int64_t
       // P=2 587 -> 620 GB/s, P=4 623 -> 640 GB/s with 96 vs 64; in the P=4
       // step (progressive update beside the round) 80 is best (period 285-287
       // vs 290 us for 64 and 96), at P=2 96 wins (209 vs 211 us)
-      workers_per_rank = ldg ? 128 : (world_size == 2 ? 96 : 80);
+      // round 2 (two rounds in flight): at P=2 128 workers win for both the
+      // step (9,747 vs 9,586 steps/s) and plain rounds (644 vs 616 GB/s at
+      // 100 MB), profiles/r2_geom2.json; at P>=3 the step keeps 80
+      workers_per_rank = ldg ? 128 : (world_size == 2 ? 128 : 80);
     } else {  // emulated world: all ranks' CTA groups share one GPU
       workers_per_rank = (144 / n_local) - 1;
       if (workers_per_rank > 16) workers_per_rank = 16;
