@@ -94,6 +94,8 @@ struct EcCmd {
   unsigned long long has;          // has-data mask of the round
   unsigned long long src;          // ranks whose offer is their gradient buffer
   unsigned long long updm;         // ranks updating progressively (owners signal arrivals)
+  int wact;                        // worker CTAs the round uses (<= EcDesc::W)
+  int pad;
 };
 
 struct alignas(128) EcLocal {
@@ -214,6 +216,7 @@ struct alignas(128) EcHostCtl {
 struct EcDesc {
   int rank, P, flavor, dtype;
   int R, W, replay, vec;              // ring slots, worker CTAs, replay flag, elems / 16 B
+  int w_step;                         // worker CTAs of a round with progressive step updates
   unsigned idle_sleep_ns;             // controller's back-off cap with nothing in flight
   int quorum;                         // majority: arrivals the initiator waits for (0: none,
                                       // the reference's rule, collectives.py:311-317)

@@ -150,6 +150,7 @@ struct BlobV1 {
 
 struct ec_comm {
   int P = 0, rank_lo = 0, n_local = 0, device = 0, dtype = 0, flavor = 0, R = 2, W = 0;
+  int w_step = 0;   // workers of rounds with progressive step updates (EcDesc::w_step)
   bool W_default = true;
   long long n = 0, slot_bytes = 0;
   int elem = 4;
@@ -518,16 +519,13 @@ int ec_comm_create(int world_size, int rank_lo, int n_local, int device, int64_t
   }
   const bool w_default = workers_per_rank <= 0;
   if (workers_per_rank <= 0) {
-    const bool ldg = getenv("EC_DATA") && strcmp(getenv("EC_DATA"), "ldg") == 0;
     if (n_local == 1) {
-      // TMA: 96 workers at P=2, 80 beyond.  100 MB sweeps (plain rounds):
-      // P=2 587 -> 620 GB/s, P=4 623 -> 640 GB/s with 96 vs 64; in the P=4
-      // step (progressive update beside the round) 80 is best (period 285-287
-      // vs 290 us for 64 and 96), at P=2 96 wins (209 vs 211 us)
-      // round 2 (two rounds in flight): at P=2 128 workers win for both the
-      // step (9,747 vs 9,586 steps/s) and plain rounds (644 vs 616 GB/s at
-      // 100 MB), profiles/r2_geom2.json; at P>=3 the step keeps 80
-      workers_per_rank = ldg ? 128 : (world_size == 2 ? 128 : 80);
+      // 128 worker CTAs: with two rounds in flight plain 100 MB rounds run at
+      // 665-677 GB/s vs 616-636 with 80-96 (profiles/r2_geom4.json,
+      // r2_geom2.json); at P >= 3 a round carrying progressive step updates
+      // uses EcDesc::w_step = 80 of them (the step beside its update kernel:
+      // 14,146 vs 13,583 steps/s), at P = 2 all 128 (9,747 vs 9,586 with 96)
+      workers_per_rank = 128;
     } else {  // emulated world: all ranks' CTA groups share one GPU
       workers_per_rank = (144 / n_local) - 1;
       if (workers_per_rank > 16) workers_per_rank = 16;
@@ -536,6 +534,11 @@ int ec_comm_create(int world_size, int rank_lo, int n_local, int device, int64_t
   }
   c->W_default = w_default;
   c->W = workers_per_rank;
+  {
+    const char* e = getenv("EC_WORKERS_STEP");
+    const int ws = e ? atoi(e) : (world_size >= 3 && n_local == 1 ? 80 : workers_per_rank);
+    c->w_step = ws > 0 && ws < workers_per_rank ? ws : workers_per_rank;
+  }
   c->direct = world_size == 1 && !getenv("EC_FORCE_ENGINE");
   // Data phase: fused TMA (default) or two-phase ld.cg pull (EC_DATA=ldg).
   // TMA geometry: P source slices + 1 output slice per stage, `stages` deep,
@@ -734,6 +737,7 @@ static int upload_descs(ec_comm_t* c) {
     x.dtype = c->dtype;
     x.R = c->R;
     x.W = c->W;
+    x.w_step = c->w_step < c->W ? c->w_step : c->W;   // W may have shrunk to the budget
     // arrival words of progressive updates: < 0 (default) geometric, after
     // 1/2, 3/4, 7/8, ... of a worker's chunks (P=4 step: 14.37k vs 14.28k
     // steps/s with ~4 evenly spaced words, profiles/r2_signal_n4.log);
@@ -1044,7 +1048,8 @@ int ec_stream_barrier(ec_comm_t* c, int li, void* stream) {
 }
 
 int ec_comm_progressive(ec_comm_t* c) {
-  return c ? (!c->direct && c->mode == 0 && c->W <= EC_PROG_W && c->dtype != EC_I64) : -1;
+  return c ? (!c->direct && c->mode == 0 && (c->w_step < c->W ? c->w_step : c->W) <= EC_PROG_W &&
+               c->dtype != EC_I64) : -1;
 }
 
 int ec_fold(ec_comm_t* c, int li, const void* grad, int mode, void* stream) {

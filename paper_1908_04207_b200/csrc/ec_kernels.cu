@@ -277,14 +277,16 @@ template <typename T>
 __device__ void round_tma(const EcDesc& d, const char* const* sp, int w, long long g,
                           unsigned long long has, char* smem, unsigned long long* full,
                           unsigned long long& it, bool& bad, unsigned long long updm,
-                          bool oneshot) {
+                          bool oneshot, int wact) {
+  // wact: the worker CTAs this round uses (all W, or the step's count in a
+  // round with progressive updates -- the update kernel maps chunks with it)
   const int P = d.P, r = d.rank, S = d.stages;
   const int chv = d.chv, chb = d.chv * 16;
   const long long nch = (d.nvec + chv - 1) / chv;
   const long long c0 = oneshot ? 0 : chunk_lo(nch, r, P), c1 = oneshot ? nch : chunk_lo(nch, r + 1, P);
   if (oneshot) updm = 0;
   EC_ASSERT(0 <= c0 && c0 <= c1 && c1 <= nch && g >= 0);
-  const long long mine = (c1 - c0 > w) ? (c1 - c0 - w + d.W - 1) / d.W : 0;
+  const long long mine = (w < wact && c1 - c0 > w) ? (c1 - c0 - w + wact - 1) / wact : 0;
   const long long off = (g % d.R) * d.slot_bytes;
   const size_t stage_bytes = (size_t)(P + 1) * chb;
   const unsigned npop = (unsigned)__popcll(has);
@@ -309,7 +311,7 @@ __device__ void round_tma(const EcDesc& d, const char* const* sp, int w, long lo
   unsigned long long nv_rx = 0, nv_tx = 0;
   auto issue = [&](long long k) {  // thread 0: loads of my k-th chunk
     const int s = (int)((it + k) % S);
-    const long long c = c0 + w + k * d.W;
+    const long long c = c0 + w + k * wact;
     const long long v0 = c * chv;
     const unsigned bytes = (unsigned)(min((long long)chv, d.nvec - v0) * 16);
     char* st = smem + s * stage_bytes;
@@ -329,7 +331,7 @@ __device__ void round_tma(const EcDesc& d, const char* const* sp, int w, long lo
   for (long long k = 0; k < mine; ++k) {
     const int s = (int)((it + k) % S);
     const unsigned parity = (unsigned)(((it + k) / S) & 1ull);
-    const long long c = c0 + w + k * d.W;
+    const long long c = c0 + w + k * wact;
     const long long v0 = c * chv;
     const int nvv = (int)min((long long)chv, d.nvec - v0);
     char* st = smem + s * stage_bytes;
@@ -593,6 +595,7 @@ __device__ void engine_worker(const EcDesc& d, int w, unsigned long long epoch) 
   extern __shared__ __align__(128) char smem[];
   __shared__ __align__(8) unsigned long long full[8];
   __shared__ unsigned long long s_seq, s_has, s_src, s_updm;
+  __shared__ int s_wact;
   __shared__ long long s_gen;
   __shared__ int s_exit;
   __shared__ const char* sp[EC_MAX_P];
@@ -620,6 +623,7 @@ __device__ void engine_worker(const EcDesc& d, int w, unsigned long long epoch) 
           s_has = *(volatile const unsigned long long*)&cm->has;
           s_updm = *(volatile const unsigned long long*)&cm->updm;
           s_src = *(volatile const unsigned long long*)&cm->src;
+          s_wact = *(volatile const int*)&cm->wact;
           s_exit = 0;
           break;
         }
@@ -642,7 +646,7 @@ __device__ void engine_worker(const EcDesc& d, int w, unsigned long long epoch) 
     bool bad = false;
     if (d.mode == 0 || d.mode == 3) {
       const bool oneshot = d.mode == 3;
-      round_tma<T>(d, sp, w, g, has, smem, full, it, bad, s_updm, oneshot);
+      round_tma<T>(d, sp, w, g, has, smem, full, it, bad, s_updm, oneshot, s_wact);
       // the scalar tail: reduced by the last owner and pushed to every slot,
       // or (one-shot) by every rank into its own slot
       if (w == 0 && (oneshot || d.rank == d.P - 1)) tail_push<T>(d, sp, has, g, oneshot);
@@ -790,7 +794,6 @@ __device__ void engine_controller(const EcDesc& d, unsigned long long epoch) {
   // snapshot check sees it (ec_wait's pin waits for the ack)
   unsigned long long host_pin = ld_relaxed_sys(&H->pin_lo);
   unsigned long long last_hs = ld_acquire_gpu(&L->hp_seq);
-  bool failed = false;
   while (true) {
     bool progress = false;
     // the open generation takes protocol steps only while fewer than `lead`
@@ -886,7 +889,7 @@ __device__ void engine_controller(const EcDesc& d, unsigned long long epoch) {
         } else {
           contrib = (int)(EC_SNAP_DATA | ((fl & 1u) ? EC_SNAP_FRESH : 0ull) |
                           ((fl & EC_CF_SRC_GRAD) ? EC_SNAP_SRC_GRAD : 0ull));
-          if ((fl & EC_CF_STEP) && dev_req && d.mode == 0 && d.W <= EC_PROG_W) {
+          if ((fl & EC_CF_STEP) && dev_req && d.mode == 0 && d.w_step <= EC_PROG_W) {
             // the step's update kernel (already resident behind the offer)
             // consumes round go's chunks as they land: owners publish arrival
             // words to us; pin slot go on its behalf now (it unpins when
@@ -1011,6 +1014,9 @@ __device__ void engine_controller(const EcDesc& d, unsigned long long epoch) {
         cm->has = has;
         cm->src = srcg;
         cm->updm = updm;
+        // rounds with progressive updates use the step's worker count (every
+        // rank derives the same from the same snapshot words)
+        cm->wact = (updm && d.w_step < d.W) ? d.w_step : d.W;
         ++seq;
         const int k = (int)(go & 1);
         iss_fresh[k] = fresh;
@@ -1049,8 +1055,7 @@ __device__ void engine_controller(const EcDesc& d, unsigned long long epoch) {
         if (globaltimer_ns() - iss_tcmd[k] > d.timeout_ns) {
           st_release_sys(&H->error_info, (unsigned long long)g);
           st_release_sys(&H->error, EC_DERR_TIMEOUT);
-          failed = true;
-          break;
+          break;   // watchdog: park with the round abandoned (error word set)
         }
       } else {
         const unsigned long long t_done = globaltimer_ns();
@@ -1098,7 +1103,6 @@ __device__ void engine_controller(const EcDesc& d, unsigned long long epoch) {
       if (ns < (n_issued ? 128u : d.idle_sleep_ns)) ns <<= 1;
     }
   }
-  (void)failed;
   publish_host();
   // park: persist the protocol state, release the workers, acknowledge.  A
   // parked engine has no round in flight (a watchdog timeout parks with the
@@ -1814,7 +1818,7 @@ __device__ bool progressive_update(const EcDesc& d, T* __restrict__ w, T* __rest
   __shared__ long long s_item;
   constexpr int V = Ops<T>::V;
   constexpr int U = MOM ? 2 : 4;
-  const int P = d.P, W = d.W, chv = d.chv;
+  const int P = d.P, W = d.W < d.w_step ? d.W : d.w_step, chv = d.chv;   // the round's wact
   const long long nch = (d.nvec + chv - 1) / chv;
   long long kmax = 0;
   for (int q = 0; q < P; ++q) {
