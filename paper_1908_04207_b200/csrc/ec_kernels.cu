@@ -1590,8 +1590,7 @@ __device__ __forceinline__ void post_request(EcLocal* L, unsigned long long seq1
   v->flags = flags;
   v->t = t;
   v->arg = arg;
-  __threadfence();
-  st_release_gpu(&rec->seq1, seq1);
+  st_release_gpu(&rec->seq1, seq1);   // release: the fields (and stash_null) before seq1
   atomicMax(&L->posted, seq1);
 }
 
