@@ -49,6 +49,7 @@ _SIGS = {
     "ec_comm_idle_stats": (_i32, [_vp, _P(_u64), _P(_u64), _P(_i32)]),
     "ec_comm_traffic": (_i32, [_vp, _i32, _P(_u64), _P(_u64)]),
     "ec_step_times": (_i32, [_vp, _i32, _i64, _P(_u64)]),
+    "ec_step_iterations": (_i32, [_vp, _i32, _i64, _P(_u64)]),
     "ec_comm_destroy": (_i32, [_vp]),
     "ec_comm_error": (_i32, [_vp, _i32, _P(_u64), _P(_u64)]),
     "ec_debug_state": (_i32, [_vp, _i32, _P(_i64)]),

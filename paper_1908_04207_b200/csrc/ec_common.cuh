@@ -168,6 +168,9 @@ struct alignas(128) EcLocal {
   // %globaltimer stamps of async step t (slot t % 64): its update kernel's
   // report, the next fold/post kernel's start and its post (step timeline)
   unsigned long long tl[64][4];    // [3]: the controller saw the step's offer
+  // checked build only: the controller's last 16 iteration starts when it saw
+  // step t's offer (tl_it[t % 8]), for the step-boundary study
+  unsigned long long tl_it[8][16];
   unsigned long long nv_rx, nv_tx; // bytes this rank's workers pulled from / pushed to other
                                    // ranks (fused TMA modes; monotone, ec_comm_traffic)
   long long guard_tau;             // EC_INF_GEN: guard off

@@ -1609,6 +1609,24 @@ int ec_step_times(ec_comm_t* c, int li, int64_t t, uint64_t* t3) {
   return EC_OK;
 }
 
+// checked build: the controller's 16 iteration starts before it saw step t's
+// offer (t one of the last 8); zeros in the production build
+int ec_step_iterations(ec_comm_t* c, int li, int64_t t, uint64_t* t16) {
+  int rc = check_li(c, li);
+  if (rc) return rc;
+  if (t < 0 || !t16) return fail(EC_E_ARG, "bad step");
+  EcRankHost* r = c->L[li];
+  cudaStream_t s;
+  CK(cudaSetDevice(c->device));
+  CK(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
+  cudaError_t e = cudaMemcpyAsync(t16, &r->local->tl_it[t & 7][0], 16 * sizeof(unsigned long long),
+                                  cudaMemcpyDeviceToHost, s);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+  cudaStreamDestroy(s);
+  if (e != cudaSuccess) return fail(EC_E_CUDA, "iterations copy: %s", cudaGetErrorString(e));
+  return EC_OK;
+}
+
 int ec_comm_traffic(ec_comm_t* c, int li, uint64_t* rx_bytes, uint64_t* tx_bytes) {
   int rc = check_li(c, li);
   if (rc) return rc;

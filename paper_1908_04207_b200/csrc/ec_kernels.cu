@@ -794,8 +794,15 @@ __device__ void engine_controller(const EcDesc& d, unsigned long long epoch) {
   // snapshot check sees it (ec_wait's pin waits for the ack)
   unsigned long long host_pin = ld_relaxed_sys(&H->pin_lo);
   unsigned long long last_hs = ld_acquire_gpu(&L->hp_seq);
+#ifdef EC_DEBUG
+  unsigned long long it_ring[16];
+  unsigned it_n = 0;
+#endif
   while (true) {
     bool progress = false;
+#ifdef EC_DEBUG
+    it_ring[it_n++ & 15] = globaltimer_ns();
+#endif
     // the open generation takes protocol steps only while fewer than `lead`
     // rounds are in flight
     const bool open_ok = n_issued < d.lead;
@@ -849,7 +856,12 @@ __device__ void engine_controller(const EcDesc& d, unsigned long long epoch) {
       arg = *(volatile long long*)&dq->arg;
       dev_req = !(fl & EC_CF_HOSTPOSTED);
       fl &= ~EC_CF_HOSTPOSTED;
-      if (type == EC_REQ_CONTRIB && (fl & EC_CF_STEP) && t >= 0) L->tl[t & 63][3] = globaltimer_ns();
+      if (type == EC_REQ_CONTRIB && (fl & EC_CF_STEP) && t >= 0) {
+        L->tl[t & 63][3] = globaltimer_ns();
+#ifdef EC_DEBUG
+        for (int i = 0; i < 16; ++i) L->tl_it[t & 7][i] = it_ring[(it_n + i) & 15];
+#endif
+      }
       unsigned long long status = 3;  // OK
       // while a round is in flight the open generation only moves on this
       // rank's own boarding (its offer for go, or an activation of go); any
