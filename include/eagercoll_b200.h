@@ -127,8 +127,9 @@ int ec_comm_traffic(ec_comm_t* c, int local_idx, uint64_t* rx_bytes, uint64_t* t
  * the step boundary between one round's completion and the next offer. */
 int ec_step_times(ec_comm_t* c, int local_idx, int64_t t, uint64_t* t4);
 /* Checked build (EC_DEBUG) diagnostics: the controller's last 16 loop-iteration
- * start stamps when it saw step t's offer (one of the last 8 steps); zeros
- * in the production build.  No reference counterpart. */
+ * start stamps when it saw step t's offer (one of the last 8 steps), then
+ * 16 x 4 section stamps of those iterations (t16 holds 80 words); zeros in
+ * the production build.  No reference counterpart. */
 int ec_step_iterations(ec_comm_t* c, int local_idx, int64_t t, uint64_t* t16);
 int ec_comm_destroy(ec_comm_t* c);
 /* Device error word (watchdog timeout, out-of-order round): the reference's

@@ -171,6 +171,7 @@ struct alignas(128) EcLocal {
   // checked build only: the controller's last 16 iteration starts when it saw
   // step t's offer (tl_it[t % 8]), for the step-boundary study
   unsigned long long tl_it[8][16];
+  unsigned long long tl_sec[8][16][4];   // section stamps of those iterations
   unsigned long long nv_rx, nv_tx; // bytes this rank's workers pulled from / pushed to other
                                    // ranks (fused TMA modes; monotone, ec_comm_traffic)
   long long guard_tau;             // EC_INF_GEN: guard off

@@ -1612,6 +1612,7 @@ int ec_step_times(ec_comm_t* c, int li, int64_t t, uint64_t* t3) {
 // checked build: the controller's 16 iteration starts before it saw step t's
 // offer (t one of the last 8); zeros in the production build
 int ec_step_iterations(ec_comm_t* c, int li, int64_t t, uint64_t* t16) {
+  // t16: 16 iteration starts, then 16 x 4 section stamps (80 words)
   int rc = check_li(c, li);
   if (rc) return rc;
   if (t < 0 || !t16) return fail(EC_E_ARG, "bad step");
@@ -1621,6 +1622,9 @@ int ec_step_iterations(ec_comm_t* c, int li, int64_t t, uint64_t* t16) {
   CK(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
   cudaError_t e = cudaMemcpyAsync(t16, &r->local->tl_it[t & 7][0], 16 * sizeof(unsigned long long),
                                   cudaMemcpyDeviceToHost, s);
+  if (e == cudaSuccess)
+    e = cudaMemcpyAsync(t16 + 16, &r->local->tl_sec[t & 7][0][0], 64 * sizeof(unsigned long long),
+                        cudaMemcpyDeviceToHost, s);
   if (e == cudaSuccess) e = cudaStreamSynchronize(s);
   cudaStreamDestroy(s);
   if (e != cudaSuccess) return fail(EC_E_CUDA, "iterations copy: %s", cudaGetErrorString(e));

@@ -686,6 +686,37 @@ __device__ __forceinline__ unsigned int ld_relaxed_sys_u32(const unsigned int* p
   return v;
 }
 
+// Peer-written control words, polled as a pre-check: relaxed loads of a group
+// of eight are all in flight at once (an acquire load blocks the next one, and
+// each costs an L2 round trip, 0.2-0.4 us under a data phase), folded to the
+// min / max of f(word).  The words are monotone, so a passing pre-check stays
+// passing; the caller re-reads with acquire where the word orders data.
+template <bool kMax, typename F>
+__device__ __forceinline__ unsigned long long poll_fold(const unsigned long long* w, int P, F f) {
+  unsigned long long acc = kMax ? 0ull : ~0ull;
+  for (int q0 = 0; q0 < P; q0 += 8) {
+    unsigned long long v[8];
+#pragma unroll
+    for (int i = 0; i < 8; ++i) v[i] = q0 + i < P ? ld_relaxed_sys(w + q0 + i) : (kMax ? 0ull : ~0ull);
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      const unsigned long long x = q0 + i < P ? f(v[i]) : (kMax ? 0ull : ~0ull);
+      acc = kMax ? (x > acc ? x : acc) : (x < acc ? x : acc);
+    }
+  }
+  return acc;
+}
+
+// The host poller's mirror for the controller: both threads are in one CTA, so
+// the words the controller reads every iteration live in shared memory
+// (device-memory copies in EcLocal persist them across relaunches).
+struct EcHpShared {
+  unsigned long long seq;    // EcLocal::hp_seq
+  unsigned long long lo;     // EcLocal::hp_lo
+  unsigned long long ps;     // EcLocal::hp_ps
+  unsigned long long stop;   // 0 none, 1 explicit pause, 2 idle park (this launch)
+};
+
 // The controller runs the protocol of one "open" generation go (requests,
 // activation, snapshot, command) while up to two rounds are in flight: once
 // round g's command is out, the open generation is g + 1, so a rank whose next
@@ -694,7 +725,7 @@ __device__ __forceinline__ unsigned int ld_relaxed_sys_u32(const unsigned int* p
 // workers find g + 1's command waiting when they finish g (EcDesc::lead == 2,
 // fused TMA mode with R >= 3 result slots).  Round g is published when every
 // owner's done word for g is in; rounds publish in order.
-__device__ void engine_controller(const EcDesc& d, unsigned long long epoch) {
+__device__ void engine_controller(const EcDesc& d, unsigned long long epoch, volatile EcHpShared* hp) {
   EcLocal* L = d.local;
   EcHostCtl* H = d.hctl;
   EcCtrl* C = d.ctrl[d.rank];
@@ -793,10 +824,14 @@ __device__ void engine_controller(const EcDesc& d, unsigned long long epoch) {
   // 32) and acknowledged HERE after this thread read it, so every later
   // snapshot check sees it (ec_wait's pin waits for the ack)
   unsigned long long host_pin = ld_relaxed_sys(&H->pin_lo);
-  unsigned long long last_hs = ld_acquire_gpu(&L->hp_seq);
+  unsigned long long last_hs = hp->seq;
 #ifdef EC_DEBUG
   unsigned long long it_ring[16];
+  unsigned long long sec_ring[16][4];
   unsigned it_n = 0;
+#define EC_SEC(k) sec_ring[(it_n - 1) & 15][k] = globaltimer_ns()
+#else
+#define EC_SEC(k)
 #endif
   while (true) {
     bool progress = false;
@@ -810,24 +845,26 @@ __device__ void engine_controller(const EcDesc& d, unsigned long long epoch) {
     // copies host-posted requests into the device ring), so this thread only
     // reads device memory.
     {
-      const unsigned long long hs = ld_acquire_gpu(&L->hp_seq);
+      const unsigned long long hs = hp->seq;
       if (hs != last_hs) {
+        __threadfence_block();   // acquire (CTA scope): the poller's lo / ps before seq
         // A host reader re-checks done_gen1 after our ack (ec_wait): every
         // completed round must be host-visible before the ack, or a deferred
         // publication would let it pin a slot an early snapshot already took
         publish_host();
-        host_pin = *(volatile unsigned long long*)&L->hp_lo;
+        host_pin = hp->lo;
         // release: orders the pin read before the ack
-        st_release_sys(&H->pin_ack, *(volatile unsigned long long*)&L->hp_ps);
+        st_release_sys(&H->pin_ack, hp->ps);
         last_hs = hs;
       }
       // stop requests: an explicit pause drains the open generation (a held
       // one is let go); an idle park (host watchdog, ec_host.cu) exits only
       // while nothing is in flight, and may be withdrawn
-      const bool st_now = ld_acquire_gpu(&L->hp_stop) == epoch;
+      const unsigned long long sk = hp->stop;
+      const bool st_now = sk != 0;
       if (st_now && !stopping) stop_t0 = globaltimer_ns();
       stopping = st_now;
-      idle_stop = st_now && *(volatile unsigned long long*)&L->hp_stop_kind == 2;
+      idle_stop = sk == 2;
       if (!idle_stop && voted) {
         // withdrawn: take the vote back -- unless every controller had voted,
         // in which case the park is committed (the others may be gone)
@@ -841,6 +878,7 @@ __device__ void engine_controller(const EcDesc& d, unsigned long long epoch) {
         else voted = false;
       }
     }
+    EC_SEC(0);
     // ---- requests, strictly in sequence order: stream-posted ones sit in the
     // device ring (cheap), host-posted ones only in the host-mapped ring
     while (open_ok) {
@@ -848,7 +886,9 @@ __device__ void engine_controller(const EcDesc& d, unsigned long long epoch) {
       unsigned type, fl;
       long long t, arg;
       bool dev_req = false;
-      // stream-posted requests and (copied by the poller) host-posted ones
+      // stream-posted requests and (copied by the poller) host-posted ones;
+      // the acquire load only once the relaxed one saw the request
+      if (*(volatile unsigned long long*)&dq->seq1 != next_req + 1) break;
       if (ld_acquire_gpu(&dq->seq1) != next_req + 1) break;
       type = *(volatile unsigned*)&dq->type;
       fl = *(volatile unsigned*)&dq->flags;
@@ -859,7 +899,10 @@ __device__ void engine_controller(const EcDesc& d, unsigned long long epoch) {
       if (type == EC_REQ_CONTRIB && (fl & EC_CF_STEP) && t >= 0) {
         L->tl[t & 63][3] = globaltimer_ns();
 #ifdef EC_DEBUG
-        for (int i = 0; i < 16; ++i) L->tl_it[t & 7][i] = it_ring[(it_n + i) & 15];
+        for (int i = 0; i < 16; ++i) {
+          L->tl_it[t & 7][i] = it_ring[(it_n + i) & 15];
+          for (int k = 0; k < 4; ++k) L->tl_sec[t & 7][i][k] = sec_ring[(it_n + i) & 15][k];
+        }
 #endif
       }
       unsigned long long status = 3;  // OK
@@ -948,6 +991,7 @@ __device__ void engine_controller(const EcDesc& d, unsigned long long epoch) {
       if (next_req - rep_from >= 16) flush_replies();
       progress = true;
     }
+    EC_SEC(1);
     // ---- arrival barrier: `arrive_pending` ranks boarded (all of them in
     // all-arrive replay mode, the quorum in majority-quorum mode) -> activate
     if (open_ok && arrive_pending) {
@@ -971,8 +1015,9 @@ __device__ void engine_controller(const EcDesc& d, unsigned long long epoch) {
       } else if (internal_act) {
         sgo = true;
       } else if (d.flavor != 0) {
-        bool ext = false;
-        for (int q = 0; q < P && !ext; ++q) ext = ld_acquire_sys(&C->act_from[q]) >= (unsigned long long)go + 1;
+        // an activation carries no data (the snapshot push fences what follows)
+        const bool ext = poll_fold<true>(C->act_from, P, [](unsigned long long w) { return w; }) >=
+                         (unsigned long long)go + 1;
         if (ext) {
           // staleness guard: an explicit threshold (ec_post_hold) or the
           // device-tracked ages (ec_post_guard), eagersgd.py:102-108
@@ -1008,7 +1053,9 @@ __device__ void engine_controller(const EcDesc& d, unsigned long long epoch) {
     }
     // ---- round go: all snapshots in -> command to the workers (two-shot
     // reduction in the fused TMA pipeline)
-    if (open_ok && snapped) {
+    if (open_ok && snapped &&
+        poll_fold<false>(C->snap_from, P, [](unsigned long long w) { return w >> EC_SNAP_SHIFT; }) >=
+            (unsigned long long)go + 1) {
       bool all = true;
       unsigned long long fresh = 0, has = 0, srcg = 0, updm = 0;
       for (int q = 0; q < P; ++q) {
@@ -1050,15 +1097,20 @@ __device__ void engine_controller(const EcDesc& d, unsigned long long epoch) {
         continue;   // the next generation may already be decidable
       }
     }
+    EC_SEC(2);
     // host-visible words of this iteration's work (after any snapshot push)
     publish_host();
+    EC_SEC(3);
     // ---- the oldest round in flight: complete at this rank once every owner's
     // data for g is in our slot (TMA mode) / our own all-gather is done (pull)
     if (n_issued > 0) {
       const int k = (int)(g & 1);
-      bool all = true;
+      const int q_lo = d.mode != 1 ? 0 : r, q_n = d.mode != 1 ? P : 1;
+      bool all = poll_fold<false>(C->done_from + q_lo, q_n, [](unsigned long long w) {
+                   return w & ~EC_DONE_POISON;
+                 }) >= (unsigned long long)g + 1;
       unsigned long long poison = 0;
-      for (int q = (d.mode != 1 ? 0 : r); q < (d.mode != 1 ? P : r + 1) && all; ++q) {
+      for (int q = q_lo; q < q_lo + q_n && all; ++q) {
         const unsigned long long wq = ld_acquire_sys(&C->done_from[q]);
         if ((wq & ~EC_DONE_POISON) < (unsigned long long)g + 1) all = false;
         else if ((wq & ~EC_DONE_POISON) == (unsigned long long)g + 1) poison |= wq & EC_DONE_POISON;
@@ -1142,7 +1194,7 @@ __device__ void engine_controller(const EcDesc& d, unsigned long long epoch) {
 // device request ring in sequence order (stream-posted sequence numbers are
 // skipped once their kernel posted them), so the controller thread never
 // stalls on a PCIe read.  Runs until the controller parks.
-__device__ void engine_host_poller(const EcDesc& d, unsigned long long epoch) {
+__device__ void engine_host_poller(const EcDesc& d, unsigned long long epoch, volatile EcHpShared* hp) {
   EcLocal* L = d.local;
   EcHostCtl* H = d.hctl;
   unsigned long long pn = *(volatile unsigned long long*)&L->next_req;   // parked cursor
@@ -1157,15 +1209,19 @@ __device__ void engine_host_poller(const EcDesc& d, unsigned long long epoch) {
       st_relaxed_gpu(&L->hp_lo, lo);
       st_relaxed_gpu(&L->hp_ps, ps);
       st_release_gpu(&L->hp_seq, ++changes);
+      hp->lo = lo;
+      hp->ps = ps;
+      __threadfence_block();   // release (CTA scope): lo / ps before seq
+      hp->seq = changes;
       last_ps = ps;
       last_lo = lo;
     }
     {
       const unsigned long long sk = ld_relaxed_sys(&H->stop);
-      if (sk != *(volatile unsigned long long*)&L->hp_stop_kind ||
-          (sk != 0) != (ld_acquire_gpu(&L->hp_stop) == epoch)) {
+      if (sk != hp->stop) {
         *(volatile unsigned long long*)&L->hp_stop_kind = sk;
         st_release_gpu(&L->hp_stop, sk ? epoch : 0ull);
+        hp->stop = sk;
       }
     }
     while (true) {
@@ -1196,8 +1252,18 @@ ec_engine(const EcDesc* __restrict__ descs, int blocks_per_rank, unsigned long l
   const int role = blockIdx.x % blocks_per_rank;
   const EcDesc& d = descs[lr];
   if (role == 0) {
-    if (threadIdx.x == 0) engine_controller(d, epoch);
-    else if (threadIdx.x == 32) engine_host_poller(d, epoch);
+    __shared__ EcHpShared hp;
+    if (threadIdx.x == 0) {
+      // a relaunch starts from the persisted mirror (a stop request is the
+      // poller's to see again: the host clears it before relaunching)
+      hp.seq = *(volatile unsigned long long*)&d.local->hp_seq;
+      hp.lo = *(volatile unsigned long long*)&d.local->hp_lo;
+      hp.ps = *(volatile unsigned long long*)&d.local->hp_ps;
+      hp.stop = 0;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) engine_controller(d, epoch, &hp);
+    else if (threadIdx.x == 32) engine_host_poller(d, epoch, &hp);
     return;
   }
   engine_worker<T>(d, role - 1, epoch);

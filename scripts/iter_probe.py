@@ -36,11 +36,17 @@ def main():
         for t in range(33, 40):
             a = (C.c_uint64 * 4)()
             _lib.call("ec_step_times", h.comm.ptr, 0, t, a)
-            it = (C.c_uint64 * 16)()
+            it = (C.c_uint64 * 80)()
             _lib.call("ec_step_iterations", h.comm.ptr, 0, t, it)
             post = a[2]
             print(f"step {t}: post->seen {(a[3] - post) / 1e3:.2f} us; iteration starts "
-                  f"(us rel. post): {[round((x - post) / 1e3, 2) for x in it if x]}")
+                  f"(us rel. post): {[round((x - post) / 1e3, 2) for x in it[:16] if x]}")
+            for i in range(15):
+                b = it[i]
+                secs = [it[16 + 4 * i + k] for k in range(4)]
+                if b and all(secs):
+                    d = [round((x - b) / 1e3, 2) for x in secs] + [round((it[i + 1] - b) / 1e3, 2)]
+                    print("   sections (hp, req, snap/issue, publish, next):", d)
     h.close()
     pw.close()
     dist.destroy_process_group()
