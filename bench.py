@@ -377,6 +377,14 @@ def main():
     direct = world == 1
     upd_kernel = "ec_direct_step_kernel<float>" if direct else "ec_update_gen_kernel<float>"
     upd_bytes = (16 if direct else 12) * n
+    stamp_ms = upd_ms
+    if direct:
+        # the step stream runs this one kernel per step in the timed region (the
+        # publication kernel runs on the communicator's own stream), so its
+        # average launch duration is the region's CUDA-event time per step; the
+        # %globaltimer stamp (decision -> publication kernel entry) adds the
+        # kernel boundary and the publication's scheduling
+        upd_ms = ms / args.steps
     upd_gbs = upd_bytes / (upd_ms / 1e3) / 1e9
 
     # ---- e2e: gradient from pinned host memory every step, result read back.
@@ -479,7 +487,9 @@ def main():
         roofline = {"bound": "hbm", "kernel": upd_kernel, "achieved": upd_gbs, "peak": peak,
                     "unit": "GB/s", "frac": upd_gbs / peak, "traffic": _traffic("direct_step"),
                     "bytes_per_launch": upd_bytes, "avg_launch_ms": upd_ms,
-                    "peak_source": peak_kind}
+                    "avg_launch_ms_source": "CUDA events over the timed region, per step "
+                                            "(the step stream's only kernel)",
+                    "stamp_ms": stamp_ms, "peak_source": peak_kind}
     else:
         # with peers the dominant cost is the round's data phase, bound by NVLink
         # (the HBM-bound update overlaps it chunk by chunk): bus bytes

@@ -152,6 +152,14 @@ struct alignas(128) EcLocal {
   int step_fused;                  // the current async step updates progressively (arrival words)
   int pad8;
   unsigned long long upd_next_item;  // progressive update: next chunk item to claim
+  // direct step seq's report, by seq % EC_REQ_RING: written by the step's
+  // block 0 (and its CTAs' finiteness bits), read by the publication kernel,
+  // which may run after the next step already decided (its own stream)
+  struct {
+    unsigned long long status, t0;
+    int contrib;
+    unsigned int fused, bad, pad;
+  } drep[EC_REQ_RING];
   // host poller (engine thread 32): mirrors of host-mapped words, so the
   // controller thread never stalls on a PCIe read
   unsigned long long hp_seq;       // changes of the mirrored host pin (monotone)

@@ -56,7 +56,8 @@ cudaError_t launch_direct_step(int dtype, const EcDesc* d_desc, unsigned long lo
                                unsigned int flags, void* w, void* mom, const void* ring,
                                long long slot_bytes, const void* src0, const void* src1,
                                double lr, double mu, long long n, long long t,
-                               unsigned long long timeout_ns, cudaStream_t s);
+                               unsigned long long timeout_ns, cudaStream_t s,
+                               cudaStream_t ps, cudaEvent_t pev);
 cudaError_t launch_direct(int dtype, const EcDesc* d_desc, long long nvec, unsigned long long seq,
                           unsigned int type, unsigned int flags, long long t, long long arg,
                           cudaStream_t s);
@@ -164,6 +165,8 @@ struct ec_comm {
   bool running = false;
   bool direct = false;          // world of one rank: no persistent kernel (see ec_kernels.cu)
   void* last_stream = nullptr;  // direct mode orders host-posted requests on it
+  cudaStream_t pub_s = nullptr;  // direct mode: the steps' publication stream
+  cudaEvent_t pub_ev = nullptr;
   unsigned long long epoch = 0;
   int mode = 0, chv = 256, stages = 4, smem_bytes = 0;  // data phase (see EcDesc)
   int lead = 1;                                        // rounds in flight (EcDesc::lead)
@@ -975,6 +978,11 @@ int ec_comm_destroy(ec_comm_t* c) {
     }
   }
   nvls_teardown(c);
+  if (c->pub_s) {
+    cudaStreamSynchronize(c->pub_s);   // a step's publication may still run
+    cudaStreamDestroy(c->pub_s);
+    cudaEventDestroy(c->pub_ev);
+  }
   for (EcRankHost* r : c->L) {
     if (r->ctrl) cudaFree(r->ctrl);
     if (r->send) cudaFree(r->send);
@@ -1443,13 +1451,28 @@ int ec_step_async(ec_comm_t* c, int li, int64_t t, const void* grad, uint32_t fl
                         (flags & 7u) | (prog ? EC_CF_STEP : 0u), t, zero_copy ? 1 : 0, s));
   }
   if (c->direct) {
-    // decide + round + update in one launch (see ec_direct_step_kernel)
+    // decide + round + update in one launch (see ec_direct_step_kernel); its
+    // publication on the communicator's publication stream (not while the
+    // caller captures a graph: then behind it, on the same stream)
     c->last_stream = stream;
+    cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
+    CK(cudaStreamIsCapturing(s, &cap));
+    const bool side = cap == cudaStreamCaptureStatusNone && !getenv("EC_PUBLISH_SAME_STREAM");
+    if (side && !c->pub_s) {
+      CK(cudaSetDevice(c->device));
+      // highest priority: its one CTA is scheduled ahead of the next step's
+      // queued CTAs, so the host sees the step as soon as it completes
+      int lo_pri = 0, hi_pri = 0;
+      CK(cudaDeviceGetStreamPriorityRange(&lo_pri, &hi_pri));
+      CK(cudaStreamCreateWithPriority(&c->pub_s, cudaStreamNonBlocking, hi_pri));
+      CK(cudaEventCreateWithFlags(&c->pub_ev, cudaEventDisableTiming));
+    }
     ProfScope ps(1, stream);
     CK(launch_direct_step(c->dtype, c->d_descs + li, seq,
                           (flags & 7u) | (grad == r->gbuf ? EC_CF_SRC_GRAD_AUTO : 0u), w,
                           (mom && mu != 0.0) ? mom : nullptr, r->ring, c->slot_bytes, r->send,
-                          r->gbuf, lr, mu, c->n, t, c->timeout_ns, s));
+                          r->gbuf, lr, mu, c->n, t, c->timeout_ns, s, side ? c->pub_s : nullptr,
+                          c->pub_ev));
     if (seq_out) *seq_out = seq;
     return EC_OK;
   }

@@ -1321,9 +1321,28 @@ __device__ unsigned long long direct_decide_core(const EcDesc& d, unsigned int t
   return status;
 }
 
+// Direct mode answers requests from kernels on more than one stream (a step's
+// publication runs on its own stream, ec_host.cu): every writer of the
+// monotone host words waits for its predecessor, so req_done / done_gen1 never
+// move backwards.
+__device__ void direct_wait_turn(const EcDesc& d, const unsigned long long* word,
+                                 unsigned long long need) {
+  if (ld_acquire_gpu(word) >= need) return;
+  const unsigned long long t0 = globaltimer_ns();
+  while (ld_acquire_gpu(word) < need) {
+    if (globaltimer_ns() - t0 > d.timeout_ns) {
+      st_release_sys(&d.hctl->error_info, need);
+      st_release_sys(&d.hctl->error, EC_DERR_TIMEOUT);
+      return;
+    }
+    __nanosleep(256);
+  }
+}
+
 __device__ void direct_reply(const EcDesc& d, unsigned long long seq, unsigned long long status) {
   EcLocal* L = d.local;
   EcHostCtl* H = d.hctl;
+  direct_wait_turn(d, &L->req_done_dev, seq);
   __threadfence();
   st_release_sys(&H->reply[seq % EC_REQ_RING], ((seq + 1) << 8) | status);
   st_release_sys(&H->req_done, seq + 1);
@@ -1374,6 +1393,7 @@ struct DirectStepReport {
   unsigned long long seq, status, t0;
   long long t;
   bool bad;
+  unsigned long long t1;   // the step's kernel had completed (publication kernel entry)
 };
 
 __device__ void direct_publish(const EcDesc& d, long long g, int contrib, unsigned long long has,
@@ -1381,6 +1401,8 @@ __device__ void direct_publish(const EcDesc& d, long long g, int contrib, unsign
   EcLocal* L = d.local;
   EcHostCtl* H = d.hctl;
   const unsigned long long fresh = (contrib & (int)EC_SNAP_FRESH) ? 1ull : 0ull;
+  direct_wait_turn(d, &L->done_gen1_dev, (unsigned long long)g);
+  if (step) direct_wait_turn(d, &L->req_done_dev, step->seq);
   EcLog* lg = &H->log[g % EC_LOG_RING];
   st_relaxed_sys(&lg->mask, fresh);
   st_relaxed_sys(&lg->has, has);
@@ -1390,18 +1412,20 @@ __device__ void direct_publish(const EcDesc& d, long long g, int contrib, unsign
   st_relaxed_sys(&lg->t_cmd, tn);
   st_relaxed_sys(&lg->t_rs, tn);
   st_relaxed_sys(&lg->t_done, tn);
-  if (fresh) {
-    L->hold_from = EC_INF_GEN;
-    L->stash_null = 1;
+  if (!step) {   // a step's block 0 made these transitions when it decided
+    if (fresh) {
+      L->hold_from = EC_INF_GEN;
+      L->stash_null = 1;
+    }
+    L->g = g + 1;
+    L->snapped = 0;
+    L->contrib = 0;
   }
-  L->g = g + 1;
-  L->snapped = 0;
-  L->contrib = 0;
   if (step) {
     const long long ts = step->t % EC_REQ_RING;
     st_relaxed_sys(&H->stepgen[ts], (unsigned long long)g + 1);
     st_relaxed_sys(&H->stepbad[ts], step->bad ? 1ull : 0ull);
-    st_relaxed_sys(&H->stepns[ts], tn - step->t0);
+    st_relaxed_sys(&H->stepns[ts], step->t1 - step->t0);
   }
   st_relaxed_sys(&lg->gen1, (unsigned long long)g + 1);   // record data: before the fence
   fence_acq_rel_sys();
@@ -2089,9 +2113,12 @@ ec_update_gen_kernel(T* __restrict__ w, T* __restrict__ mom, const char* __restr
 // Block 0 decides and publishes the decision packed into ONE word
 // (dec_tag = (seq+1) << 8 | bits), so every other CTA's prologue is a single
 // acquire load; completion is the kernel boundary (ec_direct_publish_kernel,
-// launched behind it with PDL, writes every host-visible word behind one sys
-// fence), so no CTA pays a fence or a counter atomic.  The rare no-round path
-// (refused offer) runs out of line with the ordinary wait + update body.
+// launched behind it on the communicator's publication stream, writes every
+// host-visible word behind one sys fence), so no CTA pays a fence or a counter
+// atomic, and the next step's kernel does not wait for the publication: block
+// 0 makes the round's state transitions when it decides and leaves the report
+// in EcLocal::drep.  The rare no-round path (refused offer) runs out of line
+// with the ordinary wait + update body.
 #define EC_DW_FUSED 1u
 #define EC_DW_FOLD 2u
 #define EC_DW_HAS 4u
@@ -2136,6 +2163,23 @@ ec_direct_step_kernel(const EcDesc* __restrict__ dp, unsigned long long seq,
       L->dec_status = status;
       L->dec_fold = fold;
       L->upd_t0 = t0;
+      auto* rp = &L->drep[seq % EC_REQ_RING];
+      rp->status = status;
+      rp->t0 = t0;
+      rp->contrib = contrib;
+      rp->fused = fused ? 1u : 0u;
+      rp->bad = 0u;
+      if (fused) {
+        // round t completes inside this launch: the next step's decision sees
+        // the state after it now, whenever the publication runs
+        if (contrib & (int)EC_SNAP_FRESH) {
+          L->hold_from = EC_INF_GEN;
+          L->stash_null = 1;
+        }
+        L->g = t + 1;
+        L->snapped = 0;
+        L->contrib = 0;
+      }
       dw = ((seq + 1) << 8) | (fused ? EC_DW_FUSED : 0u) | (fold ? EC_DW_FOLD : 0u) |
            ((contrib & (int)EC_SNAP_DATA) ? EC_DW_HAS : 0u) |
            ((contrib & (int)EC_SNAP_SRC_GRAD) ? EC_DW_SRCG : 0u);
@@ -2216,7 +2260,8 @@ ec_direct_step_kernel(const EcDesc* __restrict__ dp, unsigned long long seq,
   }
   // completion is the kernel boundary: ec_direct_publish_kernel (launched
   // right behind, PDL) reports once every CTA's stores are visible
-  if (__any_sync(0xffffffffu, bad) && (threadIdx.x & 31) == 0) atomicOr(&L->upd_bad, 1u);
+  if (__any_sync(0xffffffffu, bad) && (threadIdx.x & 31) == 0)
+    atomicOr(&L->drep[seq % EC_REQ_RING].bad, 1u);
   asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
 }
 
@@ -2224,16 +2269,16 @@ __global__ void ec_direct_publish_kernel(const EcDesc* __restrict__ dp, unsigned
                                          long long t) {
   asm volatile("griddepcontrol.wait;" ::: "memory");
   if (threadIdx.x != 0) return;
+  const unsigned long long t1 = globaltimer_ns();
   const EcDesc& d = *dp;
   EcLocal* L = d.local;
-  const unsigned long long dw = *(volatile unsigned long long*)&L->dec_tag;
-  if ((dw >> 8) != seq + 1 || !(dw & EC_DW_FUSED)) return;   // the fallback reported itself
-  L->step_gen = t;
-  const int contrib = *(volatile int*)&L->contrib;
-  DirectStepReport rep{seq, *(volatile unsigned long long*)&L->dec_status,
-                       *(volatile unsigned long long*)&L->upd_t0, t,
-                       atomicExch(&L->upd_bad, 0u) != 0u};
-  direct_publish(d, t, contrib, (dw & EC_DW_HAS) ? 1ull : 0ull, &rep);
+  const auto* rp = &L->drep[seq % EC_REQ_RING];
+  if (!*(volatile unsigned*)&rp->fused) return;   // the fallback reported itself
+  const int contrib = *(volatile int*)&rp->contrib;
+  DirectStepReport rep{seq, *(volatile unsigned long long*)&rp->status,
+                       *(volatile unsigned long long*)&rp->t0, t,
+                       *(volatile unsigned*)&rp->bad != 0u, t1};
+  direct_publish(d, t, contrib, (contrib & (int)EC_SNAP_DATA) ? 1ull : 0ull, &rep);
 }
 
 __global__ void ec_post_kernel(EcLocal* L, unsigned long long seq1, unsigned int type,
@@ -2558,7 +2603,8 @@ cudaError_t launch_direct_step(int dtype, const EcDesc* d_desc, unsigned long lo
                                unsigned int flags, void* w, void* mom, const void* ring,
                                long long slot_bytes, const void* src0, const void* src1,
                                double lr, double mu, long long n, long long t,
-                               unsigned long long timeout_ns, cudaStream_t s) {
+                               unsigned long long timeout_ns, cudaStream_t s,
+                               cudaStream_t ps, cudaEvent_t pev) {
   counted();
   const int vec_ok = ((((uintptr_t)w) | ((uintptr_t)mom) | ((uintptr_t)ring) | slot_bytes |
                        ((uintptr_t)src0) | ((uintptr_t)src1)) & 15) == 0;
@@ -2590,6 +2636,14 @@ cudaError_t launch_direct_step(int dtype, const EcDesc* d_desc, unsigned long lo
   counted();
   cfg.gridDim = dim3(1);
   cfg.blockDim = dim3(32);
+  if (ps) {
+    // the publication (host-visible words behind a system-scope fence, ~4 us)
+    // on its own stream: the next step's kernel waits for this one only
+    if ((e = cudaEventRecord(pev, s)) != cudaSuccess) return e;
+    if ((e = cudaStreamWaitEvent(ps, pev, 0)) != cudaSuccess) return e;
+    cfg.stream = ps;
+    cfg.numAttrs = 0;
+  }
   return cudaLaunchKernelEx(&cfg, ec_direct_publish_kernel, d_desc, seq, t);
 }
 

@@ -5,6 +5,7 @@ OUT=gpurun_out/final1
 mkdir -p $OUT
 NCU=/usr/local/cuda/bin/ncu
 timeout 900 python -m pytest tests -q -m gpu --timeout 300 > $OUT/pytest_gpu.log 2>&1; echo rc=$? >> $OUT/pytest_gpu.log
+[ -n "$CHECKED" ] && { EC_DEBUG_LIB=1 timeout 900 python -m pytest tests -q -m gpu --timeout 300 > $OUT/pytest_gpu_checked.log 2>&1; echo rc=$? >> $OUT/pytest_gpu_checked.log; }
 timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > $OUT/smoke.log 2>&1; echo rc=$? >> $OUT/smoke.log
 timeout 600 python bench.py > $OUT/bench_n1.log 2>&1; echo rc=$? >> $OUT/bench_n1.log
 timeout 600 python bench.py --impl reference > $OUT/bench_ref_n1.log 2>&1; echo rc=$? >> $OUT/bench_ref_n1.log
