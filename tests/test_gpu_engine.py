@@ -530,6 +530,62 @@ def test_direct_fused_step_matches_oracle(element, mu):
     world.close()
 
 
+def test_direct_publication_stream_keeps_host_words_in_order():
+    """World of one: a step's publication (replies, log, done_gen1) runs on the
+    communicator's own stream, possibly after the next step already decided.
+    Interleave pipelined async steps with plain rounds posted behind them
+    (whose decide / round kernels answer on the caller's stream while earlier
+    publications may still be pending) and a burst of 40 async steps: every
+    reply and generation is reported in order, each plain round's result is
+    its contribution, and w is the oracle's bits."""
+    from collections import deque
+
+    from paper_1908_04207_b200 import finish_step, train_step_async
+    n, lr = 200_003, 0.05
+    plan = ["a"] * 3 + ["r"] + ["a"] * 2 + ["r", "r"] + ["a"] * 40 + ["r"]
+    rng = np.random.default_rng(33)
+    grads = rng.standard_normal((len(plan), n)).astype(np.float32)
+    w0 = rng.standard_normal(n).astype(np.float32)
+    world = EmulatedWorld(1)
+    h = AllreduceHandle(CollectiveConfig(p=1, flavor="solo", vector_len=n, element="f4"), 0, world)
+    st = TrainState.fresh(w0, lr, rank=0, tau=None)
+    gd = torch.as_tensor(grads, device="cuda")
+    bucket = h.grad_buffer()
+    pend, gens = deque(), []
+    for t, kind in enumerate(plan):
+        if kind == "a":
+            bucket.copy_(gd[t])
+            pend.append(train_step_async(st, h, bucket, all_arrive=True))
+            if len(pend) > 3:
+                gens.append(finish_step(st, h, pend.popleft())[2])
+        else:
+            # a plain round right behind pending (unreconciled) async steps,
+            # no update; rounds are driven in order, so round t - 1 is done
+            h.wait_blocking(t - 1)
+            assert h._contribute(t, gd[t], fresh=True, activate=True)
+            gen, res = h.wait_blocking(t)
+            assert gen == t and res.included == 1 and res.nap == 1
+            assert _np(res.u).tobytes() == grads[t].tobytes()
+            while pend:
+                gens.append(finish_step(st, h, pend.popleft())[2])
+            gens.append(gen)
+            st.t = t + 1
+    while pend:
+        gens.append(finish_step(st, h, pend.popleft())[2])
+    torch.cuda.synchronize()
+    assert gens == list(range(len(plan)))
+    w = w0.copy()
+    for t, kind in enumerate(plan):
+        if kind == "a":
+            u, _, _ = R.allreduce_round([grads[t]], [True], np.float32)
+            w = R.sgd_update(w, u, lr)
+    assert st.w.cpu().numpy().tobytes() == w.tobytes()
+    gen, res = h.latest_result()
+    assert gen == len(plan) - 1 and _np(res.u).tobytes() == grads[-1].tobytes()
+    assert h.done_generation == len(plan) - 1
+    world.close()
+
+
 def test_direct_zero_copy_folds_into_a_pending_stash():
     """World of one: a zero-copy step that meets a pending (accepted, not yet
     reduced) stash folds the gradient into it inside the step kernel (no fold
