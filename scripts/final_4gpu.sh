@@ -12,4 +12,5 @@ timeout 900 $TR --master-port 29614 tests/mp_check.py > $OUT/mp_check4.log 2>&1;
 EC_RANKS_PER_GPU=2 timeout 1500 python -m torch.distributed.run --nnodes=1 --nproc-per-node=8 \
   --master-addr 127.0.0.1 --master-port 29615 tests/mp_check.py > $OUT/mp_check_p8.log 2>&1
 echo rc=$? >> $OUT/mp_check_p8.log
+timeout 1200 python -m pytest tests -q -m gpu --timeout 600 > $OUT/pytest_gpu_4gpu.log 2>&1; echo rc=$? >> $OUT/pytest_gpu_4gpu.log
 echo done
