@@ -160,6 +160,13 @@ struct alignas(128) EcLocal {
     int contrib;
     unsigned int fused, bad, pad;
   } drep[EC_REQ_RING];
+  // async step t's report (P > 1), by t % EC_REQ_RING: written by the update
+  // kernel's last CTA, made host-visible by ec_step_publish_kernel on the
+  // rank's publication stream
+  struct {
+    unsigned long long ns;
+    unsigned int bad, pad;
+  } srep[EC_REQ_RING];
   // host poller (engine thread 32): mirrors of host-mapped words, so the
   // controller thread never stalls on a PCIe read
   unsigned long long hp_seq;       // changes of the mirrored host pin (monotone)

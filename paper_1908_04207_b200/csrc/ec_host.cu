@@ -14,6 +14,7 @@
 #include <atomic>
 #include <chrono>
 #include <map>
+#include <memory>
 #include <mutex>
 #include <string>
 #include <thread>
@@ -167,6 +168,8 @@ struct ec_comm {
   void* last_stream = nullptr;  // direct mode orders host-posted requests on it
   cudaStream_t pub_s = nullptr;  // direct mode: the steps' publication stream
   cudaEvent_t pub_ev = nullptr;
+  cudaEvent_t pub_join_ev = nullptr;
+  bool pub_used = false;         // a step published on pub_s
   unsigned long long epoch = 0;
   int mode = 0, chv = 256, stages = 4, smem_bytes = 0;  // data phase (see EcDesc)
   int lead = 1;                                        // rounds in flight (EcDesc::lead)
@@ -197,6 +200,26 @@ static int check_li(ec_comm_t* c, int li) {
   if (li < 0 || li >= c->n_local) return fail(EC_E_ARG, "local index %d out of range", li);
   return EC_OK;
 }
+
+// a stream for host-visible publications, highest priority: its one-warp
+// kernels are scheduled ahead of the next step's queued CTAs
+static int make_pub_stream(ec_comm_t* c, cudaStream_t* s, cudaEvent_t* ev) {
+  int lo_pri = 0, hi_pri = 0;
+  CK(cudaSetDevice(c->device));
+  CK(cudaDeviceGetStreamPriorityRange(&lo_pri, &hi_pri));
+  CK(cudaStreamCreateWithPriority(s, cudaStreamNonBlocking, hi_pri));
+  CK(cudaEventCreateWithFlags(ev, cudaEventDisableTiming));
+  return EC_OK;
+}
+
+// publications go to their own stream unless the caller captures a graph (the
+// side stream would leave the capture unjoined) or EC_PUBLISH_SAME_STREAM is set
+static bool pub_side_ok(cudaStream_t s) {
+  cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
+  if (cudaStreamIsCapturing(s, &cap) != cudaSuccess) return false;
+  return cap == cudaStreamCaptureStatusNone && !getenv("EC_PUBLISH_SAME_STREAM");
+}
+
 
 static int device_error(EcRankHost* r) {
   unsigned long long e = aload(&r->h->error);
@@ -615,7 +638,8 @@ int ec_comm_create(int world_size, int rank_lo, int n_local, int device, int64_t
       ec_comm_destroy(c);
       return fail(EC_E_CUDA, "cudaHostGetDevicePointer: %s", cudaGetErrorString(e));
     }
-    EcLocal init;
+    std::unique_ptr<EcLocal> initp(new EcLocal());   // ~100 KB: not on the stack
+    EcLocal& init = *initp;
     memset(&init, 0, sizeof(init));
     init.hold_from = EC_INF_GEN;
     init.contributed_round = -1;
@@ -642,6 +666,11 @@ int ec_comm_create(int world_size, int rank_lo, int n_local, int device, int64_t
   if (cudaStreamCreateWithPriority(&c->es, cudaStreamNonBlocking, hi) != cudaSuccess) {
     ec_comm_destroy(c);
     return fail(EC_E_CUDA, "engine stream creation failed");
+  }
+  // the direct steps' publication stream (a world of one has no engine)
+  if (c->direct && make_pub_stream(c, &c->pub_s, &c->pub_ev) != EC_OK) {
+    ec_comm_destroy(c);
+    return fail(EC_E_CUDA, "publication stream creation failed");
   }
   *out = c;
   return EC_OK;
@@ -784,6 +813,17 @@ static int upload_descs(ec_comm_t* c) {
     astore(&r->h->stop, 0ull);
   }
   CK(cudaMemcpy(c->d_descs, d.data(), sizeof(EcDesc) * c->n_local, cudaMemcpyHostToDevice));
+  return EC_OK;
+}
+
+// direct mode: a host-posted request is answered by kernels on the caller's
+// stream, which must follow every step publication already queued on the
+// publication stream (replies and done generations are written in order)
+static int order_after_pub(ec_comm_t* c, cudaStream_t s) {
+  if (!c->pub_used) return EC_OK;
+  if (!c->pub_join_ev) CK(cudaEventCreateWithFlags(&c->pub_join_ev, cudaEventDisableTiming));
+  CK(cudaEventRecord(c->pub_join_ev, c->pub_s));
+  CK(cudaStreamWaitEvent(s, c->pub_join_ev, 0));
   return EC_OK;
 }
 
@@ -982,6 +1022,7 @@ int ec_comm_destroy(ec_comm_t* c) {
     cudaStreamSynchronize(c->pub_s);   // a step's publication may still run
     cudaStreamDestroy(c->pub_s);
     cudaEventDestroy(c->pub_ev);
+    if (c->pub_join_ev) cudaEventDestroy(c->pub_join_ev);
   }
   for (EcRankHost* r : c->L) {
     if (r->ctrl) cudaFree(r->ctrl);
@@ -991,6 +1032,7 @@ int ec_comm_destroy(ec_comm_t* c) {
     if (r->local) cudaFree(r->local);
     if (r->forced) cudaFree(r->forced);
     if (r->unpin_ev) cudaEventDestroy(r->unpin_ev);
+
     if (r->h) cudaFreeHost(r->h);
     delete r;
   }
@@ -1035,6 +1077,7 @@ int ec_comm_set_generation(ec_comm_t* c, int li, int64_t gen, int stash_pending,
   if (gen < 0) return fail(EC_E_ARG, "generation must be >= 0");
   EcRankHost* r = c->L[li];
   CK(cudaSetDevice(c->device));
+  if (c->pub_s) CK(cudaStreamSynchronize(c->pub_s));   // no step publication still queued
   // the engine's own stream is idle while it is parked
   cudaError_t e = launch_set_generation(r->local, r->hd, gen, stash_pending ? 1 : 0,
                                         contributed_round, c->es);
@@ -1106,6 +1149,7 @@ static int host_post(ec_comm_t* c, int li, unsigned type, unsigned flags, long l
   if ((rc = reserve_seq(c, r, &seq))) return rc;
   if (c->direct) {
     if (!c->running && (rc = ec_comm_start(c))) return rc;
+    if ((rc = order_after_pub(c, (cudaStream_t)c->last_stream))) return rc;
     CK(launch_direct(c->dtype, c->d_descs + li, c->n / (16 / c->elem), seq, type, flags, t, arg,
                      (cudaStream_t)c->last_stream));
     if (seq_out) *seq_out = seq;
@@ -1134,6 +1178,7 @@ int ec_post_contribute(ec_comm_t* c, int li, int64_t t, uint32_t flags, void* st
   if (c->direct) {
     if (!c->running && (rc = ec_comm_start(c))) return rc;
     c->last_stream = stream;
+    if ((rc = order_after_pub(c, (cudaStream_t)stream))) return rc;
     CK(launch_direct(c->dtype, c->d_descs + li, c->n / (16 / c->elem), seq, EC_REQ_CONTRIB,
                      flags & 7u, t, 0, (cudaStream_t)stream));
     if (seq_out) *seq_out = seq;
@@ -1455,18 +1500,9 @@ int ec_step_async(ec_comm_t* c, int li, int64_t t, const void* grad, uint32_t fl
     // publication on the communicator's publication stream (not while the
     // caller captures a graph: then behind it, on the same stream)
     c->last_stream = stream;
-    cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
-    CK(cudaStreamIsCapturing(s, &cap));
-    const bool side = cap == cudaStreamCaptureStatusNone && !getenv("EC_PUBLISH_SAME_STREAM");
-    if (side && !c->pub_s) {
-      CK(cudaSetDevice(c->device));
-      // highest priority: its one CTA is scheduled ahead of the next step's
-      // queued CTAs, so the host sees the step as soon as it completes
-      int lo_pri = 0, hi_pri = 0;
-      CK(cudaDeviceGetStreamPriorityRange(&lo_pri, &hi_pri));
-      CK(cudaStreamCreateWithPriority(&c->pub_s, cudaStreamNonBlocking, hi_pri));
-      CK(cudaEventCreateWithFlags(&c->pub_ev, cudaEventDisableTiming));
-    }
+    const bool side = pub_side_ok(s);
+    if (side && !c->pub_s && (rc = make_pub_stream(c, &c->pub_s, &c->pub_ev))) return rc;
+    if (side) c->pub_used = true;
     ProfScope ps(1, stream);
     CK(launch_direct_step(c->dtype, c->d_descs + li, seq,
                           (flags & 7u) | (grad == r->gbuf ? EC_CF_SRC_GRAD_AUTO : 0u), w,

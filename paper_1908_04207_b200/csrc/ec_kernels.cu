@@ -2016,7 +2016,7 @@ __device__ __forceinline__ void update_gen_body(T* __restrict__ w, T* __restrict
                                                 long long n, int vec_ok, EcHostCtl* H, long long t,
                                                 unsigned long long timeout_ns, unsigned long long seq1,
                                                 T* __restrict__ stash, const T* __restrict__ gbuf,
-                                                const EcDesc* __restrict__ dp) {
+                                                const EcDesc* __restrict__ dp, int pub_side = 0) {
   __shared__ long long s_gen;
   __shared__ int s_late, s_fusedu;
   if (threadIdx.x == 0) {
@@ -2077,12 +2077,21 @@ __device__ __forceinline__ void update_gen_body(T* __restrict__ w, T* __restrict
         if (tbad) atomicOr(&L->upd_bad, 1u);
       }
       if (s_late) *(volatile int*)&L->stash_null = 0;
-      st_relaxed_sys(&H->stepbad[t % EC_REQ_RING], atomicExch(&L->upd_bad, 0u) ? 1ull : 0ull);
+      const unsigned int sbad = atomicExch(&L->upd_bad, 0u) ? 1u : 0u;
       const unsigned long long t1 = globaltimer_ns();
       L->tl[t & 63][0] = t1;
       st_release_gpu(&L->pin_dev, ~0ull);  // every CTA has read the slot: unpin
-      st_relaxed_sys(&H->stepns[t % EC_REQ_RING], t1 - *(volatile unsigned long long*)&L->upd_t0);
-      st_release_sys(&H->steptag[t % EC_REQ_RING], (unsigned long long)t + 1);
+      const unsigned long long sns = t1 - *(volatile unsigned long long*)&L->upd_t0;
+      if (pub_side) {
+        // a direct step's out-of-line path: its publication kernel (own
+        // stream, after the earlier steps' publications) reports it
+        L->srep[t % EC_REQ_RING].ns = sns;
+        L->srep[t % EC_REQ_RING].bad = sbad;
+      } else {
+        st_relaxed_sys(&H->stepbad[t % EC_REQ_RING], sbad);
+        st_relaxed_sys(&H->stepns[t % EC_REQ_RING], sns);
+        st_release_sys(&H->steptag[t % EC_REQ_RING], (unsigned long long)t + 1);
+      }
     }
   }
 }
@@ -2138,9 +2147,12 @@ __device__ __noinline__ void direct_step_fallback(const EcDesc& d, unsigned long
     const long long nth0 = (long long)gridDim.x * blockDim.x;
     for (long long e = tid0; e < n; e += nth0) stash[e] = Ops<T>::add(stash[e], gbuf[e]);
   }
-  if (blockIdx.x == 0 && threadIdx.x == 0) direct_reply(d, seq, status);
+  // the reply and the step's report come from ec_direct_publish_kernel (this
+  // kernel never waits for an earlier publication: its CTAs would hold every
+  // SM slot that publication needs)
+  (void)status;
   update_gen_body<T, MOM>(w, mom, d.ring[d.rank], d.slot_bytes, d.R, L, lr, mu, n, vec_ok, d.hctl,
-                          t, timeout_ns, 0, stash, gbuf, &d);
+                          t, timeout_ns, 0, stash, gbuf, &d, 1);
 }
 
 template <typename T, bool MOM>
@@ -2273,7 +2285,22 @@ __global__ void ec_direct_publish_kernel(const EcDesc* __restrict__ dp, unsigned
   const EcDesc& d = *dp;
   EcLocal* L = d.local;
   const auto* rp = &L->drep[seq % EC_REQ_RING];
-  if (!*(volatile unsigned*)&rp->fused) return;   // the fallback reported itself
+  if (!*(volatile unsigned*)&rp->fused) {
+    // the out-of-line path (no round): the offer's reply and the step report
+    // (stepgen was stored by its wait; the kernel boundary made it visible)
+    EcHostCtl* H = d.hctl;
+    const long long ts = t % EC_REQ_RING;
+    direct_wait_turn(d, &L->req_done_dev, seq);
+    st_relaxed_sys(&H->stepbad[ts], *(volatile unsigned*)&L->srep[ts].bad);
+    st_relaxed_sys(&H->stepns[ts], *(volatile unsigned long long*)&L->srep[ts].ns);
+    st_relaxed_sys(&H->reply[seq % EC_REQ_RING],
+                   ((seq + 1) << 8) | *(volatile unsigned long long*)&rp->status);
+    fence_acq_rel_sys();
+    st_relaxed_sys(&H->req_done, seq + 1);
+    st_relaxed_gpu(&L->req_done_dev, seq + 1);
+    st_relaxed_sys(&H->steptag[ts], (unsigned long long)t + 1);
+    return;
+  }
   const int contrib = *(volatile int*)&rp->contrib;
   DirectStepReport rep{seq, *(volatile unsigned long long*)&rp->status,
                        *(volatile unsigned long long*)&rp->t0, t,

@@ -586,6 +586,37 @@ def test_direct_publication_stream_keeps_host_words_in_order():
     world.close()
 
 
+def test_direct_refused_step_takes_the_out_of_line_path():
+    """World of one: a step whose offer arrives after its round already ran (a
+    plain round took generation 0) is refused; the step kernel's out-of-line
+    path applies generation 0 and keeps the zero-copy gradient in the stash,
+    and its reply / report come from the publication kernel (no wait inside
+    the step kernel).  The next step carries that gradient: u1 = 0 + (g0 + g1)."""
+    from paper_1908_04207_b200 import finish_step, train_step_async
+    n, lr = 70_001, 0.5
+    rng = np.random.default_rng(8)
+    v, g0, g1, w0 = (rng.standard_normal(n, dtype=np.float32) for _ in range(4))
+    world = EmulatedWorld(1)
+    h = AllreduceHandle(CollectiveConfig(p=1, flavor="solo", vector_len=n, element="f4"), 0, world)
+    st = TrainState.fresh(w0, lr, rank=0, tau=None)
+    assert h._contribute(0, v, fresh=True, activate=True)
+    h.wait_blocking(0)
+    bucket = h.grad_buffer()
+    bucket.copy_(torch.as_tensor(g0, device="cuda"))
+    _, res0, gen0 = finish_step(st, h, train_step_async(st, h, bucket, all_arrive=True))
+    assert gen0 == 0
+    w = w0 - np.float32(lr) * v
+    assert st.w.cpu().numpy().tobytes() == w.tobytes()
+    bucket.copy_(torch.as_tensor(g1, device="cuda"))
+    _, res1, gen1 = finish_step(st, h, train_step_async(st, h, bucket, all_arrive=True))
+    torch.cuda.synchronize()
+    u1 = np.float32(0) + (g0 + g1)
+    assert gen1 == 1 and res1.included == 1
+    assert st.w.cpu().numpy().tobytes() == (w - np.float32(lr) * u1).tobytes()
+    assert _np(h.latest_result()[1].u).tobytes() == u1.tobytes()
+    world.close()
+
+
 def test_direct_zero_copy_folds_into_a_pending_stash():
     """World of one: a zero-copy step that meets a pending (accepted, not yet
     reduced) stash folds the gradient into it inside the step kernel (no fold
