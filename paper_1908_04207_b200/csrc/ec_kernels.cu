@@ -2168,10 +2168,47 @@ ec_direct_step_kernel(const EcDesc* __restrict__ dp, unsigned long long seq,
     unsigned long long dw;
     if (blockIdx.x == 0) {
       const unsigned long long t0 = globaltimer_ns();
-      const int fold = (flags & EC_CF_SRC_GRAD_AUTO) && !*(volatile int*)&L->stash_null;
-      const unsigned long long status = direct_decide_core(d, EC_REQ_CONTRIB, flags, t, 0);
-      const int contrib = *(volatile int*)&L->contrib;
-      const int fused = *(volatile int*)&L->snapped;
+      int fold, contrib, fused;
+      unsigned long long status;
+      {
+        // direct_decide_core for an offer, from ONE batch of plain loads: every
+        // writer of these words is an earlier kernel in stream order, so they
+        // need no acquire, and the loads overlap instead of paying an L2 round
+        // trip each while every other CTA waits for the decision
+        const long long g = L->g;
+        const int stash_null = L->stash_null, snapped = L->snapped, contrib0 = L->contrib;
+        const unsigned int poison = L->poison;
+        fold = (flags & EC_CF_SRC_GRAD_AUTO) && !stash_null;
+        unsigned int fl = flags;
+        if (fl & EC_CF_SRC_GRAD_AUTO) {
+          if (stash_null) fl |= EC_CF_SRC_GRAD;
+          fl &= ~EC_CF_SRC_GRAD_AUTO;
+        }
+        if (poison) L->poison = 0u;
+        if (!(fl & EC_CF_SRC_GRAD) && stash_null) L->stash_null = 0;   // the stash holds an offer
+        contrib = contrib0;
+        fused = snapped;
+        if (poison) {
+          status = 4;
+        } else if (t < g || (t == g && snapped)) {
+          status = 2;
+          if (fl & EC_CF_SRC_GRAD) L->late_copy = 1;
+        } else if (t > g) {
+          status = 5;
+          st_release_sys(&d.hctl->error_info, (unsigned long long)t);
+          st_release_sys(&d.hctl->error, EC_DERR_ORDER);
+        } else {
+          contrib = (int)(EC_SNAP_DATA | ((fl & 1u) ? EC_SNAP_FRESH : 0ull) |
+                          ((fl & EC_CF_SRC_GRAD) ? EC_SNAP_SRC_GRAD : 0ull));
+          L->contrib = contrib;
+          L->contributed_round = t;
+          status = 1;
+          if (fl & 2u) {   // own activation: P == 1, everyone has arrived
+            L->snapped = 1;
+            fused = 1;
+          }
+        }
+      }
       L->dec_status = status;
       L->dec_fold = fold;
       L->upd_t0 = t0;
@@ -2195,8 +2232,7 @@ ec_direct_step_kernel(const EcDesc* __restrict__ dp, unsigned long long seq,
       dw = ((seq + 1) << 8) | (fused ? EC_DW_FUSED : 0u) | (fold ? EC_DW_FOLD : 0u) |
            ((contrib & (int)EC_SNAP_DATA) ? EC_DW_HAS : 0u) |
            ((contrib & (int)EC_SNAP_SRC_GRAD) ? EC_DW_SRCG : 0u);
-      __threadfence();
-      st_release_gpu(&L->dec_tag, dw);
+      st_release_gpu(&L->dec_tag, dw);   // release: every state word above first
     } else {
       while (((dw = ld_acquire_gpu(&L->dec_tag)) >> 8) != seq + 1) __nanosleep(32);
     }
