@@ -170,6 +170,11 @@ struct ec_comm {
   cudaEvent_t pub_ev = nullptr;
   cudaEvent_t pub_join_ev = nullptr;
   bool pub_used = false;         // a step published on pub_s
+  // the last host-posted request's kernels (direct mode): a step issued on
+  // another stream is ordered behind them, so its publication never waits
+  cudaEvent_t req_ev = nullptr;
+  cudaStream_t req_stream = nullptr;
+  bool req_pending = false;
   unsigned long long epoch = 0;
   int mode = 0, chv = 256, stages = 4, smem_bytes = 0;  // data phase (see EcDesc)
   int lead = 1;                                        // rounds in flight (EcDesc::lead)
@@ -827,6 +832,15 @@ static int order_after_pub(ec_comm_t* c, cudaStream_t s) {
   return EC_OK;
 }
 
+// direct mode: remember where a host-posted request's kernels went
+static int note_request(ec_comm_t* c, cudaStream_t s) {
+  if (!c->req_ev) CK(cudaEventCreateWithFlags(&c->req_ev, cudaEventDisableTiming));
+  CK(cudaEventRecord(c->req_ev, s));
+  c->req_stream = s;
+  c->req_pending = true;
+  return EC_OK;
+}
+
 static inline void touch(ec_comm_t* c) { c->last_api_ns.store(now_ns(), std::memory_order_relaxed); }
 
 // (re)launch the persistent engine for a new epoch; caller holds live_mu
@@ -1023,6 +1037,7 @@ int ec_comm_destroy(ec_comm_t* c) {
     cudaStreamDestroy(c->pub_s);
     cudaEventDestroy(c->pub_ev);
     if (c->pub_join_ev) cudaEventDestroy(c->pub_join_ev);
+    if (c->req_ev) cudaEventDestroy(c->req_ev);
   }
   for (EcRankHost* r : c->L) {
     if (r->ctrl) cudaFree(r->ctrl);
@@ -1152,6 +1167,7 @@ static int host_post(ec_comm_t* c, int li, unsigned type, unsigned flags, long l
     if ((rc = order_after_pub(c, (cudaStream_t)c->last_stream))) return rc;
     CK(launch_direct(c->dtype, c->d_descs + li, c->n / (16 / c->elem), seq, type, flags, t, arg,
                      (cudaStream_t)c->last_stream));
+    if ((rc = note_request(c, (cudaStream_t)c->last_stream))) return rc;
     if (seq_out) *seq_out = seq;
     return EC_OK;
   }
@@ -1181,6 +1197,7 @@ int ec_post_contribute(ec_comm_t* c, int li, int64_t t, uint32_t flags, void* st
     if ((rc = order_after_pub(c, (cudaStream_t)stream))) return rc;
     CK(launch_direct(c->dtype, c->d_descs + li, c->n / (16 / c->elem), seq, EC_REQ_CONTRIB,
                      flags & 7u, t, 0, (cudaStream_t)stream));
+    if ((rc = note_request(c, (cudaStream_t)stream))) return rc;
     if (seq_out) *seq_out = seq;
     return EC_OK;
   }
@@ -1503,6 +1520,8 @@ int ec_step_async(ec_comm_t* c, int li, int64_t t, const void* grad, uint32_t fl
     const bool side = pub_side_ok(s);
     if (side && !c->pub_s && (rc = make_pub_stream(c, &c->pub_s, &c->pub_ev))) return rc;
     if (side) c->pub_used = true;
+    if (c->req_pending && c->req_stream != s) CK(cudaStreamWaitEvent(s, c->req_ev, 0));
+    c->req_pending = false;
     ProfScope ps(1, stream);
     CK(launch_direct_step(c->dtype, c->d_descs + li, seq,
                           (flags & 7u) | (grad == r->gbuf ? EC_CF_SRC_GRAD_AUTO : 0u), w,

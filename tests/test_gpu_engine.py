@@ -617,10 +617,13 @@ def test_direct_refused_step_takes_the_out_of_line_path():
     world.close()
 
 
-def test_direct_zero_copy_folds_into_a_pending_stash():
+@pytest.mark.parametrize("other_stream", [False, True])
+def test_direct_zero_copy_folds_into_a_pending_stash(other_stream):
     """World of one: a zero-copy step that meets a pending (accepted, not yet
     reduced) stash folds the gradient into it inside the step kernel (no fold
-    launch): u = 0 + (stash + g), the same bits as fold-then-round."""
+    launch): u = 0 + (stash + g), the same bits as fold-then-round.  With
+    other_stream the offer is posted from another stream than the step's (the
+    step is ordered behind it, so its publication has nothing to wait for)."""
     from paper_1908_04207_b200 import finish_step, train_step_async
     n, lr = 50_001, 0.25
     rng = np.random.default_rng(5)
@@ -629,7 +632,10 @@ def test_direct_zero_copy_folds_into_a_pending_stash():
     h = AllreduceHandle(CollectiveConfig(p=1, flavor="solo", vector_len=n, element="f4"), 0, world)
     st = TrainState.fresh(w0, lr, rank=0, tau=None)
     attach_delivery_tracking(h, st)
-    assert h._contribute(0, v, fresh=True, activate=False)   # stash holds v, round 0 open
+    side = torch.cuda.Stream()
+    torch.cuda.synchronize()
+    with torch.cuda.stream(side if other_stream else torch.cuda.current_stream()):
+        assert h._contribute(0, v, fresh=True, activate=False)   # stash holds v, round 0 open
     bucket = h.grad_buffer()
     bucket.copy_(torch.as_tensor(g, device="cuda"))
     pend = train_step_async(st, h, bucket, all_arrive=True)

@@ -5,8 +5,10 @@ rank r waits (3-r)*unit inside the call; a solo round is over before anyone
 else arrives (latency ~0, nap 1); a majority round closes when its designated
 initiator arrives: rank r waits max(0, init-r)*unit and nap = init+1.
 
-Real clocks replace the simulator's: unit = 3 ms and latencies are checked
-within a host-jitter tolerance; masks and naps exactly."""
+Real clocks replace the simulator's: unit = 3 ms; masks and naps are checked
+exactly for every round, latencies per rank as the median over its rounds
+within a host-jitter tolerance (host threads on a shared box occasionally
+oversleep by a few ms -- a single round's latency is not an oracle)."""
 
 import threading
 
@@ -48,18 +50,25 @@ def _run(flavor, rounds, p=4, seed=1234):
     return [b for r in range(p) for b in out[r]]
 
 
+def _median_error_per_rank(recs, expected):
+    out = {}
+    for r in sorted({b.rank for b in recs}):
+        out[r] = float(np.median([b.latency_us - expected(b) for b in recs if b.rank == r]))
+    return out
+
+
 def test_sync_latency_matches_the_arrival_math():
-    recs = _run("sync", rounds=4)
-    for b in recs:
-        assert b.nap == 4
-        assert abs(b.latency_us - (3 - b.rank) * UNIT_US) < TOL_US, b
+    recs = _run("sync", rounds=6)
+    assert all(b.nap == 4 for b in recs)
+    err = _median_error_per_rank(recs, lambda b: (3 - b.rank) * UNIT_US)
+    assert all(abs(e) < TOL_US for e in err.values()), err
 
 
 def test_solo_latency_is_near_zero_and_nap_one_under_strict_skew():
-    recs = _run("solo", rounds=4)
-    for b in recs:
-        assert b.nap == 1, b
-        assert b.latency_us < TOL_US, b
+    recs = _run("solo", rounds=6)
+    assert all(b.nap == 1 for b in recs)
+    err = _median_error_per_rank(recs, lambda b: 0)
+    assert all(e < TOL_US for e in err.values()), err
 
 
 def test_majority_latency_tracks_the_initiator():
@@ -68,7 +77,9 @@ def test_majority_latency_tracks_the_initiator():
         init = initiator_for_round(1234, b.round, 4)
         assert b.initiator == init
         assert b.nap == init + 1, b
-        assert abs(b.latency_us - max(0, init - b.rank) * UNIT_US) < TOL_US, b
+    err = _median_error_per_rank(
+        recs, lambda b: max(0, initiator_for_round(1234, b.round, 4) - b.rank) * UNIT_US)
+    assert all(abs(e) < TOL_US for e in err.values()), err
 
 
 def test_flavor_ordering_under_skew():
