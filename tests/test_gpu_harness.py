@@ -5,7 +5,8 @@ rank r waits (3-r)*unit inside the call; a solo round is over before anyone
 else arrives (latency ~0, nap 1); a majority round closes when its designated
 initiator arrives: rank r waits max(0, init-r)*unit and nap = init+1.
 
-Real clocks replace the simulator's: unit = 3 ms; masks and naps are checked
+Real clocks replace the simulator's: unit = 20 ms (a host thread on a shared
+box can oversleep by several ms, which must not reorder arrivals); masks and naps are checked
 exactly for every round, latencies per rank as the median over its rounds
 within a host-jitter tolerance (host threads on a shared box occasionally
 oversleep by a few ms -- a single round's latency is not an oracle)."""
@@ -22,8 +23,8 @@ from paper_1908_04207_b200.transport import DelayModel
 
 pytestmark = pytest.mark.gpu
 
-UNIT_US = 3000
-TOL_US = 1000
+UNIT_US = 20000
+TOL_US = 2000
 
 
 def _run(flavor, rounds, p=4, seed=1234):
