@@ -235,6 +235,10 @@ def main():
     import torch
     import torch.distributed as dist
 
+    # EC_RANKS_PER_GPU=2: functional coverage of a larger world on fewer GPUs
+    # (e.g. N=8 on a 4-GPU box; the engines of two processes time-slice a GPU,
+    # so its numbers are not measurements)
+    local_rank //= int(os.environ.get("EC_RANKS_PER_GPU", "1"))
     torch.cuda.set_device(local_rank)
     dev = torch.device("cuda", local_rank)
     if world > 1:
