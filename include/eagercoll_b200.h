@@ -220,7 +220,9 @@ int ec_step(ec_comm_t* c, int local_idx, int64_t t, const void* grad, int fold_m
  * post the offer, wait ON THE DEVICE for a generation >= t and pin it, update
  * from that slot, unpin.  The host reads the outcome later with
  * ec_step_result(seq, t); steps must be issued in order.  The device-side
- * wait occupies `stream`: ranks sharing one GPU need distinct streams. */
+ * wait occupies `stream`: ranks sharing one GPU need distinct streams.  Not
+ * capturable: under stream capture it returns EC_E_STATE (each step's launch
+ * arguments carry a fresh request sequence number). */
 int ec_step_async(ec_comm_t* c, int local_idx, int64_t t, const void* grad, uint32_t flags,
                   void* w, void* mom, double lr, double mu, void* stream, uint64_t* seq);
 /* The outcome of an ec_step_async step: what train_step returns

@@ -217,13 +217,6 @@ static int make_pub_stream(ec_comm_t* c, cudaStream_t* s, cudaEvent_t* ev) {
   return EC_OK;
 }
 
-// publications go to their own stream unless the caller captures a graph (the
-// side stream would leave the capture unjoined) or EC_PUBLISH_SAME_STREAM is set
-static bool pub_side_ok(cudaStream_t s) {
-  cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
-  if (cudaStreamIsCapturing(s, &cap) != cudaSuccess) return false;
-  return cap == cudaStreamCaptureStatusNone && !getenv("EC_PUBLISH_SAME_STREAM");
-}
 
 
 static int device_error(EcRankHost* r) {
@@ -1488,6 +1481,14 @@ int ec_step_async(ec_comm_t* c, int li, int64_t t, const void* grad, uint32_t fl
   if (c->dtype == EC_I64) return fail(EC_E_ARG, "eager-SGD step needs a float dtype");
   EcRankHost* r = c->L[li];
   cudaStream_t s = (cudaStream_t)stream;
+  {
+    // every step carries a fresh request sequence number and generation in
+    // its launch arguments: a captured graph would replay stale ones
+    cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
+    CK(cudaStreamIsCapturing(s, &cap));
+    if (cap != cudaStreamCaptureStatusNone)
+      return fail(EC_E_STATE, "ec_step_async cannot be captured into a CUDA graph");
+  }
   // reservation and launches under live_mu: the idle watcher never parks with
   // a reserved request outstanding
   std::lock_guard<std::recursive_mutex> live(c->live_mu);
@@ -1517,7 +1518,7 @@ int ec_step_async(ec_comm_t* c, int li, int64_t t, const void* grad, uint32_t fl
     // publication on the communicator's publication stream (not while the
     // caller captures a graph: then behind it, on the same stream)
     c->last_stream = stream;
-    const bool side = pub_side_ok(s);
+    const bool side = !getenv("EC_PUBLISH_SAME_STREAM");
     if (side && !c->pub_s && (rc = make_pub_stream(c, &c->pub_s, &c->pub_ev))) return rc;
     if (side) c->pub_used = true;
     if (c->req_pending && c->req_stream != s) CK(cudaStreamWaitEvent(s, c->req_ev, 0));

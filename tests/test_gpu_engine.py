@@ -617,6 +617,33 @@ def test_direct_refused_step_takes_the_out_of_line_path():
     world.close()
 
 
+@pytest.mark.filterwarnings("ignore:The CUDA Graph is empty")
+def test_async_step_refuses_graph_capture():
+    """ec_step_async under stream capture fails loudly (EC_E_STATE) instead of
+    baking one request sequence number into a graph that replays it; the
+    communicator stays usable afterwards."""
+    from paper_1908_04207_b200 import _lib, finish_step, train_step_async
+    n = 4099
+    world = EmulatedWorld(1)
+    h = AllreduceHandle(CollectiveConfig(p=1, flavor="solo", vector_len=n, element="f4"), 0, world)
+    st = TrainState.fresh(np.zeros(n, np.float32), 0.1, rank=0, tau=None)
+    bucket = h.grad_buffer()
+    bucket.fill_(1.0)
+    s = torch.cuda.Stream()
+    torch.cuda.synchronize()
+    graph = torch.cuda.CUDAGraph()
+    with pytest.raises(_lib.EcError):
+        with torch.cuda.graph(graph, stream=s):
+            train_step_async(st, h, bucket)
+    torch.cuda.synchronize()
+    st.t = 0
+    _, res, gen = finish_step(st, h, train_step_async(st, h, bucket))
+    torch.cuda.synchronize()
+    assert gen == 0 and res.nap == 1
+    assert float(st.w[0]) == np.float32(-0.1)
+    world.close()
+
+
 @pytest.mark.parametrize("other_stream", [False, True])
 def test_direct_zero_copy_folds_into_a_pending_stash(other_stream):
     """World of one: a zero-copy step that meets a pending (accepted, not yet
